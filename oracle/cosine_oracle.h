@@ -1,0 +1,109 @@
+/*
+ * cosine_oracle.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, fp64 CPU oracle for the batched verification step of CoSine
+ * (arXiv 2503.10325).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it.  It shares no code,
+ * header, table or helper with the CUDA path (paper_2503_10325_b200/csrc).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * "reading #n" = DESIGN.md §3 (the readings of the paper this oracle follows).
+ *
+ * All floating point inputs are fp64 copies of the (bf16 / fp32) values the
+ * GPU path receives; all arithmetic is fp64, sums are sequential in
+ * ascending vocabulary index.  No blocking, fusion or reordering.
+ */
+#ifndef COSINE_ORACLE_H
+#define COSINE_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Philox tags (reading #8). */
+enum { ORC_TAG_ACCEPT = 0, ORC_TAG_SAMPLE = 1, ORC_TAG_FUSE = 2, ORC_TAG_TREE_GEN = 3 };
+/* weight modes (reading #2) */
+enum { ORC_W_CONF = 0, ORC_W_WINNER = 1, ORC_W_UNIFORM = 2, ORC_W_POINT = 3 };
+/* select modes (Eq. 4 literal ARGMAX, or SAMPLE x* ~ fused q; reading #3) */
+enum { ORC_SEL_ARGMAX = 0, ORC_SEL_SAMPLE = 1 };
+/* draft kinds */
+enum { ORC_DRAFT_PROBS = 0, ORC_DRAFT_LOGITS = 1 };
+/* per-request status codes (low byte) and info flags */
+enum {
+  ORC_ST_OK = 0, ORC_ST_ZERO_PROB_DRAFT = 1, ORC_ST_TOKEN_OUT_OF_RANGE = 2,
+  ORC_ST_NONFINITE_OR_NEGATIVE = 3, ORC_ST_EMPTY_ROW = 4, ORC_ST_BAD_DRAFT_LEN = 5,
+  ORC_ST_BAD_TREE = 6,
+  ORC_INFO_DEGENERATE_RESIDUAL = 0x100
+};
+
+/* Philox4x32-10, one block: out[4] = philox(ctr[4], key[2]). */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* U(rid, node, tag) in [0, 1 - 2^-24] (reading #8, #9). */
+double orc_uniform(uint64_t seed, uint64_t request_id, uint32_t node, uint32_t step, uint32_t tag);
+
+/* Inverse CDF: smallest v with sum_{w'<=v} w > u * sum(w); if none, last v with w > 0;
+ * -1 if all weights are zero.  *margin (may be NULL) = distance of t to the chosen
+ * bin's edges divided by sum(w) (reading #10). */
+int64_t orc_invcdf(const double* w, int64_t V, double u, double* margin);
+
+/* Target softmax at temperature T > 0 (reading #1).
+ * Returns 0, or a status code (NONFINITE / EMPTY_ROW).  M = max_v l(v)/T, S = sum exp(l/T - M). */
+int orc_softmax(const double* l, int64_t V, double T, double* p, double* M, double* S);
+
+/* Residual norm(max(0, o - q)); returns 1 if degenerate (all zero), in which
+ * case r is left as the zero vector. */
+int orc_residual(const double* o, const double* q, int64_t V, double* r);
+
+/* Linear verification of a batch (§8(c) steps 1-7).  Returns 0 or 1 (invalid argument).
+ * Debug outputs may be NULL.  tie_margin[b] = smallest decision margin (see reading #18). */
+int orc_verify_batch(int32_t B, int32_t k, int32_t N, int64_t V,
+                     const double* target, double temperature,
+                     const double* draft, int32_t draft_kind,
+                     const int32_t* draft_tokens, const int32_t* draft_len,
+                     const uint64_t* request_ids, uint64_t seed, uint32_t step,
+                     int32_t weight_mode, int32_t select_mode,
+                     int32_t* accept_len, int32_t* out_tokens, int32_t* status,
+                     double* dbg_p_x, double* dbg_q_x, double* dbg_M, double* dbg_S,
+                     double* dbg_sigma, double* dbg_conf, double* dbg_w, int32_t* dbg_fused,
+                     double* dbg_u, double* dbg_Z, double* tie_margin);
+
+/* Fusion only (Eq. 4): fused tokens, weights, draft normalisers and
+ * (optionally) the fused q rows.  Returns 0 or 1. */
+int orc_fuse_drafts(int32_t B, int32_t k, int32_t N, int64_t V,
+                    const double* draft, int32_t draft_kind, double temperature,
+                    const int32_t* draft_tokens, const uint64_t* request_ids,
+                    uint64_t seed, uint32_t step, int32_t weight_mode, int32_t select_mode,
+                    int32_t* fused_tokens, double* weights, double* draft_norm,
+                    double* fused_q, int32_t* status, double* tie_margin);
+
+/* Residual / bonus sample for one row group per request.
+ * target [B][V] logits; row_max/row_sumexp NULL => recompute.  draft [B][N][V] PROBS or NULL
+ * (=> bonus from the target).  weights / draft_norm [B][N]. */
+int orc_sample_residual(int32_t B, int64_t V, const double* target, double temperature,
+                        const double* row_max, const double* row_sumexp,
+                        const double* draft, int32_t N, const double* weights,
+                        const double* draft_norm, const uint32_t* node_ids,
+                        const uint64_t* request_ids, uint64_t seed, uint32_t step,
+                        int32_t* out_token, int32_t* status, double* dbg_Z, double* tie_margin);
+
+/* Tree verification (reading #13).  One tree per request with J+1 nodes
+ * (node 0 = root = last verified token).  parent[B][J+1] (parent[0] = -1, parent[j] < j),
+ * node_token[B][J+1] (root token ignored), target [B][J+1][V] (row j = target distribution
+ * after the path to node j), internal_row[B][J+1] (row index into draft for nodes with
+ * children, -1 for leaves), draft [B][I][N][V], node_draft_tokens [B][I][N].
+ * accepted_nodes[B][J+1] = node ids of the accepted path (root excluded), -1 padded;
+ * out_tokens[B][J+1] = tokens of the accepted path then the final token, -1 padded. */
+int orc_verify_tree(int32_t B, int32_t J, int32_t I, int32_t N, int64_t V,
+                    const int32_t* parent, const int32_t* node_token, const int32_t* internal_row,
+                    const double* target, double temperature,
+                    const double* draft, int32_t draft_kind, const int32_t* node_draft_tokens,
+                    const uint64_t* request_ids, uint64_t seed, uint32_t step, int32_t weight_mode,
+                    int32_t* accept_len, int32_t* accepted_nodes, int32_t* out_tokens,
+                    int32_t* status, double* tie_margin);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

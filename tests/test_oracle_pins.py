@@ -1,0 +1,488 @@
+"""Pins of the fp64 CPU oracle against what the paper and the mathematics fix (no GPU).
+
+Every test cites the passage it checks.  A plausible mistake anywhere in the oracle
+(a dropped term, a wrong sign or index, a transposed operand, a wrong Philox
+constant or counter layout) fails at least one of them:
+
+* Philox / uniforms  — Random123 known-answer vectors (golden file), uniformity.
+* softmax            — scipy.special.softmax (library routine), masking / errors.
+* inverse CDF        — numpy.searchsorted over numpy.cumsum (library routine).
+* residual           — SPEC worked values S:72-74 and the invariant S:77.
+* fusion (Eq. 4)     — S:291-293 examples and the tie rule.
+* acceptance         — draft == target gives 100% acceptance; the closed form
+                       P(accept) = sum_v min(p, q) by Monte Carlo.
+* whole step         — exact rational enumeration (oracle/enum_check.py): the method
+                       emits the target conditional at every position (P:126-127,
+                       P:130-133); the oracle's realisations follow that exact law
+                       (chi-square) in every mode, including the biased paper-literal
+                       ARGMAX+CONF mode (reading #3).
+* greedy             — T = 0 equals the argmax decode (numpy.argmax).
+* tree               — a chain tree is bit-identical to the linear path;
+                       the tree walk realises the enumerated law, which equals o.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import scipy.special
+import scipy.stats
+
+import oracle
+from oracle import enum_check as ec
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------------------- Philox
+def test_philox_known_answer_vectors():
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt"))
+            if l.strip() and not l.startswith("#")]
+    assert len(rows) == 3
+    for r in rows:
+        v = [int(x, 16) for x in r]
+        out = oracle.philox4x32_10(v[0:4], v[4:6])
+        assert [int(x) for x in out] == v[6:10]
+
+
+def test_uniform_counter_layout_and_range():
+    # U = (x0 >> 8) * 2^-24 of ctr = {rid_lo, rid_hi, node, (step << 4) | tag}, key = seed
+    seed, rid, node, step, tag = 0x0123456789ABCDEF, 0xFEDCBA9876543210, 7, 3, 1
+    x = oracle.philox4x32_10([rid & 0xffffffff, rid >> 32, node, (step << 4) | tag],
+                             [seed & 0xffffffff, seed >> 32])
+    assert oracle.uniform(seed, rid, node, step, tag) == (int(x[0]) >> 8) / 2 ** 24
+    us = np.array([oracle.uniform(5, r, 1, 0, 0) for r in range(20000)])
+    assert us.min() >= 0.0 and us.max() <= 1.0 - 2 ** -24
+    counts, _ = np.histogram(us, bins=20, range=(0, 1))
+    assert scipy.stats.chisquare(counts).pvalue > 1e-4
+    # distinct tags / nodes / steps give independent streams
+    a = np.array([oracle.uniform(5, r, 1, 0, 0) for r in range(2000)])
+    b = np.array([oracle.uniform(5, r, 1, 0, 1) for r in range(2000)])
+    assert abs(np.corrcoef(a, b)[0, 1]) < 0.1
+
+
+# --------------------------------------------------------------------------- softmax
+@pytest.mark.parametrize("T", [1.0, 0.5, 2.0])
+def test_softmax_matches_scipy(T):
+    rng = np.random.default_rng(1)
+    l = rng.normal(size=1000) * 5
+    st, p, M, S = oracle.softmax(l, T)
+    assert st == 0
+    ref = scipy.special.softmax(l / T)
+    np.testing.assert_allclose(p, ref, rtol=1e-12, atol=1e-300)
+    assert M == pytest.approx((l / T).max(), rel=0, abs=0)
+    assert S == pytest.approx(np.exp(l / T - M).sum(), rel=1e-13)
+
+
+def test_softmax_masking_and_errors():
+    st, p, _, _ = oracle.softmax([0.0, -np.inf, 0.0], 1.0)
+    assert st == 0 and p.tolist() == [0.5, 0.0, 0.5]
+    assert oracle.softmax([0.0, np.nan], 1.0)[0] == oracle.ST_NONFINITE
+    assert oracle.softmax([0.0, np.inf], 1.0)[0] == oracle.ST_NONFINITE
+    assert oracle.softmax([-np.inf, -np.inf], 1.0)[0] == oracle.ST_EMPTY
+
+
+# --------------------------------------------------------------------------- inverse CDF
+def test_invcdf_matches_searchsorted():
+    rng = np.random.default_rng(2)
+    for _ in range(300):
+        V = int(rng.integers(1, 40))
+        w = rng.random(V) * (rng.random(V) < 0.7)
+        if w.sum() == 0:
+            w[int(rng.integers(0, V))] = 1.0
+        u = float(rng.random())
+        c = np.cumsum(w)
+        ref = int(np.searchsorted(c, u * c[-1], side="right"))  # smallest v with C(v) > t
+        assert oracle.invcdf(w, u) == ref
+    assert oracle.invcdf([0.0, 0.0], 0.3) == -1
+    assert oracle.invcdf([0.0, 1.0, 0.0], 0.0) == 1  # zero-weight bins are never drawn
+
+
+# --------------------------------------------------------------------------- residual
+def test_residual_spec_examples():
+    g = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))
+    for ex in g["residual"]:
+        deg, r = oracle.residual(ex["o"], ex["q"])
+        if ex.get("degenerate"):
+            assert deg
+        else:
+            assert not deg
+            np.testing.assert_allclose(r, ex["r"], atol=1e-15)
+
+
+def test_residual_invariant():
+    # sums to 1 when non-degenerate and is 0 wherever q >= o
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        V = int(rng.integers(2, 30))
+        o, q = rng.random(V), rng.random(V)
+        o, q = o / o.sum(), q / q.sum()
+        deg, r = oracle.residual(o, q)
+        assert not deg
+        assert abs(r.sum() - 1) < 1e-12
+        assert np.all(r[q >= o] == 0) and np.all(r[q < o] > 0)
+
+
+# --------------------------------------------------------------------------- fusion
+def _rows_with_conf(conf, V=2):
+    """Drafter n's row puts probability conf[n] on token 0 (its own token) and the rest on 1."""
+    N = len(conf)
+    d = np.zeros((1, 1, N, V))
+    for n, c in enumerate(conf):
+        d[0, 0, n, 0] = c
+        d[0, 0, n, 1] = 1 - c
+    return d
+
+
+def test_fusion_spec_examples():
+    g = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))
+    for ex in g["fuse"]:
+        conf = ex["conf"]
+        N = len(conf)
+        d = _rows_with_conf(conf, V=2 + N)
+        # each drafter's own token: 0 for all, but make them distinguishable by moving drafter n's
+        # confident mass to token n (same confidence, distinct tokens)
+        d2 = np.zeros_like(d)
+        for n in range(N):
+            d2[0, 0, n, n] = d[0, 0, n, 0]
+            d2[0, 0, n, N] = d[0, 0, n, 1]
+        X = np.arange(N, dtype=np.int32).reshape(1, 1, N)
+        for wm in (oracle.W_CONF, oracle.W_WINNER, oracle.W_UNIFORM, oracle.W_POINT):
+            r = oracle.fuse_drafts(d2, X, [0], weight_mode=wm)
+            assert r["status"][0] == 0
+            assert r["fused_tokens"][0, 0] == ex["expect_node"]  # Eq. 4 argmax, ties -> lowest n
+        r = oracle.fuse_drafts(d2, X, [0], weight_mode=oracle.W_CONF, want_q=True)
+        c = np.array(conf)
+        np.testing.assert_allclose(r["weights"][0, 0], c / c.sum(), rtol=1e-14)
+        np.testing.assert_allclose(r["draft_norm"][0, 0], np.ones(N), rtol=1e-14)
+        # fused q = sum_n w_n q_n (reading #2)
+        np.testing.assert_allclose(r["fused_q"][0, 0], (c / c.sum()) @ d2[0, 0], rtol=1e-13)
+
+
+def test_fusion_renormalises_bf16_rows():
+    # reading #6: a drafter row that does not sum to 1 is renormalised by its sum
+    d = np.array([[[[0.2, 0.2, 0.1]]]])  # sums to 0.5
+    r = oracle.fuse_drafts(d, np.array([[[1]]], np.int32), [0], want_q=True)
+    assert r["draft_norm"][0, 0, 0] == pytest.approx(0.5)
+    np.testing.assert_allclose(r["fused_q"][0, 0], [0.4, 0.4, 0.2], rtol=1e-14)
+
+
+# --------------------------------------------------------------------------- acceptance pins
+def test_draft_equals_target_accepts_everything():
+    # q = o  =>  min(1, o/q) = 1; with identical logits rows (N = 1, LOGITS)
+    rng = np.random.default_rng(4)
+    B, k, V = 64, 6, 300
+    t = rng.normal(size=(B, k + 1, V)) * 5
+    d = t[:, :k, None, :].copy()
+    X = np.zeros((B, k, 1), np.int32)
+    for b in range(B):
+        for i in range(k):
+            p = scipy.special.softmax(t[b, i])
+            X[b, i, 0] = rng.choice(V, p=p)
+    for T in (1.0, 0.7):
+        r = oracle.verify_batch(t, d, X, np.arange(B), temperature=T, draft_kind=oracle.DRAFT_LOGITS)
+        assert (r["status"] == 0).all()
+        assert (r["accept_len"] == k).all()
+        np.testing.assert_array_equal(r["out_tokens"][:, :k], X[:, :, 0])
+
+
+def _mc_bound(p, n):
+    return 4.5 * math.sqrt(p * (1 - p) / n) + 1e-9
+
+
+@pytest.mark.parametrize("N,wm", [(1, oracle.W_CONF), (3, oracle.W_UNIFORM)])
+def test_closed_form_acceptance_rate(N, wm):
+    # x ~ q (SAMPLE) accepted w.p. min(1, p/q)  =>  P(accept) = sum_v min(p(v), q(v))
+    rng = np.random.default_rng(5 + N)
+    V, n = 12, 40000
+    l = rng.normal(size=V) * 1.5
+    p = scipy.special.softmax(l)
+    qs = rng.dirichlet(np.ones(V), size=N)
+    q = qs.mean(0)
+    t = np.broadcast_to(np.stack([l, l]), (n, 2, V)).copy()
+    d = np.broadcast_to(qs[None, None], (n, 1, N, V)).copy()
+    X = np.zeros((n, 1, N), np.int32)  # own tokens only enter the (unused) CONF weights
+    for m in range(N):
+        X[:, 0, m] = int(np.argmax(qs[m]))
+    r = oracle.verify_batch(t, d, X, np.arange(n), seed=11, weight_mode=wm,
+                            select_mode=oracle.SEL_SAMPLE)
+    rate = (r["accept_len"] >= 1).mean()
+    expect = np.minimum(p, q).sum()
+    assert abs(rate - expect) < _mc_bound(expect, n)
+
+
+def test_ab_example():
+    # o = (.5, .5), q = (1, 0), draft a: accept w.p. 0.5; the emitted token is o-distributed
+    g = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))["ab_example"]
+    n = 40000
+    t = np.log(np.broadcast_to(np.array(g["o"]), (n, 2, 2)))
+    d = np.broadcast_to(np.array(g["q"]), (n, 1, 1, 2)).copy()
+    X = np.zeros((n, 1, 1), np.int32)
+    r = oracle.verify_batch(t, d, X, np.arange(n), seed=3)
+    acc = (r["accept_len"] == 1).mean()
+    assert abs(acc - g["accept_prob"]) < _mc_bound(0.5, n)
+    first = r["out_tokens"][:, 0]
+    assert abs((first == 0).mean() - g["marginal"][0]) < _mc_bound(0.5, n)
+    assert (first[r["accept_len"] == 0] == 1).all()  # residual of (.5,.5)-(1,0) is (0,1)
+
+
+# --------------------------------------------------------------------------- greedy
+def test_greedy_is_argmax_decode():
+    rng = np.random.default_rng(6)
+    B, k, N, V = 50, 5, 3, 40
+    t = np.round(rng.normal(size=(B, k + 1, V)) * 2)  # many exact ties: lowest index wins
+    d = rng.dirichlet(np.ones(V), size=(B, k, N))
+    X = rng.integers(0, V, (B, k, N)).astype(np.int32)
+    # make every drafter token carry some mass
+    for b in range(B):
+        for i in range(k):
+            for n in range(N):
+                d[b, i, n, X[b, i, n]] += 0.1
+    r = oracle.verify_batch(t, d, X, np.arange(B), temperature=0.0)
+    am = np.argmax(t, axis=-1)
+    for b in range(B):
+        xs = r["fused_tokens"][b]
+        L = next((i for i in range(k) if xs[i] != am[b, i]), k)
+        assert r["accept_len"][b] == L
+        assert list(r["out_tokens"][b, :L]) == list(xs[:L])
+        assert r["out_tokens"][b, L] == am[b, L]
+
+
+# --------------------------------------------------------------------------- exact enumeration
+def _models(seed, V, depth, context_free=False):
+    rng = np.random.default_rng(seed)
+    if context_free:
+        tabs = [ec.random_dist(rng, V) for _ in range(depth + 2)]
+        return lambda prefix: tabs[len(prefix)]
+    return ec.random_tabular_model(rng, V, depth)
+
+
+EXACT_MODES = [(ec.W_CONF, ec.SEL_SAMPLE), (ec.W_WINNER, ec.SEL_SAMPLE),
+               (ec.W_UNIFORM, ec.SEL_SAMPLE), (ec.W_POINT, ec.SEL_ARGMAX)]
+
+
+@pytest.mark.parametrize("wm,sm", EXACT_MODES)
+def test_enumeration_method_preserves_target(wm, sm):
+    # P:126-127 / P:130-133: every emitted token ~ o(. | prefix), exactly
+    for seed in range(6):
+        V, gamma = 3, 2
+        target = _models(100 + seed, V, gamma + 1)
+        drafters = [_models(200 + seed * 7 + n, V, gamma + 1) for n in range(2)]
+        law = ec.linear_law(target, drafters, gamma, wm, sm)
+        assert sum(law.values()) == 1
+        assert ec.max_tvd_to_target(law, target, V, gamma + 1) == 0
+
+
+def test_enumeration_argmax_conf_is_biased():
+    # reading #3: the paper-literal Eq. 4 argmax with a mixture q is not distribution exact
+    worst = Fraction(0)
+    for seed in range(10):
+        V = 4
+        target = _models(300 + seed, V, 2)
+        drafters = [_models(400 + seed * 7 + n, V, 2) for n in range(2)]
+        law = ec.linear_law(target, drafters, 1, ec.W_CONF, ec.SEL_ARGMAX)
+        worst = max(worst, ec.max_tvd_to_target(law, target, V, 1))
+    assert worst > Fraction(1, 100)
+
+
+def _sample_linear_case(rng, target, drafters, k, n_req, V, wm):
+    """Inputs along the fused path: X_n ~ q_n(. | prefix) and (ARGMAX) x* = Eq. 4's argmax."""
+    N = len(drafters)
+    t = np.zeros((n_req, k + 1, V))
+    d = np.zeros((n_req, k, N, V))
+    X = np.zeros((n_req, k, N), np.int32)
+    for b in range(n_req):
+        prefix = ()
+        for i in range(k):
+            t[b, i] = np.log(np.array([float(x) for x in target(prefix)]) + 1e-300)
+            qs = [np.array([float(x) for x in dm(prefix)]) for dm in drafters]
+            for n in range(N):
+                d[b, i, n] = qs[n]
+                X[b, i, n] = rng.choice(V, p=qs[n] / qs[n].sum())
+            c = [qs[n][X[b, i, n]] for n in range(N)]
+            nstar = int(np.argmax(c))
+            prefix = prefix + (int(X[b, i, nstar]),)
+        t[b, k] = np.log(np.array([float(x) for x in target(prefix)]) + 1e-300)
+    return t, d, X
+
+
+def _chi2_law(counts, law, n):
+    keys = sorted(law)
+    exp = np.array([float(law[k2]) * n for k2 in keys])
+    obs = np.array([counts.get(k2, 0) for k2 in keys], dtype=float)
+    assert sum(counts.get(k2, 0) for k2 in keys) == sum(counts.values()), "impossible outcome"
+    small = exp < 5
+    if small.any():
+        exp = np.append(exp[~small], exp[small].sum())
+        obs = np.append(obs[~small], obs[small].sum())
+    return scipy.stats.chisquare(obs, exp).pvalue
+
+
+@pytest.mark.parametrize("wm,sm,ctx_free", [
+    (ec.W_CONF, ec.SEL_ARGMAX, False),   # paper-literal (biased) mode
+    (ec.W_POINT, ec.SEL_ARGMAX, False),
+    (ec.W_CONF, ec.SEL_SAMPLE, True),
+    (ec.W_UNIFORM, ec.SEL_SAMPLE, True),
+])
+def test_oracle_realises_enumerated_law(wm, sm, ctx_free):
+    V, k, n = 3, 2, 30000
+    target = _models(500, V, k + 1, ctx_free)
+    drafters = [_models(600 + j, V, k + 1, ctx_free) for j in range(2)]
+    law = ec.linear_law(target, drafters, k, wm, sm)
+    rng = np.random.default_rng(7)
+    t, d, X = _sample_linear_case(rng, target, drafters, k, n, V, wm)
+    r = oracle.verify_batch(t, d, X, np.arange(n), seed=123, weight_mode=wm, select_mode=sm)
+    assert (r["status"] == 0).all()
+    counts = {}
+    for b in range(n):
+        seq = tuple(int(x) for x in r["out_tokens"][b, : r["accept_len"][b] + 1])
+        counts[seq] = counts.get(seq, 0) + 1
+    assert _chi2_law(counts, law, n) > 1e-4
+
+
+# --------------------------------------------------------------------------- errors
+def test_error_statuses_and_isolation():
+    rng = np.random.default_rng(8)
+    B, k, N, V = 7, 3, 2, 20
+    t = rng.normal(size=(B, k + 1, V))
+    d = rng.dirichlet(np.ones(V), size=(B, k, N))
+    X = rng.integers(0, V, (B, k, N)).astype(np.int32)
+    dl = np.full(B, k, np.int32)
+    d[1, 0, 1, X[1, 0, 1]] = 0.0                 # zero-probability own token
+    X[2, 1, 0] = V                               # token out of range
+    t[3, 2, 5] = np.nan                          # non-finite logit
+    d[4, 1, 0, 3] = -0.1                         # negative probability
+    t[5, 0, :] = -np.inf                         # empty row
+    dl[6] = 0                                    # bad gamma
+    r = oracle.verify_batch(t, d, X, np.arange(B), draft_len=dl)
+    assert list(r["status"]) == [0, oracle.ST_ZERO_PROB, oracle.ST_TOKEN_RANGE, oracle.ST_NONFINITE,
+                                 oracle.ST_NONFINITE, oracle.ST_EMPTY, oracle.ST_BAD_LEN]
+    assert r["accept_len"][0] >= 0 and (r["accept_len"][1:] == -1).all()
+    assert (r["out_tokens"][1:] == -1).all()
+
+
+def test_rows_past_draft_len_are_ignored():
+    rng = np.random.default_rng(9)
+    B, k, N, V = 4, 4, 2, 30
+    t = rng.normal(size=(B, k + 1, V))
+    d = rng.dirichlet(np.ones(V), size=(B, k, N))
+    X = rng.integers(0, V, (B, k, N)).astype(np.int32)
+    dl = np.array([1, 2, 3, 4], np.int32)
+    r1 = oracle.verify_batch(t, d, X, np.arange(B), draft_len=dl, seed=4)
+    for b in range(B):
+        t[b, dl[b] + 1:] = np.nan
+        d[b, dl[b]:] = np.nan
+    r2 = oracle.verify_batch(t, d, X, np.arange(B), draft_len=dl, seed=4)
+    np.testing.assert_array_equal(r1["out_tokens"], r2["out_tokens"])
+    assert (r2["status"] == 0).all() and (r2["accept_len"] <= dl).all()
+
+
+def test_result_independent_of_batch_order():
+    # reading #8: Philox keyed by global request id
+    rng = np.random.default_rng(10)
+    B, k, N, V = 6, 3, 2, 25
+    t = rng.normal(size=(B, k + 1, V)) * 3
+    d = rng.dirichlet(np.ones(V), size=(B, k, N))
+    X = rng.integers(0, V, (B, k, N)).astype(np.int32)
+    rid = np.arange(100, 100 + B)
+    r1 = oracle.verify_batch(t, d, X, rid, seed=9)
+    perm = rng.permutation(B)
+    r2 = oracle.verify_batch(t[perm], d[perm], X[perm], rid[perm], seed=9)
+    np.testing.assert_array_equal(r1["out_tokens"][perm], r2["out_tokens"])
+
+
+# --------------------------------------------------------------------------- sample_residual
+def test_sample_residual_matches_verify_path():
+    rng = np.random.default_rng(12)
+    B, k, N, V = 40, 3, 2, 60
+    t = rng.normal(size=(B, k + 1, V)) * 3
+    d = rng.dirichlet(np.ones(V) * 0.5, size=(B, k, N))
+    X = np.zeros((B, k, N), np.int32)
+    for b in range(B):
+        for i in range(k):
+            for n in range(N):
+                X[b, i, n] = rng.choice(V, p=d[b, i, n])
+    r = oracle.verify_batch(t, d, X, np.arange(B), seed=5)
+    L = r["accept_len"]
+    rows = t[np.arange(B), L]
+    has_rej = L < k
+    Lc = np.minimum(L, k - 1)
+    s = oracle.sample_residual(rows[has_rej], L[has_rej].astype(np.uint32), np.arange(B)[has_rej],
+                               seed=5, draft=d[np.arange(B), Lc][has_rej],
+                               weights=r["weights"][np.arange(B), Lc][has_rej],
+                               draft_norm=r["sigma"][np.arange(B), Lc][has_rej])
+    np.testing.assert_array_equal(s["out_token"], r["out_tokens"][has_rej, L[has_rej]])
+    sb = oracle.sample_residual(rows[~has_rej], L[~has_rej].astype(np.uint32), np.arange(B)[~has_rej],
+                                seed=5)
+    np.testing.assert_array_equal(sb["out_token"], r["out_tokens"][~has_rej, k])
+
+
+# --------------------------------------------------------------------------- tree
+def test_chain_tree_equals_linear():
+    # a chain tree is the linear path, bit for bit under the same Philox stream
+    rng = np.random.default_rng(13)
+    B, k, N, V = 30, 4, 2, 50
+    t = rng.normal(size=(B, k + 1, V)) * 3
+    d = rng.dirichlet(np.ones(V) * 0.3, size=(B, k, N))
+    X = np.zeros((B, k, N), np.int32)
+    for b in range(B):
+        for i in range(k):
+            for n in range(N):
+                X[b, i, n] = rng.choice(V, p=d[b, i, n])
+    r = oracle.verify_batch(t, d, X, np.arange(B), seed=21)
+    nn = k + 1
+    parent = np.tile(np.arange(-1, k, dtype=np.int32), (B, 1))
+    tok = np.zeros((B, nn), np.int32)
+    tok[:, 1:] = r["fused_tokens"]
+    irow = np.tile(np.array(list(range(k)) + [-1], np.int32), (B, 1))
+    rt = oracle.verify_tree(parent, tok, irow, t, d, X, np.arange(B), seed=21)
+    np.testing.assert_array_equal(rt["accept_len"], r["accept_len"])
+    np.testing.assert_array_equal(rt["out_tokens"], r["out_tokens"])
+
+
+def test_tree_enumeration_exact_and_realised():
+    V, n = 3, 30000
+    fan = (2, 1)
+    target = _models(700, V, 3)
+    drafters = [_models(800 + j, V, 3) for j in range(2)]
+    law = ec.tree_law(target, drafters, fan, ec.W_CONF)
+    assert sum(law.values()) == 1
+    assert ec.max_tvd_to_target(law, target, V, len(fan) + 1) == 0  # reading #13 is exact
+    # realisations: children drawn without replacement from the fused q (test-side)
+    rng = np.random.default_rng(14)
+    nn, I, N = 5, 3, 2
+    parent = np.tile(np.array([-1, 0, 0, 1, 2], np.int32), (n, 1))
+    irow = np.tile(np.array([0, 1, 2, -1, -1], np.int32), (n, 1))
+    tok = np.zeros((n, nn), np.int32)
+    t = np.zeros((n, nn, V))
+    d = np.zeros((n, I, N, V))
+    Xn = np.zeros((n, I, N), np.int32)
+
+    def node(b, j, prefix, row, m):
+        t[b, j] = np.log(np.array([float(x) for x in target(prefix)]))
+        qs = [np.array([float(x) for x in dm(prefix)]) for dm in drafters]
+        for q_i in range(N):
+            d[b, row, q_i] = qs[q_i]
+            Xn[b, row, q_i] = rng.choice(V, p=qs[q_i])
+        c = np.array([qs[q_i][Xn[b, row, q_i]] for q_i in range(N)])
+        w = c / c.sum()
+        qm = w @ np.stack(qs)
+        return list(rng.choice(V, size=m, replace=False, p=qm)) if m else []
+
+    for b in range(n):
+        kids = node(b, 0, (), 0, 2)
+        tok[b, 1], tok[b, 2] = kids
+        g1 = node(b, 1, (kids[0],), 1, 1)
+        g2 = node(b, 2, (kids[1],), 2, 1)
+        tok[b, 3], tok[b, 4] = g1[0], g2[0]
+        t[b, 3] = np.log(np.array([float(x) for x in target((kids[0], g1[0]))]))
+        t[b, 4] = np.log(np.array([float(x) for x in target((kids[1], g2[0]))]))
+    rt = oracle.verify_tree(parent, tok, irow, t, d, Xn, np.arange(n), seed=99)
+    assert (rt["status"] == 0).all()
+    counts = {}
+    for b in range(n):
+        seq = tuple(int(x) for x in rt["out_tokens"][b, : rt["accept_len"][b] + 1])
+        counts[seq] = counts.get(seq, 0) + 1
+    assert _chi2_law(counts, law, n) > 1e-4
