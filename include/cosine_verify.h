@@ -1,0 +1,185 @@
+/*
+ * cosine_verify.h — C ABI of the B200-native CoSine verification library
+ * (libcosine_verify.so, sm_100a).
+ *
+ * What it computes: the batched parallel verification step of CoSine
+ * (arXiv 2503.10325), Alg. 2 "foreach draft t in T in parallel: (V_t, R_t) <- Verify(t)"
+ * (PAPER.md P:463-464), applied to drafts merged by the confidence-based token
+ * fusion of Alg. 1 / Eq. 4:
+ *   - target distribution o_i = softmax(l_i / T) over the full vocabulary;
+ *   - per-drafter confidence c_{n,i} = q_{n,i}(X_{n,i}) and the fused token
+ *     x*_i = X_{n*,i}, n* = argmax_n c_{n,i} (Eq. 4), fused distribution q_i (reading #2);
+ *   - acceptance u < min(1, o_i(x*)/q_i(x*)) with counter-based Philox uniforms;
+ *   - first-rejection truncation, residual resample from norm(max(0, o - q))
+ *     or the bonus token x_{gamma+1} ~ o.
+ * "reading #n" refers to DESIGN.md §3, where every place the paper is silent or
+ * ambiguous is resolved.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", never throws; every call returns a cosine_status_t.
+ *   - Device pointers unless stated otherwise.  The caller owns every I/O buffer;
+ *     rows are row-major with the vocabulary innermost.  Row bases and the leading
+ *     dimensions (ld * sizeof(element)) must be multiples of 16 bytes, else
+ *     COSINE_ERR_UNSUPPORTED.  ld >= the context's vocabulary width.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered and asynchronous.  Host-side argument errors return
+ *     synchronously and enqueue nothing.
+ *   - Device-detected data errors are reported per request in status[b]; that request's
+ *     accept_len is -1 and its out_tokens row is all -1; other requests are unaffected.
+ *   - The context owns scratch memory (sized at init from the max_* fields).  One context
+ *     may be used by one host thread / one stream at a time.
+ *   - Randomness: U(rid, node, tag) = (Philox4x32-10(ctr = {rid_lo, rid_hi, node,
+ *     (step << 4) | tag}, key = {seed_lo, seed_hi}).x0 >> 8) * 2^-24 (readings #8, #9).
+ *     Tags: ACCEPT = 0, SAMPLE = 1, FUSE = 2.  Results depend only on global request ids,
+ *     never on batch order or on how requests are sharded across GPUs.
+ */
+#ifndef COSINE_VERIFY_H
+#define COSINE_VERIFY_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cosine_ctx_s* cosine_ctx_t;
+typedef void* cosine_stream_t; /* a cudaStream_t */
+
+typedef enum {
+  COSINE_OK = 0,
+  COSINE_ERR_INVALID_ARGUMENT = 1, /* bad shape, mode, NULL pointer, out-of-range size */
+  COSINE_ERR_UNSUPPORTED = 2,      /* dtype / alignment / mode combination not supported */
+  COSINE_ERR_CUDA = 3,             /* a CUDA runtime call failed (see cosine_last_error) */
+  COSINE_ERR_NCCL = 4,
+  COSINE_ERR_OUT_OF_MEMORY = 5
+} cosine_status_t;
+
+/* Per-request status codes written to status[b] (low byte) plus info flags. */
+#define COSINE_REQ_OK 0
+#define COSINE_REQ_ZERO_PROB_DRAFT 1      /* a drafter's own token has q = 0          */
+#define COSINE_REQ_TOKEN_OUT_OF_RANGE 2   /* draft token outside [0, V)                */
+#define COSINE_REQ_NONFINITE_INPUT 3      /* NaN / +inf logit; NaN, inf or negative prob      */
+#define COSINE_REQ_EMPTY_ROW 4            /* all -inf logits, or a probability row summing to 0 */
+#define COSINE_REQ_BAD_DRAFT_LEN 5        /* draft_len[b] outside [1, k]                      */
+#define COSINE_INFO_DEGENERATE_RESIDUAL 0x100 /* Z == 0: resampled from o (reading #11) */
+#define COSINE_INFO_NEAR_TIE 0x200        /* a decision margin < 1e-6 (reading #18)          */
+
+typedef enum { COSINE_BF16 = 0, COSINE_F32 = 1 } cosine_dtype_t;
+/* Drafter rows: probabilities (renormalised by their sum, reading #6) or logits (softmax at the
+ * call's temperature). */
+typedef enum { COSINE_DRAFT_PROBS = 0, COSINE_DRAFT_LOGITS = 1 } cosine_draft_kind_t;
+/* Fused distribution q_i = sum_n w_n q_{n,i} (reading #2): CONF w_n = c_n / sum c (default),
+ * WINNER w = e_{n*}, UNIFORM w = 1/N, POINT q = delta_{x*}. */
+typedef enum { COSINE_W_CONF = 0, COSINE_W_WINNER = 1, COSINE_W_UNIFORM = 2, COSINE_W_POINT = 3 } cosine_weight_mode_t;
+/* Fused token: Eq. 4's argmax (paper-literal) or a draw x* ~ q_i with U(rid, i+1, FUSE)
+ * (distribution-exact; reading #3). */
+typedef enum { COSINE_SEL_ARGMAX = 0, COSINE_SEL_SAMPLE = 1 } cosine_select_mode_t;
+
+typedef struct {
+  int32_t device;          /* CUDA device ordinal the context lives on                      */
+  int64_t vocab_size;      /* global V                                                       */
+  int64_t vocab_begin;     /* this rank's shard [vocab_begin, vocab_end); [0, V) unsharded    */
+  int64_t vocab_end;
+  int32_t max_batch;       /* largest B of any call                                          */
+  int32_t max_draft_len;   /* largest k                                                      */
+  int32_t max_drafters;    /* largest N (<= 8)                                               */
+  int32_t max_tree_nodes;  /* reserved (tree verification), 0 if unused                      */
+  cosine_dtype_t target_dtype;
+  cosine_dtype_t draft_dtype;
+  cosine_draft_kind_t draft_kind;
+  uint64_t seed;           /* Philox key                                                     */
+  int32_t nranks;          /* 1 = unsharded (batch sharding = independent contexts)          */
+  int32_t rank;
+  const void* nccl_unique_id; /* reserved for vocab sharding (nranks > 1)                    */
+  int32_t cluster_size;    /* 0 = automatic; else 1, 2, 4 or 8 CTAs per (request, position)  */
+} cosine_config_t;
+
+/* Optional per-unit diagnostics of cosine_verify_batch (any member may be NULL). */
+typedef struct {
+  float* p_x;           /* [B][k]  o_i(x*_i)                                                 */
+  float* q_x;           /* [B][k]  q_i(x*_i)                                                 */
+  float* accept_u;      /* [B][k]  U(rid, i+1, ACCEPT)                                        */
+  float* row_max;       /* [B][k+1] M = max_v l(v) (raw logit; T = 0: the max)               */
+  float* row_sumexp;    /* [B][k+1] S = sum_v exp((l(v) - M) / T)  (T = 0: 0)                 */
+  float* draft_norm;    /* [B][k][N] sigma (PROBS: row sum; LOGITS: sum exp((d - max)/T))   */
+  float* conf;          /* [B][k][N] c_{n,i}                                                 */
+  float* weights;       /* [B][k][N] w_{n,i}                                                 */
+  int32_t* fused_tokens;/* [B][k]  x*_i                                                      */
+  float* residual_mass; /* [B] Z of the final sample in probability units (bonus: 1)         */
+  float* tie_margin;    /* [B] smallest decision margin the GPU saw for the realised path     */
+} cosine_debug_t;
+
+/* Create a context on cfg->device (allocates scratch).  *out = NULL on failure. */
+cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out);
+/* Free the context (synchronises its device).  NULL is a no-op. */
+cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx);
+/* Last error message of ctx (or of the calling thread's last failed init if ctx is NULL). */
+const char* cosine_last_error(cosine_ctx_t ctx);
+
+/*
+ * cosine_fuse_drafts — Eq. 4 token fusion only (Alg. 1 TokenFusion P:376-381).
+ *   draft        [B][k][N][ld_q] drafter rows (config draft_dtype / draft_kind)
+ *   draft_tokens [B][k][N] int32 X_{n,i};  request_ids [B] uint64 (global ids);  step
+ *   temperature  used only for COSINE_DRAFT_LOGITS (must be > 0 then)
+ * Outputs: fused_tokens [B][k] (x*_i), weights [B][k][N] (w_{n,i}), draft_norm [B][k][N]
+ *   (sigma), fused_q [B][k][ld_fq] fp32 q_i(v) for v < V (NULL = not materialised), status [B].
+ *   weights / draft_norm may be NULL.  A request with an error has all fused_tokens = -1.
+ */
+cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                   int32_t N, const void* draft, int64_t ld_q,
+                                   const int32_t* draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, float temperature,
+                                   cosine_weight_mode_t weight_mode, cosine_select_mode_t select_mode,
+                                   int32_t* fused_tokens, float* weights, float* draft_norm,
+                                   float* fused_q, int64_t ld_fq, int32_t* status);
+
+/*
+ * cosine_verify_batch — the whole verification step for B independent requests.
+ *   target_logits [B][k+1][ld_t]: row i is the target's next-token logits after the prefix and
+ *                 x*_0..x*_{i-1}; row gamma_b is the bonus row (reading #14).
+ *   temperature   T > 0 samples; T == 0 is greedy (lowest-index argmax, reading #7).
+ *   draft         [B][k][N][ld_q] drafter rows at the fused-path positions (Eq. 4).
+ *   draft_tokens  [B][k][N] int32;  draft_len [B] int32 gamma_b in [1, k] or NULL (= k) (Alg. 2
+ *                 AdaptiveSpeculation; reading #15).
+ *   request_ids   [B] uint64 global ids;  step = decoding step (Philox counter word).
+ * Outputs: accept_len [B] = L_b (-1 on a per-request error); out_tokens [B][k+1] = x*_0 ..
+ *   x*_{L-1}, y, then -1; status [B].  debug may be NULL.
+ * Rows after gamma_b are never read.  All rows 0..gamma_b are read and validated.
+ */
+cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                    int32_t N, const void* target_logits, int64_t ld_t,
+                                    float temperature, const void* draft, int64_t ld_q,
+                                    const int32_t* draft_tokens, const int32_t* draft_len,
+                                    const uint64_t* request_ids, uint32_t step,
+                                    cosine_weight_mode_t weight_mode,
+                                    cosine_select_mode_t select_mode, int32_t* accept_len,
+                                    int32_t* out_tokens, int32_t* status,
+                                    const cosine_debug_t* debug);
+
+/*
+ * cosine_sample_residual — the final-token sample of one row group per request,
+ * for callers that verify elsewhere.
+ *   target_rows [B][ld_t] logits of the row at L_b;  temperature (0 = argmax)
+ *   row_max, row_sumexp [B] fp32 M = max l and S = sum exp((l - M)/T), or both NULL (recompute)
+ *   draft_rows [B][N][ld_q] drafter PROBS rows at L_b, or NULL => bonus sample y ~ o
+ *   weights, draft_norm [B][N] fp32 w_n and sigma_n (e.g. from cosine_fuse_drafts)
+ *   node_ids [B] uint32 Philox node (= L_b);  request_ids [B];  step
+ * Output: out_token [B] y (-1 on error), status [B].
+ * y = smallest v with C(v) > U(rid, node, SAMPLE) * Z over r(v) = max(0, o(v) - q(v))
+ * (q = sum_n w_n d_n(v) / sigma_n) — or over o itself for the bonus and when Z == 0.
+ */
+cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B,
+                                       const void* target_rows, int64_t ld_t, float temperature,
+                                       const float* row_max, const float* row_sumexp,
+                                       const void* draft_rows, int64_t ld_q, const float* weights,
+                                       const float* draft_norm, int32_t N,
+                                       const uint32_t* node_ids, const uint64_t* request_ids,
+                                       uint32_t step, int32_t* out_token, int32_t* status);
+
+/* Number of kernels the last successful call on ctx enqueued (for launch accounting). */
+int32_t cosine_last_launch_count(cosine_ctx_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COSINE_VERIFY_H */

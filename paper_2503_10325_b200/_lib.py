@@ -1,0 +1,176 @@
+"""ctypes binding of libcosine_verify.so — argument marshalling only.
+
+Every function here has the name of the C entry point it calls
+(include/cosine_verify.h) and does nothing but turn torch tensors into device
+pointers / sizes and C status codes into exceptions.  Every step of the method
+runs in the CUDA kernels.  There is no CPU fallback: if the shared library is
+missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcosine_verify.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python paper_2503_10325_b200/build.py` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+BF16, F32 = 0, 1
+DRAFT_PROBS, DRAFT_LOGITS = 0, 1
+W_CONF, W_WINNER, W_UNIFORM, W_POINT = 0, 1, 2, 3
+SEL_ARGMAX, SEL_SAMPLE = 0, 1
+REQ_OK, REQ_ZERO_PROB, REQ_TOKEN_RANGE, REQ_NONFINITE, REQ_EMPTY, REQ_BAD_LEN = range(6)
+INFO_DEGENERATE, INFO_NEAR_TIE = 0x100, 0x200
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CUDA", 4: "NCCL", 5: "OUT_OF_MEMORY"}
+
+_P = ctypes.c_void_p
+_i32, _u32, _i64, _u64, _f32 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
+
+
+class cosine_config_t(ctypes.Structure):
+    _fields_ = [
+        ("device", _i32), ("vocab_size", _i64), ("vocab_begin", _i64), ("vocab_end", _i64),
+        ("max_batch", _i32), ("max_draft_len", _i32), ("max_drafters", _i32), ("max_tree_nodes", _i32),
+        ("target_dtype", ctypes.c_int), ("draft_dtype", ctypes.c_int), ("draft_kind", ctypes.c_int),
+        ("seed", _u64), ("nranks", _i32), ("rank", _i32), ("nccl_unique_id", _P),
+        ("cluster_size", _i32),
+    ]
+
+
+class cosine_debug_t(ctypes.Structure):
+    _fields_ = [(n, _P) for n in ("p_x", "q_x", "accept_u", "row_max", "row_sumexp", "draft_norm",
+                                  "conf", "weights", "fused_tokens", "residual_mass", "tie_margin")]
+
+
+_lib.cosine_verify_init.argtypes = [ctypes.POINTER(cosine_config_t), ctypes.POINTER(_P)]
+_lib.cosine_verify_init.restype = ctypes.c_int
+_lib.cosine_verify_destroy.argtypes = [_P]
+_lib.cosine_verify_destroy.restype = ctypes.c_int
+_lib.cosine_last_error.argtypes = [_P]
+_lib.cosine_last_error.restype = ctypes.c_char_p
+_lib.cosine_last_launch_count.argtypes = [_P]
+_lib.cosine_last_launch_count.restype = _i32
+_lib.cosine_fuse_drafts.argtypes = [_P, _P, _i32, _i32, _i32, _P, _i64, _P, _P, _u32, _f32,
+                                    ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _i64, _P]
+_lib.cosine_fuse_drafts.restype = ctypes.c_int
+_lib.cosine_verify_batch.argtypes = [_P, _P, _i32, _i32, _i32, _P, _i64, _f32, _P, _i64, _P, _P,
+                                     _P, _u32, ctypes.c_int, ctypes.c_int, _P, _P, _P,
+                                     ctypes.POINTER(cosine_debug_t)]
+_lib.cosine_verify_batch.restype = ctypes.c_int
+_lib.cosine_sample_residual.argtypes = [_P, _P, _i32, _P, _i64, _f32, _P, _P, _P, _i64, _P, _P,
+                                        _i32, _P, _P, _u32, _P, _P]
+_lib.cosine_sample_residual.restype = ctypes.c_int
+
+EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_error",
+                    "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
+                    "cosine_last_launch_count")
+
+
+class CosineError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream, device):
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(rc, ctx):
+    if rc != 0:
+        raise CosineError(rc, _lib.cosine_last_error(ctx).decode())
+
+
+_DT = {torch.bfloat16: BF16, torch.float32: F32}
+
+
+class Context:
+    """Opaque cosine_ctx_t handle (passed straight to the C functions)."""
+
+    def __init__(self, handle, cfg):
+        self._as_parameter_ = handle
+        self.cfg = cfg
+        self.device = cfg.device
+        self.vocab_size = cfg.vocab_size
+
+    def __repr__(self):
+        return f"Context(V={self.vocab_size}, device={self.device})"
+
+
+def cosine_verify_init(vocab_size: int, *, device: int = 0, max_batch: int, max_draft_len: int,
+                       max_drafters: int, target_dtype=torch.bfloat16, draft_dtype=torch.bfloat16,
+                       draft_kind: int = DRAFT_PROBS, seed: int = 0, cluster_size: int = 0):
+    """Create a context on `device`; returns a Context."""
+    cfg = cosine_config_t(device=device, vocab_size=vocab_size, vocab_begin=0, vocab_end=vocab_size,
+                          max_batch=max_batch, max_draft_len=max_draft_len, max_drafters=max_drafters,
+                          max_tree_nodes=0, target_dtype=_DT[target_dtype], draft_dtype=_DT[draft_dtype],
+                          draft_kind=draft_kind, seed=seed, nranks=1, rank=0, nccl_unique_id=None,
+                          cluster_size=cluster_size)
+    h = _P()
+    _check(_lib.cosine_verify_init(ctypes.byref(cfg), ctypes.byref(h)), None)
+    return Context(h, cfg)
+
+
+def cosine_verify_destroy(ctx) -> None:
+    _check(_lib.cosine_verify_destroy(ctx), None)
+
+
+def cosine_last_launch_count(ctx) -> int:
+    return int(_lib.cosine_last_launch_count(ctx))
+
+
+def cosine_fuse_drafts(ctx, draft, draft_tokens, request_ids, fused_tokens, status, *, step=0,
+                       temperature=1.0, weight_mode=W_CONF, select_mode=SEL_ARGMAX, weights=None,
+                       draft_norm=None, fused_q=None, stream=None):
+    B, k, N, ld_q = draft.shape
+    ld_fq = fused_q.shape[-1] if fused_q is not None else 0
+    rc = _lib.cosine_fuse_drafts(ctx, _stream(stream, draft.device), B, k, N, _ptr(draft), ld_q,
+                                 _ptr(draft_tokens), _ptr(request_ids), step, temperature,
+                                 weight_mode, select_mode, _ptr(fused_tokens), _ptr(weights),
+                                 _ptr(draft_norm), _ptr(fused_q), ld_fq, _ptr(status))
+    _check(rc, ctx)
+
+
+def cosine_verify_batch(ctx, target_logits, draft, draft_tokens, request_ids, accept_len, out_tokens,
+                        status, *, temperature=1.0, draft_len=None, step=0, weight_mode=W_CONF,
+                        select_mode=SEL_ARGMAX, debug=None, stream=None):
+    """target_logits [B][k+1][ld_t], draft [B][k][N][ld_q] (contiguous, on the ctx's device)."""
+    B, kp1, ld_t = target_logits.shape
+    N, ld_q = draft.shape[2], draft.shape[3]
+    dbg = None
+    if debug is not None:
+        dbg = cosine_debug_t(**{f: _ptr(debug.get(f)) for f, _ in cosine_debug_t._fields_})
+    rc = _lib.cosine_verify_batch(ctx, _stream(stream, target_logits.device), B, kp1 - 1, N,
+                                  _ptr(target_logits), ld_t, temperature, _ptr(draft), ld_q,
+                                  _ptr(draft_tokens), _ptr(draft_len), _ptr(request_ids), step,
+                                  weight_mode, select_mode, _ptr(accept_len), _ptr(out_tokens),
+                                  _ptr(status), ctypes.byref(dbg) if dbg is not None else None)
+    _check(rc, ctx)
+
+
+def cosine_sample_residual(ctx, target_rows, node_ids, request_ids, out_token, status, *,
+                           temperature=1.0, row_max=None, row_sumexp=None, draft_rows=None,
+                           weights=None, draft_norm=None, step=0, stream=None):
+    B, ld_t = target_rows.shape
+    N = draft_rows.shape[1] if draft_rows is not None else 0
+    ld_q = draft_rows.shape[2] if draft_rows is not None else 0
+    rc = _lib.cosine_sample_residual(ctx, _stream(stream, target_rows.device), B, _ptr(target_rows),
+                                     ld_t, temperature, _ptr(row_max), _ptr(row_sumexp),
+                                     _ptr(draft_rows), ld_q, _ptr(weights), _ptr(draft_norm), N,
+                                     _ptr(node_ids), _ptr(request_ids), step, _ptr(out_token),
+                                     _ptr(status))
+    _check(rc, ctx)
