@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark of the batched verification step (CoSine, arXiv 2503.10325) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+
+One "step" = one cosine_verify_batch call over one batch of synthetic inputs already
+resident in HBM (all of SURVEY §8(a): target softmax stats, drafter normalisers,
+Eq. 4 fusion, acceptance, first rejection, residual / bonus resample).  For N > 1
+(torchrun, one process per GPU) every rank verifies its own batch of the same
+shape with distinct global request ids: weak scaling, no data-path collective
+(requests are independent, Alg. 2).  Prints ONE JSON line on rank 0.
+
+`--impl reference` times the CPU oracle (oracle/, fp64 C) on the host cores as the
+reference arm: each step verifies a bounded sample (one request) of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified draft tokens/sec and HBM GB/s vs 8 TB/s at 1/2/4/8 B200"
+UNIT = "verified draft tokens/s"
+WORKLOADS = {
+    "c1": "c1: batch=1, 2 drafters, k=4, vocab=32000, fp32 logits/probs, CONF fusion, T=1",
+    "c2": "c2: batch=64, 3 drafters, k=8, vocab=32000 (Llama-2), bf16 logits/probs, CONF fusion, T=1",
+    "c3": "c3: batch=256, 4 drafters, k=8, vocab=128256 (Llama-3), bf16 logits/probs, CONF fusion, T=1",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cluster-size", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=1234)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    def __init__(self, device_index: int, period: float = 0.01):
+        super().__init__(daemon=True)
+        self.period = period
+        self.samples = []
+        self.reasons = set()
+        self.stop_ev = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def run(self):
+        if not self.ok:
+            return
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            "display_clock_setting": 0x100,
+        }
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cfg_of(name):
+    from paper_2503_10325_b200 import synth
+    c = dict(synth.CONFIGS[name])
+    return c
+
+
+# --------------------------------------------------------------------------------------
+def cpu_oracle_rate(host_inputs, k, N, V, budget_s, seed):
+    """Time the CPU oracle (as it stands, single-threaded) on whole requests of the workload
+    until ~budget_s seconds of CPU work; returns (tokens/s, requests, seconds)."""
+    import numpy as np
+    import oracle
+    t = host_inputs["target"]
+    d = host_inputs["draft"]
+    X = host_inputs["draft_tokens"]
+    rid = host_inputs["request_ids"]
+    done_req, tok, spent = 0, 0, 0.0
+    B = t.shape[0]
+    while spent < budget_s and done_req < B:
+        b = done_req
+        tt = t[b:b + 1, :, :V].double().numpy()
+        dd = d[b:b + 1, :, :, :V].double().numpy()
+        xx = X[b:b + 1].numpy()
+        rr = rid[b:b + 1].numpy().astype(np.uint64)
+        t0 = time.perf_counter()
+        oracle.verify_batch(tt, dd, xx, rr, temperature=1.0, seed=seed)
+        spent += time.perf_counter() - t0
+        done_req += 1
+        tok += k
+    return tok / spent, done_req, spent
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle on the box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from paper_2503_10325_b200 import synth
+    import oracle
+    import numpy as np
+    c = cfg_of(args.config)
+    B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
+    steps, warm = args.steps, args.warmup
+    nreq = min(B, steps + warm)
+    inp = synth.linear_inputs(nreq, k, N, V, dtype=dt, seed=args.seed, device="cpu", chunk=4)
+    times = []
+    for s in range(warm + steps):
+        b = s % nreq
+        tt = inp["target"][b:b + 1, :, :V].double().numpy()
+        dd = inp["draft"][b:b + 1, :, :, :V].double().numpy()
+        xx = inp["draft_tokens"][b:b + 1].numpy()
+        rr = inp["request_ids"][b:b + 1].numpy().astype(np.uint64)
+        t0 = time.perf_counter()
+        oracle.verify_batch(tt, dd, xx, rr, temperature=1.0, seed=args.seed)
+        dt_s = time.perf_counter() - t0
+        if s >= warm:
+            times.append(dt_s)
+    total = sum(times)
+    value = steps * k / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "sample_per_step": "1 request (k verified tokens)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{steps} steps x 1 request of {args.config} (fp64 C oracle, 1 thread)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_2503_10325_b200 as cv
+    from paper_2503_10325_b200 import synth
+
+    c = cfg_of(args.config)
+    B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
+    esz = torch.tensor([], dtype=dt).element_size()
+    dev = torch.device("cuda", local)
+    inp = synth.linear_inputs(B, k, N, V, dtype=dt, seed=args.seed + 7919 * rank, device=dev,
+                              rid_base=rank * B)
+    ver = cv.Verifier(V, max_batch=B, k=k, N=N, device=local, target_dtype=dt, draft_dtype=dt,
+                      seed=args.seed, cluster_size=args.cluster_size)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"],
+                   temperature=1.0)
+        return cv.cosine_last_launch_count(ver.ctx)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    t_start.record(stream)
+    for s in range(args.steps):
+        ev[s][0].record(stream)
+        launches += step()
+        ev[s][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.stop_ev.set()
+    sampler.join()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    acc = ver.accept_len[:B].float().mean().item()
+    status_nonzero = int((ver.status[:B] & 0xff).ne(0).sum().item())
+
+    tokens_per_step = B * k * world
+    value = tokens_per_step * args.steps / (elapsed_ms / 1e3)
+    alg_bytes = synth.algorithmic_bytes(B, k, N, V, esz, esz)
+    kern_avg_s = statistics.mean(kern_ms) / 1e3
+    achieved = alg_bytes / kern_avg_s / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(args.config)
+    except Exception:
+        pass
+
+    # ---- e2e: the public call from pinned host buffers, H2D + kernel + D2H in the region
+    e2e = None
+    if not args.no_e2e:
+        names = ("target", "draft", "draft_tokens", "request_ids")
+        host = {n: inp[n].cpu().pin_memory() for n in names}
+        devbuf = {n: torch.empty_like(inp[n]) for n in names}
+        h2d = sum(host[n].numel() * host[n].element_size() for n in names)
+        d2h = B * 4 + B * (k + 1) * 4 + B * 4
+        ver.verify_host(host, devbuf)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            ver.verify_host(host, devbuf)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": tokens_per_step * args.e2e_steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(te.item()) / args.e2e_steps}
+        del devbuf, host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host_inp = {n: inp[n][: min(B, 512)].cpu() for n in ("target", "draft", "draft_tokens", "request_ids")}
+        rate, nreq, spent = cpu_oracle_rate(host_inp, k, N, V, args.cpu_seconds, args.seed)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{nreq} requests of {args.config} ({nreq * k} verified tokens), fp64 C oracle, "
+                         f"1 thread, {spent:.1f} s"}
+
+    if rank == 0:
+        clocks = sampler.result()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if dt == torch.bfloat16 else "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "batch_per_gpu": B, "global_batch": B * world,
+                       "k": k, "drafters": N, "vocab": V, "parallelism": f"batch-sharded x{world}",
+                       "l2": f"inputs {alg_bytes / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
+                       "mean_accept_len": acc, "request_errors": status_nonzero},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac_of_8tbs": achieved / 8000.0, "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_us": kern_avg_s * 1e6, "kernel": "cosine::unit_kernel"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    ver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -16,6 +16,8 @@ constexpr int kMaxN = 8;       // drafters
 constexpr int kMaxC = 16;      // CTAs per cluster (one (request, position) unit per cluster)
 constexpr int kGroup = 8;      // vocabulary elements per group (one 16-byte bf16 vector)
 constexpr int kNoReject = 0x7fffffff;
+constexpr int kSegGroups = 512;  // solo sampling: groups per warp-owned segment
+constexpr int kMaxSeg = 256;     // segments per row (segment size grows beyond)
 constexpr float kNegBig = -3.402823466e+38f;  // running-max seed: finite so that -inf - m = -inf
 
 // Philox tags (header: ACCEPT = 0, SAMPLE = 1, FUSE = 2).
@@ -144,6 +146,42 @@ __device__ __forceinline__ void warp_argmax(float& v, int64_t& idx) {
     const int64_t oi = __shfl_xor_sync(0xffffffffu, idx, o);
     if (oi >= 0 && (idx < 0 || ov > v || (ov == v && oi < idx))) { v = ov; idx = oi; }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster barrier halves and mbarriers (PTX ISA: barrier.cluster, mbarrier, mapa)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init_cluster() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Arrive (release, cluster scope) on the mbarrier at the same smem offset in CTA `rank`.
+__device__ __forceinline__ void mbar_remote_arrive(uint64_t* bar, uint32_t rank) {
+  uint32_t raddr;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 }  // namespace cosine

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -125,8 +126,8 @@ struct UnitState {  // CTA 0, thread 0 only
 __device__ __forceinline__ float fmin_(float a, float b) { return a < b ? a : b; }
 
 // Per-element sampling weights of one group (kinds above).
-template <typename TT, typename TQ, bool kLogits, int NMAX>
-__device__ __forceinline__ void group_weights(const Params& P, const Decision& d, int kind,
+template <typename TT, typename TQ, bool kLogits, int NMAX, typename PP>
+__device__ __forceinline__ void group_weights(const PP& P, const Decision& d, int kind,
                                               const TT* trow, const TQ* drow, int Nd, int64_t gi,
                                               float w[8]) {
   const bool need_t = (kind != kWFuseQ && kind != kWWriteQ);
@@ -185,6 +186,95 @@ __device__ __forceinline__ void group_weights(const Params& P, const Decision& d
   }
 }
 
+// Block barrier: kBar == 0 -> __syncthreads; else named barrier 1 over kBar threads (the
+// consumer warps of the persistent kernel, which must not wait for the producer warp).
+template <int kBar>
+__device__ __forceinline__ void sync_part() {
+  if (kBar == 0) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"r"(kBar) : "memory");
+}
+
+// Tile-ordered block scan of groups [sb, se): smallest v with C(v) > tc (C = running sum of
+// w from sb), rounding fallback = last v with w(v) > 0 (reading #10).  Result valid in every
+// thread; *s_margin (thread 0) = distance of tc to the chosen bin's edges / Z.
+template <typename TT, typename TQ, bool kLogits, int NMAX, int kBar = 0, typename PP = Params>
+__device__ __forceinline__ int64_t scan_range(const PP& P, const Decision& d, int kind,
+                                           const TT* trow, const TQ* drow, int Nd, int64_t sb,
+                                           int64_t se, double tc, double Z, double* s_scan,
+                                           int64_t* s_wi, int64_t* s_found, float* s_margin) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;  // kBar: consumer-only barrier
+  if (tid == 0) { *s_found = -1; *s_margin = 0.f; }
+  sync_part<kBar>();
+  double base = 0.0;
+  for (int64_t t0 = sb; t0 < se; t0 += kThreads) {
+    const int64_t gi = t0 + tid;
+    float w[8];
+    double s = 0.0;
+    if (gi < se) {
+      group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+      s = (double)sum8(w);
+    }
+    double incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += nb;
+    }
+    if (lane == 31) s_scan[warp] = incl;
+    sync_part<kBar>();
+    double wpre = 0.0, tot = 0.0;
+    for (int w2 = 0; w2 < kWarps; ++w2) {
+      if (w2 < warp) wpre += s_scan[w2];
+      tot += s_scan[w2];
+    }
+    const double excl = base + wpre + incl - s;
+    if (gi < se && s > 0.0 && excl <= tc && tc < excl + s) {
+      double cum = excl;
+      int ef = -1;
+      float mg = 0.f;
+      for (int e = 0; e < 8; ++e) {
+        const double prev = cum;
+        cum += (double)w[e];
+        if (cum > tc) {
+          ef = e;
+          mg = (float)(fmin(tc - prev, cum - tc) / Z);
+          break;
+        }
+      }
+      if (ef < 0) {
+        for (int e = 7; e >= 0; --e)
+          if (w[e] > 0.f) { ef = e; break; }
+      }
+      *s_found = gi * kGroup + ef;
+      *s_margin = mg;
+    }
+    base += tot;
+    sync_part<kBar>();
+    if (*s_found >= 0) break;
+  }
+  if (*s_found < 0) {
+    int64_t last = -1;
+    for (int64_t gi = sb + tid; gi < se; gi += kThreads) {
+      float w[8];
+      group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+      for (int e = 0; e < 8; ++e)
+        if (w[e] > 0.f) last = max(last, gi * kGroup + e);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+    if (lane == 0) s_wi[warp] = last;
+    sync_part<kBar>();
+    if (tid == 0) {
+      int64_t l2 = -1;
+      for (int w2 = 0; w2 < kWarps; ++w2) l2 = max(l2, s_wi[w2]);
+      *s_found = l2;
+      *s_margin = 0.f;
+    }
+    sync_part<kBar>();
+  }
+  return *s_found;
+}
+
 // Block-wide sum of a double (result valid in thread 0).
 __device__ __forceinline__ double block_sum(double x, double* s_buf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -220,6 +310,8 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
   __shared__ int32_t s_wbad[kWarps];
   __shared__ double s_scan[kWarps];
   __shared__ int64_t s_found;
+  __shared__ float s_margin;
+  __shared__ double s_seg[kMaxSeg];
 
   // ---------------- unit decode ----------------
   int b = 0, i = 0, g = 0;
@@ -228,8 +320,10 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
   const TQ* drow = nullptr;
   const int N = P.N;
   if (P.mode == kModeVerify) {
-    b = (int)(unit / (P.k + 1));
-    i = (int)(unit % (P.k + 1));
+    // position-major order: when position i of a request runs, its earlier positions have
+    // (mostly) decided, so the first-rejection gate below is nearly exact
+    i = (int)(unit / P.B);
+    b = (int)(unit % P.B);
     g = P.draft_len ? P.draft_len[b] : P.k;
     if (g < 1 || g > P.k) {  // per-request error, no unit of b runs
       if (i == 0 && rank == 0 && tid == 0) {
@@ -245,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
     trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t;
     if (has_d) drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
   } else if (P.mode == kModeFuse) {
-    b = (int)(unit / P.k);
-    i = (int)(unit % P.k);
+    i = (int)(unit / P.B);
+    b = (int)(unit % P.B);
     g = P.k;
     has_d = true;
     drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
@@ -259,6 +353,19 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
   }
   const int Nd = has_d ? N : 0;
   const uint64_t rid = P.rids[b];
+  // solo: the C-1 helper CTAs leave as soon as their statistics are in CTA 0; CTA 0 alone
+  // decides and (rarely: first rejection / bonus) samples from the L2-resident rows.
+  // Cooperative (all CTAs stay) only when every unit needs a full-row pass after the stats:
+  // x* ~ q (SAMPLE select) or materialising q (fuse_drafts with fused_q).
+  const bool solo = !(P.select_mode == COSINE_SEL_SAMPLE || (P.mode == kModeFuse && P.fused_q));
+  __shared__ __align__(8) uint64_t s_bar;
+  if (solo) {
+    if (rank == 0 && tid == 0) {
+      mbar_init(&s_bar, (uint32_t)C);
+      fence_mbar_init_cluster();
+    }
+    cluster_arrive_relaxed();
+  }
 
   // ---------------- candidate gathers (CTA 0; in flight during the stream) ----------------
   const int n_gath = (P.mode != kModeSample && has_d) ? N * (N + (has_t ? 1 : 0)) : 0;
@@ -442,11 +549,21 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
         for (int w = 0; w < kWarps; ++w) sacc += s_wd[w][1 + n];
         rec.dsum[n] = sacc;
       }
+      if (solo) cluster_wait();  // CTA 0's mbarrier is initialised
       CtaRec* dst = cluster.map_shared_rank(s_rec, 0) + rank;
       *dst = rec;
+      if (solo) mbar_remote_arrive(&s_bar, 0);
     }
   }
-  cluster.sync();
+  if (solo) {
+    if (tid != 0) cluster_wait();
+    if (rank != 0) return;  // helpers leave: no DSMEM access to them from now on
+    if (tid == 0) mbar_wait_parity(&s_bar, 0);
+    __syncthreads();
+  } else {
+    cluster.sync();
+  }
+  const int bcast = solo ? 1 : C;
 
   // ---------------- decision loop ----------------
   for (int round = 0;; ++round) {
@@ -701,9 +818,12 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
         s_out.degenerate = 0;
         s_out.z = NAN;
       }
-      for (int r = 0; r < C; ++r) cluster.map_shared_rank(s_dec, r)[round & 1] = d;
+      if (solo) s_dec[round & 1] = d;
+      else
+        for (int r = 0; r < bcast; ++r) cluster.map_shared_rank(s_dec, r)[round & 1] = d;
     }
-    cluster.sync();
+    if (solo) __syncthreads();
+    else cluster.sync();
     const Decision d = s_dec[round & 1];
     if (!d.need) break;
 
@@ -734,6 +854,61 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
     // ---- one inverse-CDF sampling round (reading #10) ----
     int kind = d.kind;
     int degenerate = 0;
+    if (solo) {
+      // CTA 0 alone over the whole row group: pass A = per-segment sums (one warp per
+      // segment, no block barrier), then a tile scan of the crossing segment only.
+      const int64_t segG = max((int64_t)kSegGroups, (P.ngroups + kMaxSeg - 1) / kMaxSeg);
+      const int nseg = (int)((P.ngroups + segG - 1) / segG);
+      for (int attempt = 0;; ++attempt) {
+        __syncthreads();
+        for (int sg = warp; sg < nseg; sg += kWarps) {
+          double acc = 0.0;
+          const int64_t e1 = min(P.ngroups, (sg + 1) * segG);
+#pragma unroll 4
+          for (int64_t gi = sg * segG + lane; gi < e1; gi += 32) {
+            float w[8];
+            group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+            acc += (double)sum8(w);
+          }
+          acc = warp_sum(acc);
+          if (lane == 0) s_seg[sg] = acc;
+        }
+        __syncthreads();
+        double Z = 0.0;
+        for (int sg = 0; sg < nseg; ++sg) Z += s_seg[sg];
+        if (!(Z > 0.0) && (kind == kWResidual || kind == kWPoint) && attempt == 0) {
+          kind = kWProb;  // all mass cancelled: resample from o (reading #11)
+          degenerate = 1;
+          continue;
+        }
+        const double t = d.u * Z;
+        int sstar = -1;
+        double tc = 0.0, O = 0.0;
+        for (int sg = 0; sg < nseg; ++sg) {
+          const double z = s_seg[sg];
+          if (O + z > t) { sstar = sg; tc = t - O; break; }
+          O += z;
+        }
+        int64_t y = -1;
+        float margin = 0.f;
+        if (sstar >= 0)
+          y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sstar * segG,
+                                                 min(P.ngroups, (sstar + 1) * segG), tc, Z, s_scan,
+                                                 s_wi, &s_found, &s_margin);
+        if (tid == 0) {
+          margin = s_margin;
+          s_out.y = y;
+          s_out.margin = margin;
+          s_out.degenerate = degenerate;
+          s_out.z = (float)((kind == kWBonus) ? Z * (double)d.invS : Z);
+          s_out.tx = 0.f;
+          for (int n = 0; n < kMaxN; ++n) s_out.dx[n] = 0.f;
+        }
+        __syncthreads();
+        break;
+      }
+      continue;
+    }
     for (int attempt = 0;; ++attempt) {
       double acc = 0.0;
       for (int64_t gi = gb + tid; gi < ge; gi += kThreads) {
@@ -761,83 +936,13 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
         O += zcc;
       }
       if (rank == cstar) {
-        // pass B: tile-ordered block scan of this chunk, find smallest v with C(v) > t
-        if (tid == 0) s_found = -1;
-        __syncthreads();
-        double base = 0.0;
-        float my_margin = 0.f;
-        for (int64_t t0 = gb; t0 < ge; t0 += kThreads) {
-          const int64_t gi = t0 + tid;
-          float w[8];
-          double s = 0.0;
-          if (gi < ge) {
-            group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
-            s = (double)sum8(w);
-          }
-          // inclusive warp scan, then across warps
-          double incl = s;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const double nb = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += nb;
-          }
-          if (lane == 31) s_scan[warp] = incl;
-          __syncthreads();
-          double wpre = 0.0, tot = 0.0;
-          for (int w2 = 0; w2 < kWarps; ++w2) {
-            if (w2 < warp) wpre += s_scan[w2];
-            tot += s_scan[w2];
-          }
-          const double excl = base + wpre + incl - s;
-          if (gi < ge && s > 0.0 && excl <= tc && tc < excl + s) {
-            double cum = excl;
-            int ef = -1;
-            for (int e = 0; e < 8; ++e) {
-              const double prev = cum;
-              cum += (double)w[e];
-              if (cum > tc) {
-                ef = e;
-                my_margin = (float)(fmin(tc - prev, cum - tc) / Z);
-                break;
-              }
-            }
-            if (ef < 0) {
-              for (int e = 7; e >= 0; --e)
-                if (w[e] > 0.f) { ef = e; break; }
-              my_margin = 0.f;
-            }
-            s_found = gi * kGroup + ef;
-            s_out.margin = my_margin;  // local copy, forwarded below
-          }
-          base += tot;
-          __syncthreads();
-          if (s_found >= 0) break;
-        }
-        if (s_found < 0) {
-          // rounding fallback: the last v of the chunk with w(v) > 0 (reading #10)
-          int64_t last = -1;
-          for (int64_t gi = gb + tid; gi < ge; gi += kThreads) {
-            float w[8];
-            group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
-            for (int e = 0; e < 8; ++e)
-              if (w[e] > 0.f) last = max(last, gi * kGroup + e);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-          if (lane == 0) s_wi[warp] = last;
-          __syncthreads();
-          if (tid == 0) {
-            int64_t l2 = -1;
-            for (int w2 = 0; w2 < kWarps; ++w2) l2 = max(l2, s_wi[w2]);
-            s_found = l2;
-            s_out.margin = 0.f;
-          }
-          __syncthreads();
-        }
+        const int64_t y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gb, ge, tc, Z,
+                                                             s_scan, s_wi, &s_found, &s_margin);
+        (void)y;
         if (tid == 0) {
           SampleOut so;
           so.y = s_found;
-          so.margin = s_out.margin;
+          so.margin = s_margin;
           so.degenerate = degenerate;
           so.z = (float)((kind == kWBonus) ? Z * (double)d.invS : Z);
           so.tx = 0.f;
@@ -960,12 +1065,29 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
   P.first_rej[b] = kNoReject;
 }
 
+}  // namespace cosine
+#include "cosine_stream.cuh"
+namespace cosine {
+
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) { done[j] = 0; first_rej[j] = kNoReject; }
 }
 
 using KernelFn = void (*)(Params);
+using StreamFn = void (*)(StreamParams);
+
+template <typename TT, typename TQ>
+StreamFn pick_stream2(bool logits, int N) {
+  if (logits) return N <= 4 ? stream_kernel<TT, TQ, true, 4> : stream_kernel<TT, TQ, true, 8>;
+  return N <= 4 ? stream_kernel<TT, TQ, false, 4> : stream_kernel<TT, TQ, false, 8>;
+}
+StreamFn pick_stream(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N) {
+  if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_stream2<__nv_bfloat16, __nv_bfloat16>(logits, N);
+  if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_stream2<__nv_bfloat16, float>(logits, N);
+  if (tt == COSINE_F32 && tq == COSINE_BF16) return pick_stream2<float, __nv_bfloat16>(logits, N);
+  return pick_stream2<float, float>(logits, N);
+}
 
 template <typename TT, typename TQ>
 KernelFn pick_kernel2(bool logits, int N) {
@@ -994,6 +1116,7 @@ struct cosine_ctx_s {
   int32_t* first_rej = nullptr;
   std::string err;
   int32_t last_launches = 0;
+  int32_t last_cluster = 0, last_ncl = 0;
 };
 
 static thread_local std::string g_init_error;
@@ -1061,6 +1184,80 @@ cosine_status_t launch(cosine_ctx_t ctx, cudaStream_t stream, Params& P, int64_t
     return fail(ctx, COSINE_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   }
   ctx->last_launches = 1;
+  return COSINE_OK;
+}
+
+// Persistent kernel: pick the cluster size / cluster count that keeps every SM streaming
+// (max co-resident clusters from the occupancy API; requests are dealt round-robin).
+cosine_status_t launch_stream(cosine_ctx_t ctx, cudaStream_t stream, StreamParams& S,
+                              cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+  StreamFn fn = pick_stream(tt, tq, logits, S.N);
+  const int tsz = (int)esize(tt), qsz = (int)esize(tq);
+  S.t_slot = kTileElems * tsz;
+  S.q_slot = kTileElems * qsz;
+  S.stage_bytes = S.t_slot + S.N * S.q_slot;
+  const int budget = 200 * 1024;
+  S.stages = std::min(kMaxStages, budget / S.stage_bytes);
+  if (S.stages < 2) return fail(ctx, COSINE_ERR_UNSUPPORTED, "stage does not fit in shared memory");
+  const size_t dsmem = (size_t)S.stages * S.stage_bytes;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(ctx, COSINE_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e)); }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device);
+  int best_C = 0, best_ncl = 0;
+  double best_eff = -1.0;
+  const int cands[3] = {8, 4, 2};
+  for (int ci = 0; ci < 3; ++ci) {
+    const int C = cands[ci];
+    if (ctx->cfg.cluster_size > 0 && C != ctx->cfg.cluster_size) continue;
+    cudaLaunchConfig_t lc;
+    memset(&lc, 0, sizeof(lc));
+    lc.gridDim = dim3((unsigned)(C * 64), 1, 1);
+    lc.blockDim = dim3(kStreamThreads, 1, 1);
+    lc.dynamicSmemBytes = dsmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int maxcl = 0;
+    if (cudaOccupancyMaxActiveClusters(&maxcl, fn, &lc) != cudaSuccess || maxcl < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    const int ncl = std::min(S.B, maxcl);
+    const int rounds = (S.B + ncl - 1) / ncl;
+    const double eff = (double)S.B / ((double)rounds * maxcl) * ((double)maxcl * C / sms);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best_C = C; best_ncl = ncl; }
+  }
+  if (best_C == 0) return fail(ctx, COSINE_ERR_CUDA, "no cluster configuration fits");
+  S.C = best_C;
+  S.ncl = best_ncl;
+  S.cgroups = (S.ngroups + S.C - 1) / S.C;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.gridDim = dim3((unsigned)(S.C * S.ncl), 1, 1);
+  lc.blockDim = dim3(kStreamThreads, 1, 1);
+  lc.dynamicSmemBytes = dsmem;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  e = cudaLaunchKernelEx(&lc, fn, S);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("stream kernel launch: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 1;
+  ctx->last_cluster = S.C;
+  ctx->last_ncl = S.ncl;
   return COSINE_OK;
 }
 
@@ -1252,6 +1449,21 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   P.out_tokens = out_tokens;
   P.status = status;
   if (debug) P.dbg = *debug;
+  const char* force_v2 = getenv("COSINE_FORCE_CLUSTER_KERNEL");
+  if (select_mode == COSINE_SEL_ARGMAX && !(force_v2 && force_v2[0] == '1')) {
+    StreamParams S;
+    memset(&S, 0, sizeof(S));
+    S.B = B; S.k = k; S.N = N;
+    S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+    S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+    S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+    S.rids = request_ids; S.seed = P.seed; S.step = step;
+    S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
+    const char* dflags = getenv("COSINE_DEBUG_FLAGS");
+    S.debug_flags = dflags ? atoi(dflags) : 0;
+    return launch_stream(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                         ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+  }
   return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
                 ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
 }

@@ -39,5 +39,5 @@ fails += run(8, 4, 3, 5000, torch.bfloat16, wm=2)
 fails += run(8, 4, 3, 5000, torch.bfloat16, wm=3)
 fails += run(8, 4, 3, 5000, torch.bfloat16, sm=1)
 fails += run(8, 4, 2, 5000, torch.float32, kind='logits', T=0.7)
-fails += run(8, 4, 3, 5000, torch.bfloat16, cs=1)
+fails += run(8, 4, 3, 5000, torch.bfloat16, cs=2)
 print("FAILS", fails)
