@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libcosine_verify.so")
 SOURCES = [os.path.join(CSRC, "cosine_verify.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "cosine_kernels.cuh"), os.path.join(CSRC, "cosine_stream.cuh"), os.path.join(INCLUDE, "cosine_verify.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "cosine_kernels.cuh"), os.path.join(CSRC, "cosine_split.cuh"), os.path.join(INCLUDE, "cosine_verify.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

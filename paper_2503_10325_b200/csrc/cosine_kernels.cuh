@@ -17,6 +17,8 @@ constexpr int kMaxC = 16;      // CTAs per cluster (one (request, position) unit
 constexpr int kGroup = 8;      // vocabulary elements per group (one 16-byte bf16 vector)
 constexpr int kNoReject = 0x7fffffff;
 constexpr int kSegGroups = 512;  // solo sampling: groups per warp-owned segment
+constexpr int kTileGroups = 256;  // sampling segment: groups per warp
+constexpr int kTileElems = kTileGroups * 8;
 constexpr int kMaxSeg = 256;     // segments per row (segment size grows beyond)
 constexpr float kNegBig = -3.402823466e+38f;  // running-max seed: finite so that -inf - m = -inf
 

@@ -1,0 +1,688 @@
+// cosine_split.cuh — the two kernels behind cosine_verify_batch (Eq. 4 ARGMAX fusion).
+//
+// Kernel A (stats_kernel): one CTA per (unit, vocabulary chunk), unit = (request b,
+//   position i <= gamma_b).  Each CTA streams its chunk of the unit's target logit row and N
+//   drafter rows exactly once with 128-bit read-only loads, reduces them (online max /
+//   sum-exp of the target, drafter row sums, greedy argmax) and writes a 128-byte partial
+//   record.  Nothing else: no decision code, so the kernel stays register-lean (high
+//   occupancy = many loads in flight) and never waits.
+// Kernel B (decide_sample_kernel): one thread-block cluster per request.  Every CTA combines
+//   the partial records of the request's positions (one warp per position), takes the
+//   decisions — confidences and Eq. 4 fusion, acceptance u * q(x*) < o(x*)
+//    — finds the first rejection L and the cluster draws the final token by
+//   inverse CDF over the residual norm(max(0, o - q)) of row L, or over o of the bonus row
+//   (P:133): pass A = per-warp segment sums, chunk sums exchanged over DSMEM; pass B = one
+//   warp scans the crossing segment.  CTA 0 writes the request's outputs.
+#pragma once
+
+namespace cosine {
+
+struct PartRec {  // one per (unit, chunk); 128 bytes
+  float tmax;     // T > 0: chunk max logit; greedy: best value
+  int32_t bad;    // bit0 target non-finite (greedy), bit1 negative drafter prob
+  int64_t targ;   // greedy argmax (global index), -1 if none
+  double tsum;    // sum 2^((l - tmax) k2) over the chunk
+  float dmax[kMaxN];
+  double dsum[kMaxN];
+};
+
+constexpr int kMaxPos = 65;  // draft positions per request (k <= 64) in kernel B
+
+struct SplitParams {
+  int B, k, N;
+  int64_t V, ld_t, ld_q, ngroups, gfull;
+  int C;          // CTAs per unit (kernel A)
+  int64_t cg;     // groups per chunk (kernel A)
+  int C2;         // cluster size (kernel B)
+  int64_t cg2;    // groups per chunk (kernel B)
+  float k2f;
+  double k2d;
+  int greedy, weight_mode;
+  const void* target;
+  const void* draft;
+  const int32_t* draft_tokens;
+  const int32_t* draft_len;
+  const uint64_t* rids;
+  uint64_t seed;
+  uint32_t step;
+  int32_t* accept_len;
+  int32_t* out_tokens;
+  int32_t* status;
+  cosine_debug_t dbg;
+  PartRec* parts;
+  struct PosDec* pdec;
+  double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
+  int64_t nseg;
+  int spr;         // B2a CTAs per request
+  int b_off, nb;   // this launch covers requests [b_off, b_off + nb) (batch pipelining)
+};
+
+
+// One warp scans groups [gb, ge) in vocabulary order: smallest v with C(v) > tc, C the running
+// sum of w from gb; rounding fallback = last v with w(v) > 0 (reading #10).  All lanes return y.
+template <typename TT, typename TQ, bool kLogits, int NMAX, typename PP>
+__device__ __forceinline__ int64_t warp_scan_range(const PP& P, const Decision& d, int kind,
+                                                   const TT* trow, const TQ* drow, int Nd, int64_t gb,
+                                                   int64_t ge, double tc, double Z, float* margin) {
+  const int lane = threadIdx.x & 31;
+  double base = 0.0;
+  for (int64_t t0 = gb; t0 < ge; t0 += 32) {
+    const int64_t gi = t0 + lane;
+    float w[8];
+    double s = 0.0;
+    if (gi < ge) {
+      group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+      s = (double)sum8(w);
+    }
+    double incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += nb;
+    }
+    const double excl = base + incl - s;
+    const bool hit = gi < ge && s > 0.0 && excl <= tc && tc < excl + s;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) {
+      const int src = __ffs(m) - 1;
+      int64_t y = -1;
+      float mg = 0.f;
+      if (lane == src) {
+        double cum = excl;
+        int ef = -1;
+        for (int e = 0; e < 8; ++e) {
+          const double prev = cum;
+          cum += (double)w[e];
+          if (cum > tc) {
+            ef = e;
+            mg = (float)(fmin(tc - prev, cum - tc) / Z);
+            break;
+          }
+        }
+        if (ef < 0)
+          for (int e = 7; e >= 0; --e)
+            if (w[e] > 0.f) { ef = e; break; }
+        y = gi * kGroup + ef;
+      }
+      y = __shfl_sync(0xffffffffu, y, src);
+      *margin = __shfl_sync(0xffffffffu, mg, src);
+      return y;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  int64_t last = -1;
+  for (int64_t gi = gb + lane; gi < ge; gi += 32) {
+    float w[8];
+    group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+    for (int e = 0; e < 8; ++e)
+      if (w[e] > 0.f) last = max(last, gi * kGroup + e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+  *margin = 0.f;
+  return last;
+}
+
+// ============================== kernel A ==============================
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && sizeof(TQ) == 2) ? 6 : 4)
+    stats_kernel(const SplitParams P) {
+  const int C = P.C;
+  const int64_t unit = blockIdx.x / C;
+  const int rank = (int)(blockIdx.x % C);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N = P.N;
+  const int b = P.b_off + (int)(unit / (P.k + 1));
+  const int i = (int)(unit % (P.k + 1));
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (g < 1 || g > P.k || i > g) return;  // rows past gamma_b are never read
+  const int Nd = (i < g) ? N : 0;
+  const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t;
+  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
+
+  __shared__ float s_wf[kWarps][1 + kMaxN];
+  __shared__ float s_wv[kWarps];
+  __shared__ int64_t s_wi[kWarps];
+  __shared__ double s_wd[kWarps][1 + kMaxN];
+  __shared__ int32_t s_wbad[kWarps];
+
+  const bool greedy = P.greedy != 0;
+  const float k2 = P.k2f;
+  float tmx = kNegBig, tmk = kNegBig, ts = 0.f;  // running max, fl(max * k2), sum 2^(l k2 - tmk)
+  float tb = -INFINITY;
+  int64_t ti = -1;
+  bool tbad = false, dneg = false;
+  float dm[NMAX], dmk[NMAX], ds[NMAX];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) { dm[n] = kNegBig; dmk[n] = kNegBig; ds[n] = 0.f; }
+  const int64_t gb = (int64_t)rank * P.cg;
+  const int64_t ge = min(P.ngroups, gb + P.cg);
+  const int64_t gfe = min(ge, P.gfull);  // full groups of the chunk
+
+  auto t_step = [&](const float (&f)[8], int64_t gi) {
+    if (greedy) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (f[e] > tb) { tb = f[e]; ti = gi * kGroup + e; }
+        tbad |= !(f[e] <= 3.402823466e+38f);
+      }
+    } else {
+      const float gm = max8(f);
+      if (gm > tmx) {  // rescale by 2^(old fl(m k2) - new fl(m k2)); exact in fp64 below
+        const float nmk = gm * k2;
+        ts *= ex2(tmk - nmk);
+        tmx = gm;
+        tmk = nmk;
+      }
+      float e8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) e8[e] = ex2(fmaf(f[e], k2, -tmk));
+      ts += sum8(e8);
+    }
+  };
+  auto d_step = [&](int n, const float (&f)[8]) {
+    if (kLogits) {
+      const float gm = max8(f);
+      if (gm > dm[n]) {
+        const float nmk = gm * k2;
+        ds[n] *= ex2(dmk[n] - nmk);
+        dm[n] = gm;
+        dmk[n] = nmk;
+      }
+      float e8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) e8[e] = ex2(fmaf(f[e], k2, -dmk[n]));
+      ds[n] += sum8(e8);
+    } else {
+      ds[n] += sum8(f);
+    }
+  };
+
+  for (int64_t gi = gb + tid; gi < gfe; gi += kThreads) {
+    Group<TT> tv;
+    Group<TQ> dv[NMAX];
+    tv.load(trow, gi);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n)
+      if (n < Nd) dv[n].load(drow + (int64_t)n * P.ld_q, gi);
+    float f[8];
+    tv.unpack(f);
+    t_step(f, gi);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n < Nd) {
+        dv[n].unpack(f);
+        if (!kLogits && dv[n].any_sign()) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dneg |= (f[e] < 0.f);
+        }
+        d_step(n, f);
+      }
+    }
+  }
+  if (gfe < ge && tid == (int)((gfe - gb) % kThreads)) {  // the row's partial last group
+    const int64_t gi = gfe;
+    float f[8];
+    load_partial(trow, gi, P.V, -INFINITY, f);
+    t_step(f, gi);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n < Nd) {
+        load_partial(drow + (int64_t)n * P.ld_q, gi, P.V, kLogits ? -INFINITY : 0.f, f);
+        if (!kLogits) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dneg |= (f[e] < 0.f);
+        }
+        d_step(n, f);
+      }
+    }
+  }
+
+  // ---------------- CTA reduction -> partial record ----------------
+  float tmw = kNegBig, tbw = tb;
+  int64_t tiw = ti;
+  if (greedy) warp_argmax(tbw, tiw);
+  else tmw = warp_max(tmx);
+  float dmw[NMAX];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) dmw[n] = (kLogits && n < Nd) ? warp_max(dm[n]) : kNegBig;
+  if (lane == 0) {
+    s_wf[warp][0] = tmw;
+    s_wv[warp] = tbw;
+    s_wi[warp] = tiw;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) s_wf[warp][1 + n] = dmw[n];
+  }
+  __syncthreads();
+  float Mc = kNegBig;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) Mc = fmaxf(Mc, s_wf[w][0]);
+  // thread sums are relative to 2^(fl(m k2)); rescale exactly (fp64) to 2^(Mc k2)
+  double tsd = 0.0;
+  if (!greedy && ts != 0.f) tsd = (double)ts * exp2((double)tmk - (double)Mc * (double)k2);
+  tsd = warp_sum(tsd);
+  double dsd[NMAX];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) {
+    dsd[n] = 0.0;
+    if (n < Nd) {
+      if (kLogits) {
+        float dMc = kNegBig;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) dMc = fmaxf(dMc, s_wf[w][1 + n]);
+        if (ds[n] != 0.f) dsd[n] = (double)ds[n] * exp2((double)dmk[n] - (double)dMc * (double)k2);
+      } else {
+        dsd[n] = (double)ds[n];
+      }
+      dsd[n] = warp_sum(dsd[n]);
+    }
+  }
+  const int bad = (__any_sync(0xffffffffu, tbad) ? 1 : 0) | (__any_sync(0xffffffffu, dneg) ? 2 : 0);
+  if (lane == 0) {
+    s_wd[warp][0] = tsd;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) s_wd[warp][1 + n] = dsd[n];
+    s_wbad[warp] = bad;
+  }
+  __syncthreads();
+  if (tid < 32) {  // warp 0 assembles the record: lane j owns field j
+    PartRec* rec = P.parts + ((int64_t)P.b_off * (P.k + 1) + unit) * C + rank;
+    if (lane == 0) {
+      float bv = Mc;
+      int64_t bi = -1;
+      if (greedy) {
+        bv = -INFINITY;
+        for (int w = 0; w < kWarps; ++w) {
+          const float v = s_wv[w];
+          const int64_t ix = s_wi[w];
+          if (ix >= 0 && (bi < 0 || v > bv || (v == bv && ix < bi))) { bv = v; bi = ix; }
+        }
+      }
+      double t = 0.0;
+      int bd = 0;
+      for (int w = 0; w < kWarps; ++w) { t += s_wd[w][0]; bd |= s_wbad[w]; }
+      rec->tmax = bv;
+      rec->targ = bi;
+      rec->tsum = t;
+      rec->bad = bd;
+    } else if (lane <= kMaxN) {
+      const int n = lane - 1;
+      float mx = kNegBig;
+      double sacc = 0.0;
+      if (n < NMAX) {
+        for (int w = 0; w < kWarps; ++w) { mx = fmaxf(mx, s_wf[w][1 + n]); sacc += s_wd[w][1 + n]; }
+      }
+      rec->dmax[n] = mx;
+      rec->dsum[n] = sacc;
+    }
+  }
+}
+
+// ============================== kernel B ==============================
+struct PosDec {  // decisions of one position (shared memory of every CTA of the cluster)
+  int32_t status, accept, xstar;
+  int64_t amax;
+  float m_fa, M;
+  double S, px, qx, u;
+  float a[kMaxN], dm[kMaxN];
+  float sig[kMaxN], c[kMaxN], w[kMaxN];
+};
+
+// Kernel B1: one warp per (request, position).  The warp combines the C partial records
+// (lane r owns chunk r; fixed-order shuffle reductions), loads the candidate gathers (one lane
+// each), then lane 0 takes the position's decisions.
+template <typename TT, typename TQ, bool kLogits>
+__global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t lunit = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t unit = (int64_t)P.b_off * (P.k + 1) + lunit;
+  const int N = P.N, C = P.C;
+  __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kWarps][kMaxN];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel A's partial records (PDL)
+  if (lunit >= (int64_t)P.nb * (P.k + 1)) return;
+  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (g < 1 || g > P.k || i > g) return;
+  const bool has_d = i < g;
+  const bool greedy = P.greedy != 0;
+  const double k2 = (double)P.k2f;
+  const int ng = has_d ? N * (N + 1) : 0;
+  if (lane < ng) {
+    const int n = lane % N, m = lane / N;
+    const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
+    float v = 0.f;
+    if (tk >= 0 && (int64_t)tk < P.V) {
+      if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
+      else v = load_one((const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t, tk);
+    }
+    s_gx[warp][m * kMaxN + n] = v;
+    if (m == 0) s_tok[warp][n] = tk;
+  }
+  // ---- combine the partial records (chunk r in lane r) ----
+  const PartRec* parts = P.parts + unit * C;
+  const bool own = lane < C;
+  const float tmax = own ? parts[lane].tmax : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
+  PosDec pd;
+  pd.status = 0; pd.accept = 1; pd.xstar = -1; pd.amax = -1; pd.m_fa = INFINITY; pd.M = 0.f; pd.S = 0.0;
+  pd.px = pd.qx = pd.u = NAN;
+  for (int n = 0; n < kMaxN; ++n) { pd.a[n] = 0.f; pd.dm[n] = 0.f; pd.sig[n] = NAN; pd.c[n] = NAN; pd.w[n] = NAN; }
+  bool t_nf = false, t_empty = false, d_nf = false, d_empty = false, tok_bad = false, zero = false;
+  if (greedy) {
+    float bv = own ? tmax : -INFINITY;
+    int64_t bi = own ? parts[lane].targ : -1;
+    warp_argmax(bv, bi);
+    t_nf = (bad & 1) != 0;
+    t_empty = (bi < 0);
+    pd.amax = bi;
+    pd.M = bv;
+  } else {
+    const float M = warp_max(tmax);
+    const double tsum = own ? parts[lane].tsum : 0.0;
+    const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
+    pd.M = M;
+    pd.S = S;
+    t_nf = !isfinite(S) || !isfinite(M);
+    t_empty = !t_nf && !(S > 0.0);
+  }
+  double sig[kMaxN];
+  float dmax[kMaxN];
+  if (has_d) {
+    if (bad & 2) d_nf = true;
+    for (int n = 0; n < N; ++n) {
+      double sv;
+      float mx = kNegBig;
+      const double ds = own ? parts[lane].dsum[n] : 0.0;
+      if (kLogits) {
+        const float dmr = own ? parts[lane].dmax[n] : kNegBig;
+        mx = warp_max(dmr);
+        sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
+        if (!isfinite(mx)) d_nf = true;
+      } else {
+        sv = warp_sum(ds);
+      }
+      sig[n] = sv;
+      dmax[n] = mx;
+      if (!isfinite(sv)) d_nf = true;
+      else if (!(sv > 0.0)) d_empty = true;
+    }
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  const float* gx = s_gx[warp];
+  const int32_t* tok = s_tok[warp];
+  if (has_d)
+    for (int n = 0; n < N; ++n)
+      if (tok[n] < 0 || (int64_t)tok[n] >= P.V) tok_bad = true;
+  int stc = 0;
+  if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
+  else if (t_nf || d_nf) stc = COSINE_REQ_NONFINITE_INPUT;
+  else if (t_empty || d_empty) stc = COSINE_REQ_EMPTY_ROW;
+  // q_n(x) of a gathered drafter value (PROBS: d / sigma; LOGITS: softmax at the same k2)
+  auto qval = [&](int m, double dv) {
+    return kLogits ? exp2(dv * k2 - (double)dmax[m] * k2) / sig[m] : dv / sig[m];
+  };
+  double c[kMaxN], w[kMaxN];
+  if (!stc && has_d) {
+    for (int n = 0; n < N; ++n) {
+      c[n] = qval(n, (double)gx[n * kMaxN + n]);  // c_{n,i} = q_{n,i}(X_{n,i})
+      if (c[n] == 0.0) zero = true;
+    }
+    if (zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+  }
+  pd.status = stc;
+  if (!stc && has_d) {
+    // Eq. 4: n* = argmax_n c_n, ties -> lowest n; fused weights (reading #2)
+    int ns = 0;
+    for (int n = 1; n < N; ++n)
+      if (c[n] > c[ns]) ns = n;
+    double second = -1.0;
+    for (int n = 0; n < N; ++n)
+      if (n != ns && c[n] > second) second = c[n];
+    pd.m_fa = (N > 1) ? (float)((c[ns] - second) / c[ns]) : INFINITY;
+    if (P.weight_mode == COSINE_W_CONF) {
+      double sc = 0.0;
+      for (int n = 0; n < N; ++n) sc += c[n];
+      for (int n = 0; n < N; ++n) w[n] = c[n] / sc;
+    } else if (P.weight_mode == COSINE_W_UNIFORM) {
+      for (int n = 0; n < N; ++n) w[n] = 1.0 / (double)N;
+    } else {
+      for (int n = 0; n < N; ++n) w[n] = (n == ns) ? 1.0 : 0.0;
+    }
+    pd.xstar = tok[ns];
+    if (P.weight_mode == COSINE_W_POINT) {
+      pd.qx = 1.0;
+    } else {
+      double q = 0.0;
+      for (int m = 0; m < N; ++m) q += w[m] * qval(m, (double)gx[m * kMaxN + ns]);
+      pd.qx = q;
+    }
+    pd.u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
+    if (greedy) {
+      pd.accept = ((int64_t)pd.xstar == pd.amax);
+    } else {
+      // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
+      pd.px = exp2((double)gx[N * kMaxN + ns] * k2 - (double)pd.M * k2) / pd.S;
+      pd.accept = (pd.u * pd.qx < pd.px);
+      pd.m_fa = fmin_(pd.m_fa, (float)fabs(pd.u - pd.px / pd.qx));
+    }
+    for (int n = 0; n < N; ++n) {
+      pd.a[n] = (float)(w[n] / sig[n]);
+      pd.dm[n] = dmax[n];
+      pd.sig[n] = (float)sig[n];
+      pd.c[n] = (float)c[n];
+      pd.w[n] = (float)w[n];
+    }
+  }
+  P.pdec[unit] = pd;
+  const cosine_debug_t& D = P.dbg;
+  if (D.row_max) D.row_max[unit] = pd.M;
+  if (D.row_sumexp) D.row_sumexp[unit] = greedy ? 0.f : (float)pd.S;
+  if (has_d) {
+    const int64_t o1 = (int64_t)b * P.k + i;
+    if (D.p_x) D.p_x[o1] = (float)pd.px;
+    if (D.q_x) D.q_x[o1] = (float)pd.qx;
+    if (D.accept_u) D.accept_u[o1] = (float)pd.u;
+    if (D.fused_tokens) D.fused_tokens[o1] = pd.xstar;
+    for (int n = 0; n < N; ++n) {
+      if (D.draft_norm) D.draft_norm[o1 * N + n] = pd.sig[n];
+      if (D.conf) D.conf[o1 * N + n] = pd.c[n];
+      if (D.weights) D.weights[o1 * N + n] = pd.w[n];
+    }
+  }
+}
+
+// The request-level view of B1's decisions (first error, first rejection L, margins).
+struct ReqView {
+  int32_t g, err, L, sample;  // sample: T > 0 and no error -> a final inverse-CDF draw at row L
+  float tm;
+};
+// Inclusive prefix sum over the lanes, accumulated strictly left to right (lane order), so
+// every lane's partial equals the sequential sum of segments 0..lane.
+__device__ __forceinline__ double warp_sum_ordered(double x) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0, r = 0.0;
+  for (int l = 0; l < 32; ++l) {
+    acc += __shfl_sync(0xffffffffu, x, l);
+    if (l == lane) r = acc;
+  }
+  return r;
+}
+
+// Warp-cooperative: lane j reads position j's decision (one L2 round trip, not k+1).
+__device__ __forceinline__ ReqView request_view(const SplitParams& P, int b) {
+  const int lane = threadIdx.x & 31;
+  ReqView v;
+  v.g = P.draft_len ? P.draft_len[b] : P.k;
+  v.err = 0;
+  v.L = v.g;
+  v.tm = INFINITY;
+  v.sample = 0;
+  if (v.g < 1 || v.g > P.k) { v.err = COSINE_REQ_BAD_DRAFT_LEN; return v; }
+  const PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
+  int err = 0, L = v.g;
+  for (int j0 = 0; j0 <= v.g; j0 += 32) {  // positions in rounds of 32 (k <= 64)
+    const int j = j0 + lane;
+    const bool in = j <= v.g;
+    const int st = in ? pds[j].status : 0;
+    const bool rej = in && j < v.g && !pds[j].accept;
+    const unsigned me = __ballot_sync(0xffffffffu, st != 0);
+    const unsigned mr = __ballot_sync(0xffffffffu, rej);
+    if (!err && me) err = __shfl_sync(0xffffffffu, st, __ffs(me) - 1);
+    if (L == v.g && mr) L = j0 + __ffs(mr) - 1;
+  }
+  float tm = INFINITY;
+  for (int j0 = 0; j0 <= L; j0 += 32) {
+    const int j = j0 + lane;
+    tm = fmin_(tm, (j <= L) ? pds[j].m_fa : INFINITY);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tm = fminf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+  v.err = err;
+  v.L = L;
+  v.tm = tm;
+  v.sample = (!err && !P.greedy) ? 1 : 0;
+  return v;
+}
+
+__device__ __forceinline__ Decision sample_decision(const SplitParams& P, int b, const ReqView& v) {
+  const PosDec& pl = P.pdec[(int64_t)b * (P.k + 1) + v.L];
+  const bool resid = v.L < v.g;
+  Decision d;
+  d.need = 1;
+  d.kind = resid ? ((P.weight_mode == COSINE_W_POINT) ? kWPoint : kWResidual) : kWBonus;
+  d.xstar = pl.xstar;
+  d.node = (uint32_t)v.L;
+  d.u = philox_u24(P.seed, P.rids[b], (uint32_t)v.L, P.step, kTagSample);
+  d.M = pl.M;
+  d.invS = (float)(1.0 / pl.S);
+  d.k2 = P.k2f;
+  for (int n = 0; n < kMaxN; ++n) { d.a[n] = pl.a[n]; d.dm[n] = pl.dm[n]; }
+  return d;
+}
+
+// Kernel B2a: residual / bonus mass of every 256-group segment of the sampled row.
+// One warp per segment (2048 vocabulary entries), lane-strided 128-bit loads.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, 4) segsum_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
+  const int64_t seg = (int64_t)(blockIdx.x % P.spr) * kWarps + warp;
+  __shared__ ReqView s_v;
+  __shared__ Decision s_d;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B1's decisions (PDL)
+  if (warp == 0) {
+    const ReqView v = request_view(P, b);
+    if (lane == 0) {
+      s_v = v;
+      if (v.sample) s_d = sample_decision(P, b, v);
+    }
+  }
+  __syncthreads();
+  const ReqView v = s_v;
+  if (!v.sample || seg >= P.nseg) return;
+  const Decision d = s_d;
+  const int Nd = (v.L < v.g) ? P.N : 0;
+  const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
+  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
+  const int64_t g0 = seg * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
+  double acc = 0.0;
+  for (int64_t gi = g0 + lane; gi < g1; gi += 64) {  // two groups of loads in flight per lane
+    float w0[8], w1[8];
+    const bool two = gi + 32 < g1;
+    group_weights<TT, TQ, kLogits, NMAX>(P, d, d.kind, trow, drow, Nd, gi, w0);
+    if (two) group_weights<TT, TQ, kLogits, NMAX>(P, d, d.kind, trow, drow, Nd, gi + 32, w1);
+    acc += (double)sum8(w0);
+    if (two) acc += (double)sum8(w1);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) P.segsum[(int64_t)b * P.nseg + seg] = acc;
+}
+
+// Kernel B2b: one warp per request: Z = sum of the segment masses (segment order), the
+// crossing segment, a warp scan of that segment only; then the request's outputs.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads) finish_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B2a's segment masses (PDL)
+  const int bl = blockIdx.x * kWarps + warp;
+  if (bl >= P.nb) return;
+  const int b = P.b_off + bl;
+  const ReqView v = request_view(P, b);
+  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
+  const PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
+  if (v.err) {
+    for (int j = lane; j <= P.k; j += 32) out[j] = -1;
+    if (lane == 0) { P.accept_len[b] = -1; P.status[b] = v.err; }
+    return;
+  }
+  int64_t y = -1;
+  float margin = INFINITY, zmass = NAN;
+  int deg = 0;
+  if (!v.sample) {
+    y = pds[v.L].amax;  // greedy: argmax of row L (reading #7)
+  } else {
+    const Decision d = sample_decision(P, b, v);
+    const int Nd = (v.L < v.g) ? P.N : 0;
+    const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
+    const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
+    const double* ss = P.segsum + (int64_t)b * P.nseg;
+    // Z = sum of the segment masses in segment order: lanes load, ordered warp scan
+    double Z = 0.0;
+    for (int64_t s0 = 0; s0 < P.nseg; s0 += 32) {
+      const double x = (s0 + lane < P.nseg) ? ss[s0 + lane] : 0.0;
+      Z += __shfl_sync(0xffffffffu, warp_sum_ordered(x), 31);
+    }
+    int kind = d.kind;
+    int64_t sstar = -1;
+    double tc = 0.0;
+    if (!(Z > 0.0) && (kind == kWResidual || kind == kWPoint)) {
+      // all mass cancelled: resample from o (reading #11); rare path, the warp recomputes
+      kind = kWProb;
+      deg = 1;
+      double acc = 0.0;
+      for (int64_t gi = lane; gi < P.ngroups; gi += 32) {
+        float w[8];
+        group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+        acc += (double)sum8(w);
+      }
+      Z = warp_sum(acc);
+      float mg = 0.f;
+      y = warp_scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, 0, P.ngroups, d.u * Z, Z, &mg);
+      margin = mg;
+    } else if (Z > 0.0) {
+      const double t = d.u * Z;
+      double O = 0.0;
+      for (int64_t s0 = 0; s0 < P.nseg && sstar < 0; s0 += 32) {
+        const double x = (s0 + lane < P.nseg) ? ss[s0 + lane] : 0.0;
+        const double incl = O + warp_sum_ordered(x);  // O + inclusive prefix, in segment order
+        const unsigned m = __ballot_sync(0xffffffffu, (s0 + lane < P.nseg) && incl > t);
+        if (m) {
+          const int src = __ffs(m) - 1;
+          sstar = s0 + src;
+          tc = t - __shfl_sync(0xffffffffu, incl - x, src);
+        }
+        O = __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (sstar >= 0) {
+        float mg = 0.f;
+        y = warp_scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sstar * kTileGroups,
+                                                   min(P.ngroups, (sstar + 1) * kTileGroups), tc, Z, &mg);
+        margin = mg;
+      }
+    }
+    zmass = (float)((kind == kWBonus) ? Z * (double)d.invS : Z);
+  }
+  for (int j = lane; j <= P.k; j += 32) out[j] = (j < v.L) ? pds[j].xstar : (j == v.L ? (int32_t)y : -1);
+  if (lane == 0) {
+    P.accept_len[b] = v.L;
+    const float tm = fmin_(v.tm, margin);
+    P.status[b] = (deg ? COSINE_INFO_DEGENERATE_RESIDUAL : 0) | (tm < 1e-6f ? COSINE_INFO_NEAR_TIE : 0) |
+                  (y < 0 ? 0xff : 0);
+    if (P.dbg.residual_mass) P.dbg.residual_mass[b] = zmass;
+    if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
+  }
+}
+
+}  // namespace cosine

@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
 }
 
 }  // namespace cosine
-#include "cosine_stream.cuh"
+#include "cosine_split.cuh"
 namespace cosine {
 
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
@@ -1075,20 +1075,29 @@ __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
 }
 
 using KernelFn = void (*)(Params);
-using StreamFn = void (*)(StreamParams);
+using SplitFn = void (*)(SplitParams);
+constexpr int kMaxChunks = 8;
 
 template <typename TT, typename TQ>
-StreamFn pick_stream2(bool logits, int N) {
-  if (logits) return N <= 4 ? stream_kernel<TT, TQ, true, 4> : stream_kernel<TT, TQ, true, 8>;
-  return N <= 4 ? stream_kernel<TT, TQ, false, 4> : stream_kernel<TT, TQ, false, 8>;
+void pick_split2(bool logits, int N, SplitFn* f) {
+  if (logits) {
+    f[0] = N <= 4 ? stats_kernel<TT, TQ, true, 4> : stats_kernel<TT, TQ, true, 8>;
+    f[1] = decide_kernel<TT, TQ, true>;
+    f[2] = N <= 4 ? segsum_kernel<TT, TQ, true, 4> : segsum_kernel<TT, TQ, true, 8>;
+    f[3] = N <= 4 ? finish_kernel<TT, TQ, true, 4> : finish_kernel<TT, TQ, true, 8>;
+  } else {
+    f[0] = N <= 4 ? stats_kernel<TT, TQ, false, 4> : stats_kernel<TT, TQ, false, 8>;
+    f[1] = decide_kernel<TT, TQ, false>;
+    f[2] = N <= 4 ? segsum_kernel<TT, TQ, false, 4> : segsum_kernel<TT, TQ, false, 8>;
+    f[3] = N <= 4 ? finish_kernel<TT, TQ, false, 4> : finish_kernel<TT, TQ, false, 8>;
+  }
 }
-StreamFn pick_stream(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N) {
-  if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_stream2<__nv_bfloat16, __nv_bfloat16>(logits, N);
-  if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_stream2<__nv_bfloat16, float>(logits, N);
-  if (tt == COSINE_F32 && tq == COSINE_BF16) return pick_stream2<float, __nv_bfloat16>(logits, N);
-  return pick_stream2<float, float>(logits, N);
+void pick_split(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, SplitFn* f) {
+  if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_split2<__nv_bfloat16, __nv_bfloat16>(logits, N, f);
+  if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_split2<__nv_bfloat16, float>(logits, N, f);
+  if (tt == COSINE_F32 && tq == COSINE_BF16) return pick_split2<float, __nv_bfloat16>(logits, N, f);
+  return pick_split2<float, float>(logits, N, f);
 }
-
 template <typename TT, typename TQ>
 KernelFn pick_kernel2(bool logits, int N) {
   if (logits) return N <= 4 ? unit_kernel<TT, TQ, true, 4> : unit_kernel<TT, TQ, true, 8>;
@@ -1112,6 +1121,12 @@ struct cosine_ctx_s {
   cosine_config_t cfg;
   int64_t V;
   UnitRec* recs = nullptr;
+  PartRec* parts = nullptr;
+  PosDec* pdec = nullptr;
+  double* segsum = nullptr;
+  size_t segsum_cap = 0;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev[kMaxChunks + 1] = {};
   int32_t* done = nullptr;
   int32_t* first_rej = nullptr;
   std::string err;
@@ -1146,7 +1161,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 size_t esize(cosine_dtype_t t) { return t == COSINE_BF16 ? 2 : 4; }
 
 int pick_cluster(const cosine_ctx_t ctx, int64_t units, int64_t ngroups) {
-  if (ctx->cfg.cluster_size > 0) return ctx->cfg.cluster_size;
+  if (ctx->cfg.cluster_size > 0) return std::min(ctx->cfg.cluster_size, 8);
   // ~8 groups (64 elements per row) per thread, then widen while the grid is small
   int C = 1;
   while (C < 8 && ngroups > (int64_t)C * kThreads * 8) C *= 2;
@@ -1187,77 +1202,74 @@ cosine_status_t launch(cosine_ctx_t ctx, cudaStream_t stream, Params& P, int64_t
   return COSINE_OK;
 }
 
-// Persistent kernel: pick the cluster size / cluster count that keeps every SM streaming
-// (max co-resident clusters from the occupancy API; requests are dealt round-robin).
-cosine_status_t launch_stream(cosine_ctx_t ctx, cudaStream_t stream, StreamParams& S,
-                              cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
-  StreamFn fn = pick_stream(tt, tq, logits, S.N);
-  const int tsz = (int)esize(tt), qsz = (int)esize(tq);
-  S.t_slot = kTileElems * tsz;
-  S.q_slot = kTileElems * qsz;
-  S.stage_bytes = S.t_slot + S.N * S.q_slot;
-  const int budget = 200 * 1024;
-  S.stages = std::min(kMaxStages, budget / S.stage_bytes);
-  if (S.stages < 2) return fail(ctx, COSINE_ERR_UNSUPPORTED, "stage does not fit in shared memory");
-  const size_t dsmem = (size_t)S.stages * S.stage_bytes;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
-  if (e != cudaSuccess) { cudaGetLastError(); return fail(ctx, COSINE_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e)); }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device);
-  int best_C = 0, best_ncl = 0;
-  double best_eff = -1.0;
-  const int cands[3] = {8, 4, 2};
-  for (int ci = 0; ci < 3; ++ci) {
-    const int C = cands[ci];
-    if (ctx->cfg.cluster_size > 0 && C != ctx->cfg.cluster_size) continue;
-    cudaLaunchConfig_t lc;
-    memset(&lc, 0, sizeof(lc));
-    lc.gridDim = dim3((unsigned)(C * 64), 1, 1);
-    lc.blockDim = dim3(kStreamThreads, 1, 1);
-    lc.dynamicSmemBytes = dsmem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    int maxcl = 0;
-    if (cudaOccupancyMaxActiveClusters(&maxcl, fn, &lc) != cudaSuccess || maxcl < 1) {
-      cudaGetLastError();
-      continue;
-    }
-    const int ncl = std::min(S.B, maxcl);
-    const int rounds = (S.B + ncl - 1) / ncl;
-    const double eff = (double)S.B / ((double)rounds * maxcl) * ((double)maxcl * C / sms);
-    if (eff > best_eff + 1e-9) { best_eff = eff; best_C = C; best_ncl = ncl; }
+// Kernel A (stats + decisions) then kernel B (first rejection + cooperative sample), the
+// latter launched with programmatic dependent launch so its launch overlaps A's tail.
+cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S,
+                             cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+  SplitFn fn[4];
+  pick_split(tt, tq, logits, S.N, fn);
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  // kernel A: ~8 groups (64 elements per row) per thread, at least ~8 CTAs per SM of work
+  int C = 1;
+  if (ctx->cfg.cluster_size > 0) {
+    C = ctx->cfg.cluster_size;
+  } else {
+    while (C < kMaxC && S.ngroups > (int64_t)C * kThreads * 8) C *= 2;
+    while (C < kMaxC && units * C < 148 * 8 && S.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
   }
-  if (best_C == 0) return fail(ctx, COSINE_ERR_CUDA, "no cluster configuration fits");
-  S.C = best_C;
-  S.ncl = best_ncl;
-  S.cgroups = (S.ngroups + S.C - 1) / S.C;
+  S.C = C;
+  S.cg = (S.ngroups + C - 1) / C;
+  S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
+  S.spr = (int)((S.nseg + kWarps - 1) / kWarps);
+  S.parts = ctx->parts;
+  S.pdec = ctx->pdec;
+  S.segsum = ctx->segsum;
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  // Batch pipelining: kernel A of chunk j+1 (HBM-bound) overlaps the latency-bound decision /
+  // sampling kernels of chunk j, which run on the context's high-priority internal stream.
+  int nch = std::max(1, std::min(kMaxChunks, S.B / 32));
+  const char* nc_env = getenv("COSINE_CHUNKS");
+  if (nc_env) nch = std::max(1, std::min(kMaxChunks, std::min(S.B, atoi(nc_env))));
   cudaLaunchConfig_t lc;
   memset(&lc, 0, sizeof(lc));
-  lc.gridDim = dim3((unsigned)(S.C * S.ncl), 1, 1);
-  lc.blockDim = dim3(kStreamThreads, 1, 1);
-  lc.dynamicSmemBytes = dsmem;
-  lc.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)S.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  e = cudaLaunchKernelEx(&lc, fn, S);
+  lc.blockDim = dim3(kThreads, 1, 1);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaError_t e = cudaSuccess;
+  int launches = 0;
+  for (int j = 0; j < nch && e == cudaSuccess; ++j) {
+    S.b_off = (int)((int64_t)S.B * j / nch);
+    S.nb = (int)((int64_t)S.B * (j + 1) / nch) - S.b_off;
+    const int64_t cu = (int64_t)S.nb * (S.k + 1);
+    lc.stream = stream;
+    lc.attrs = nullptr;
+    lc.numAttrs = 0;
+    lc.gridDim = dim3((unsigned)(cu * C), 1, 1);
+    e = cudaLaunchKernelEx(&lc, fn[0], S);  // A_j on the caller's stream
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[j], stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->ev[j], 0);
+    const unsigned grids[3] = {(unsigned)((cu + kWarps - 1) / kWarps), (unsigned)(S.nb * S.spr),
+                               (unsigned)((S.nb + kWarps - 1) / kWarps)};
+    lc.stream = ctx->aux;
+    for (int q = 0; q < 3 && e == cudaSuccess; ++q) {
+      lc.gridDim = dim3(grids[q], 1, 1);
+      lc.attrs = q ? at : nullptr;  // B2a, B2b: programmatic dependents of their predecessor
+      lc.numAttrs = q ? 1 : 0;
+      e = cudaLaunchKernelEx(&lc, fn[1 + q], S);
+    }
+    launches += 4;
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[kMaxChunks], ctx->aux);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ctx->ev[kMaxChunks], 0);  // join
   if (e != cudaSuccess) {
     cudaGetLastError();
     ctx->last_launches = 0;
-    return fail(ctx, COSINE_ERR_CUDA, std::string("stream kernel launch: ") + cudaGetErrorString(e));
+    return fail(ctx, COSINE_ERR_CUDA, std::string("verify kernels: ") + cudaGetErrorString(e));
   }
-  ctx->last_launches = 1;
-  ctx->last_cluster = S.C;
-  ctx->last_ncl = S.ncl;
+  ctx->last_launches = launches;
+  ctx->last_cluster = C;
   return COSINE_OK;
 }
 
@@ -1307,8 +1319,9 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad vocabulary range");
   if (cfg->vocab_end - cfg->vocab_begin > (int64_t)0x7fffffff)
     return fail(nullptr, COSINE_ERR_UNSUPPORTED, "vocabulary wider than 2^31 - 1");
-  if (cfg->max_batch < 0 || cfg->max_draft_len < 1 || cfg->max_drafters < 1 || cfg->max_drafters > kMaxN)
-    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad max_* sizes (max_drafters <= 8)");
+  if (cfg->max_batch < 0 || cfg->max_draft_len < 1 || cfg->max_draft_len > kMaxPos - 1 ||
+      cfg->max_drafters < 1 || cfg->max_drafters > kMaxN)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad max_* sizes (max_draft_len <= 64, max_drafters <= 8)");
   if ((cfg->target_dtype != COSINE_BF16 && cfg->target_dtype != COSINE_F32) ||
       (cfg->draft_dtype != COSINE_BF16 && cfg->draft_dtype != COSINE_F32))
     return fail(nullptr, COSINE_ERR_UNSUPPORTED, "dtype must be COSINE_BF16 or COSINE_F32");
@@ -1317,8 +1330,8 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   if (cfg->nranks != 1 || cfg->rank != 0 || cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab_size)
     return fail(nullptr, COSINE_ERR_UNSUPPORTED, "vocabulary sharding (nranks > 1) is not built in this version");
   if (cfg->cluster_size != 0 && cfg->cluster_size != 1 && cfg->cluster_size != 2 &&
-      cfg->cluster_size != 4 && cfg->cluster_size != 8)
-    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cluster_size must be 0, 1, 2, 4 or 8");
+      cfg->cluster_size != 4 && cfg->cluster_size != 8 && cfg->cluster_size != 16)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cluster_size must be 0, 1, 2, 4, 8 or 16");
   cosine_ctx_t ctx = new (std::nothrow) cosine_ctx_s();
   if (!ctx) return fail(nullptr, COSINE_ERR_OUT_OF_MEMORY, "host allocation failed");
   ctx->cfg = *cfg;
@@ -1329,6 +1342,18 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   cudaError_t e = cudaMalloc(&ctx->recs, nb * (size_t)(cfg->max_draft_len + 1) * sizeof(UnitRec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->done, nb * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->first_rej, nb * sizeof(int32_t));
+  const size_t nu = nb * (size_t)(cfg->max_draft_len + 1);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->parts, nu * kMaxC * sizeof(PartRec));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
+  ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
+  if (e == cudaSuccess) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi);
+  }
+  for (int j = 0; j <= kMaxChunks && e == cudaSuccess; ++j)
+    e = cudaEventCreateWithFlags(&ctx->ev[j], cudaEventDisableTiming);
   if (e == cudaSuccess) {
     init_scratch<<<(unsigned)((nb + 255) / 256), 256>>>(ctx->done, ctx->first_rej, (int)nb);
     e = cudaGetLastError();
@@ -1340,6 +1365,12 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     cudaFree(ctx->recs);
     cudaFree(ctx->done);
     cudaFree(ctx->first_rej);
+    cudaFree(ctx->parts);
+    cudaFree(ctx->pdec);
+    cudaFree(ctx->segsum);
+    for (int j = 0; j <= kMaxChunks; ++j)
+      if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     delete ctx;
     return fail(nullptr, e == cudaErrorMemoryAllocation ? COSINE_ERR_OUT_OF_MEMORY : COSINE_ERR_CUDA, msg);
   }
@@ -1354,6 +1385,12 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->recs);
   cudaFree(ctx->done);
   cudaFree(ctx->first_rej);
+  cudaFree(ctx->parts);
+  cudaFree(ctx->pdec);
+  cudaFree(ctx->segsum);
+  for (int j = 0; j <= kMaxChunks; ++j)
+    if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
   return COSINE_OK;
 }
@@ -1451,7 +1488,7 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   if (debug) P.dbg = *debug;
   const char* force_v2 = getenv("COSINE_FORCE_CLUSTER_KERNEL");
   if (select_mode == COSINE_SEL_ARGMAX && !(force_v2 && force_v2[0] == '1')) {
-    StreamParams S;
+    SplitParams S;
     memset(&S, 0, sizeof(S));
     S.B = B; S.k = k; S.N = N;
     S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
@@ -1459,10 +1496,8 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
     S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
     S.rids = request_ids; S.seed = P.seed; S.step = step;
     S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
-    const char* dflags = getenv("COSINE_DEBUG_FLAGS");
-    S.debug_flags = dflags ? atoi(dflags) : 0;
-    return launch_stream(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
-                         ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+    return launch_split(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                        ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
   }
   return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
                 ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);

@@ -1,0 +1,70 @@
+"""Helpers shared by the GPU parity tests: run the CUDA path and the oracle on the same
+seeded inputs and compare (test infrastructure; imports the oracle)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+
+TIE = 1e-6        # north_star: ties within 1e-6 of a threshold are flagged, not failures
+PROB_RTOL = 1e-5  # north_star: probabilities within 1e-5 relative (fp32)
+
+
+def gpu_verify(inp, *, T=1.0, seed=7, step=0, wm=0, sm=0, draft_kind="probs", cluster_size=0,
+               device=0, subset=None):
+    import paper_2503_10325_b200 as cv
+    tgt, drf = inp["target"], inp["draft"]
+    B, kp1, _ = tgt.shape
+    N = drf.shape[2]
+    dev = torch.device("cuda", device)
+    ver = cv.Verifier(inp["V"], max_batch=B, k=kp1 - 1, N=N, device=device, target_dtype=tgt.dtype,
+                      draft_dtype=drf.dtype, seed=seed, debug=True, cluster_size=cluster_size,
+                      draft_kind=cv.DRAFT_LOGITS if draft_kind == "logits" else cv.DRAFT_PROBS)
+    d = {n: (t.to(dev) if torch.is_tensor(t) else t) for n, t in inp.items()}
+    a, o, s = ver.verify(d["target"], d["draft"], d["draft_tokens"], d["request_ids"], temperature=T,
+                         draft_len=d["draft_len"], step=step, weight_mode=wm, select_mode=sm)
+    torch.cuda.synchronize()
+    out = dict(accept_len=a.cpu().numpy().copy(), out_tokens=o.cpu().numpy().copy(),
+               status=s.cpu().numpy().copy(), launches=cv.cosine_last_launch_count(ver.ctx))
+    for n, t in ver.debug.items():
+        out[n] = t[:B].cpu().numpy().copy()
+    ver.close()
+    return out
+
+
+def oracle_verify(inp, *, T=1.0, seed=7, step=0, wm=0, sm=0, draft_kind="probs", subset=None):
+    sel = slice(None) if subset is None else subset
+    dl = inp["draft_len"]
+    return oracle.verify_batch(inp["target"][sel].cpu(), inp["draft"][sel].cpu(),
+                               inp["draft_tokens"][sel].cpu(), inp["request_ids"][sel].cpu(),
+                               temperature=T, seed=seed, step=step,
+                               draft_len=None if dl is None else dl[sel].cpu(),
+                               draft_kind=oracle.DRAFT_LOGITS if draft_kind == "logits" else oracle.DRAFT_PROBS,
+                               weight_mode=wm, select_mode=sm, vocab=inp["V"])
+
+
+def compare(g, r, subset=None, check_probs=True, greedy=False):
+    """Bit-exact accept_len / out_tokens / status except where the oracle flags a near tie."""
+    idx = np.arange(len(r["accept_len"])) if subset is None else np.asarray(subset)
+    ga, go, gs = g["accept_len"][idx], g["out_tokens"][idx], g["status"][idx]
+    assert (gs & 0xff == r["status"] & 0xff).all(), (gs, r["status"])
+    mism = np.nonzero((ga != r["accept_len"]) | (go != r["out_tokens"]).any(1))[0]
+    flagged = r["tie_margin"] < TIE
+    bad = [int(b) for b in mism if not flagged[b]]
+    assert not bad, f"unflagged mismatches at {bad[:5]}: gpu {ga[bad[0]]} {go[bad[0]]} " \
+                    f"oracle {r['accept_len'][bad[0]]} {r['out_tokens'][bad[0]]} margin {r['tie_margin'][bad[0]]}"
+    if check_probs:
+        ok = (r["status"] & 0xff) == 0
+        pairs = [("q_x", "q_x"), ("draft_norm", "sigma"), ("conf", "conf"), ("weights", "weights")]
+        if not greedy:  # T = 0 has no softmax statistics
+            pairs += [("p_x", "p_x"), ("row_sumexp", "S")]
+        for gk, rk in pairs:
+            gv, rv = g[gk][idx][ok], r[rk][ok]
+            m = np.isfinite(rv) & (np.abs(rv) > 1e-30)
+            if rk == "S":
+                m &= rv > 0
+            if m.any():
+                rel = np.abs(gv[m] - rv[m]) / np.abs(rv[m])
+                assert rel.max() < PROB_RTOL, f"{gk}: max rel err {rel.max():.3g}"
+    return len(mism), int(flagged.sum())
