@@ -179,6 +179,13 @@ cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream,
 /* Number of kernels the last successful call on ctx enqueued (for launch accounting). */
 int32_t cosine_last_launch_count(cosine_ctx_t ctx);
 
+/* Live timing of the dominant kernel (the streaming statistics kernel of cosine_verify_batch):
+ * when enabled, every verify call brackets it with CUDA events on the caller's stream.
+ * cosine_profile_read synchronises on them, returns the summed duration (ms) and the number of
+ * bracketed launches since the last read / enable, and resets the accumulator. */
+cosine_status_t cosine_profile_enable(cosine_ctx_t ctx, int32_t enable);
+cosine_status_t cosine_profile_read(cosine_ctx_t ctx, double* total_ms, int32_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,8 +13,8 @@ from . import _lib
 from ._lib import (  # noqa: F401
     BF16, F32, DRAFT_LOGITS, DRAFT_PROBS, INFO_DEGENERATE, INFO_NEAR_TIE, SEL_ARGMAX, SEL_SAMPLE,
     W_CONF, W_POINT, W_UNIFORM, W_WINNER, Context, CosineError, cosine_fuse_drafts,
-    cosine_last_launch_count, cosine_sample_residual, cosine_verify_batch, cosine_verify_destroy,
-    cosine_verify_init,
+    cosine_last_launch_count, cosine_profile_enable, cosine_profile_read, cosine_sample_residual,
+    cosine_verify_batch, cosine_verify_destroy, cosine_verify_init,
 )
 
 __all__ = [

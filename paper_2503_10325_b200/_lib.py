@@ -69,9 +69,14 @@ _lib.cosine_sample_residual.argtypes = [_P, _P, _i32, _P, _i64, _f32, _P, _P, _P
                                         _i32, _P, _P, _u32, _P, _P]
 _lib.cosine_sample_residual.restype = ctypes.c_int
 
+_lib.cosine_profile_enable.argtypes = [_P, _i32]
+_lib.cosine_profile_enable.restype = ctypes.c_int
+_lib.cosine_profile_read.argtypes = [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]
+_lib.cosine_profile_read.restype = ctypes.c_int
+
 EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_error",
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
-                    "cosine_last_launch_count")
+                    "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read")
 
 
 class CosineError(RuntimeError):
@@ -131,6 +136,18 @@ def cosine_verify_destroy(ctx) -> None:
 
 def cosine_last_launch_count(ctx) -> int:
     return int(_lib.cosine_last_launch_count(ctx))
+
+
+def cosine_profile_enable(ctx, enable: bool = True) -> None:
+    _check(_lib.cosine_profile_enable(ctx, int(bool(enable))), ctx)
+
+
+def cosine_profile_read(ctx):
+    """-> (summed ms of the bracketed stats-kernel launches, number of launches)."""
+    t = ctypes.c_double()
+    n = _i32()
+    _check(_lib.cosine_profile_read(ctx, ctypes.byref(t), ctypes.byref(n)), ctx)
+    return t.value, n.value
 
 
 def cosine_fuse_drafts(ctx, draft, draft_tokens, request_ids, fused_tokens, status, *, step=0,

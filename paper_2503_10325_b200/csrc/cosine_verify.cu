@@ -24,6 +24,8 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "cosine_kernels.cuh"
 #include "cosine_verify.h"
@@ -1127,6 +1129,10 @@ struct cosine_ctx_s {
   size_t segsum_cap = 0;
   cudaStream_t aux = nullptr;
   cudaEvent_t ev[kMaxChunks + 1] = {};
+  // optional live timing of the dominant kernel (stats_kernel) with CUDA events on the stream
+  int prof_on = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+  size_t prof_n = 0;
   int32_t* done = nullptr;
   int32_t* first_rej = nullptr;
   std::string err;
@@ -1228,7 +1234,7 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
   // Batch pipelining: kernel A of chunk j+1 (HBM-bound) overlaps the latency-bound decision /
   // sampling kernels of chunk j, which run on the context's high-priority internal stream.
-  int nch = std::max(1, std::min(kMaxChunks, S.B / 32));
+  int nch = 1;  // batch pipelining measured no gain on B200 (kernel A saturates every slot)
   const char* nc_env = getenv("COSINE_CHUNKS");
   if (nc_env) nch = std::max(1, std::min(kMaxChunks, std::min(S.B, atoi(nc_env))));
   cudaLaunchConfig_t lc;
@@ -1247,7 +1253,21 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
     lc.attrs = nullptr;
     lc.numAttrs = 0;
     lc.gridDim = dim3((unsigned)(cu * C), 1, 1);
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (ctx->prof_on) {
+      if (ctx->prof_n == ctx->prof_ev.size()) {
+        cudaEvent_t a0, a1;
+        cudaEventCreate(&a0);
+        cudaEventCreate(&a1);
+        ctx->prof_ev.emplace_back(a0, a1);
+      }
+      pe0 = ctx->prof_ev[ctx->prof_n].first;
+      pe1 = ctx->prof_ev[ctx->prof_n].second;
+      ctx->prof_n++;
+      cudaEventRecord(pe0, stream);
+    }
     e = cudaLaunchKernelEx(&lc, fn[0], S);  // A_j on the caller's stream
+    if (pe1) cudaEventRecord(pe1, stream);
     if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[j], stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->ev[j], 0);
     const unsigned grids[3] = {(unsigned)((cu + kWarps - 1) / kWarps), (unsigned)(S.nb * S.spr),
@@ -1391,6 +1411,10 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   for (int j = 0; j <= kMaxChunks; ++j)
     if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  for (auto& pe : ctx->prof_ev) {
+    cudaEventDestroy(pe.first);
+    cudaEventDestroy(pe.second);
+  }
   delete ctx;
   return COSINE_OK;
 }
@@ -1400,6 +1424,32 @@ const char* cosine_last_error(cosine_ctx_t ctx) {
 }
 
 int32_t cosine_last_launch_count(cosine_ctx_t ctx) { return ctx ? ctx->last_launches : 0; }
+
+cosine_status_t cosine_profile_enable(cosine_ctx_t ctx, int32_t enable) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  ctx->prof_on = enable ? 1 : 0;
+  ctx->prof_n = 0;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_profile_read(cosine_ctx_t ctx, double* total_ms, int32_t* launches) {
+  if (!ctx || !total_ms || !launches) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard dg(ctx->cfg.device);
+  double t = 0.0;
+  for (size_t j = 0; j < ctx->prof_n; ++j) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->prof_ev[j].second) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, ctx->prof_ev[j].first, ctx->prof_ev[j].second) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, COSINE_ERR_CUDA, "profile events not recorded");
+    }
+    t += ms;
+  }
+  *total_ms = t;
+  *launches = (int32_t)ctx->prof_n;
+  ctx->prof_n = 0;
+  return COSINE_OK;
+}
 
 cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
                                    int32_t N, const void* draft, int64_t ld_q,
