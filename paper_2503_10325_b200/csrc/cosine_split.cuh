@@ -51,6 +51,7 @@ struct SplitParams {
   cosine_debug_t dbg;
   PartRec* parts;
   struct PosDec* pdec;
+  int32_t* counters;  // [B] CTAs of a request done (kernel B), reset by the last one
   double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
   int64_t nseg;
   int spr;         // B2a CTAs per request
@@ -328,22 +329,15 @@ struct PosDec {  // decisions of one position (shared memory of every CTA of the
   float sig[kMaxN], c[kMaxN], w[kMaxN];
 };
 
-// Kernel B1: one warp per (request, position).  The warp combines the C partial records
-// (lane r owns chunk r; fixed-order shuffle reductions), loads the candidate gathers (one lane
-// each), then lane 0 takes the position's decisions.
+// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131):
+// lane r combines chunk r's partial record (fixed-order shuffle reductions, fp64), lanes gather
+// o(X_n) and q_m(X_n), lane 0 writes the decision to *out (and the diagnostics if asked).
 template <typename TT, typename TQ, bool kLogits>
-__global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t lunit = (int64_t)blockIdx.x * kWarps + warp;
-  const int64_t unit = (int64_t)P.b_off * (P.k + 1) + lunit;
+__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
+                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
+  const int lane = threadIdx.x & 31;
   const int N = P.N, C = P.C;
-  __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
-  __shared__ int32_t s_tok[kWarps][kMaxN];
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel A's partial records (PDL)
-  if (lunit >= (int64_t)P.nb * (P.k + 1)) return;
-  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
-  const int g = P.draft_len ? P.draft_len[b] : P.k;
-  if (g < 1 || g > P.k || i > g) return;
+  const int64_t unit = (int64_t)b * (P.k + 1) + i;
   const bool has_d = i < g;
   const bool greedy = P.greedy != 0;
   const double k2 = (double)P.k2f;
@@ -356,8 +350,8 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
       if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
       else v = load_one((const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t, tk);
     }
-    s_gx[warp][m * kMaxN + n] = v;
-    if (m == 0) s_tok[warp][n] = tk;
+    s_gxw[m * kMaxN + n] = v;
+    if (m == 0) s_tokw[n] = tk;
   }
   // ---- combine the partial records (chunk r in lane r) ----
   const PartRec* parts = P.parts + unit * C;
@@ -410,8 +404,8 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   }
   __syncwarp();
   if (lane != 0) return;
-  const float* gx = s_gx[warp];
-  const int32_t* tok = s_tok[warp];
+  const float* gx = s_gxw;
+  const int32_t* tok = s_tokw;
   if (has_d)
     for (int n = 0; n < N; ++n)
       if (tok[n] < 0 || (int64_t)tok[n] >= P.V) tok_bad = true;
@@ -475,7 +469,8 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
       pd.w[n] = (float)w[n];
     }
   }
-  P.pdec[unit] = pd;
+  *out = pd;
+  if (!write_debug) return;
   const cosine_debug_t& D = P.dbg;
   if (D.row_max) D.row_max[unit] = pd.M;
   if (D.row_sumexp) D.row_sumexp[unit] = greedy ? 0.f : (float)pd.S;
@@ -493,68 +488,50 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   }
 }
 
-// The request-level view of B1's decisions (first error, first rejection L, margins).
+// Kernel B1: one warp per (request, position) -> PosDec in global memory (+ diagnostics).
+template <typename TT, typename TQ, bool kLogits>
+__global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
+  __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kWarps][kMaxN];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel A's partial records (PDL)
+  if (unit >= (int64_t)P.B * (P.k + 1)) return;
+  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (g < 1 || g > P.k || i > g) return;
+  warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[unit], true);
+}
+
+// The request-level view of the position decisions (first error, first rejection L, margins).
 struct ReqView {
   int32_t g, err, L, sample;  // sample: T > 0 and no error -> a final inverse-CDF draw at row L
   float tm;
 };
-// Inclusive prefix sum over the lanes, accumulated strictly left to right (lane order), so
-// every lane's partial equals the sequential sum of segments 0..lane.
-__device__ __forceinline__ double warp_sum_ordered(double x) {
-  const int lane = threadIdx.x & 31;
-  double acc = 0.0, r = 0.0;
-  for (int l = 0; l < 32; ++l) {
-    acc += __shfl_sync(0xffffffffu, x, l);
-    if (l == lane) r = acc;
-  }
-  return r;
-}
-
-// Warp-cooperative: lane j reads position j's decision (one L2 round trip, not k+1).
-__device__ __forceinline__ ReqView request_view(const SplitParams& P, int b) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ ReqView request_view(const SplitParams& P, const PosDec* pds, int g) {
   ReqView v;
-  v.g = P.draft_len ? P.draft_len[b] : P.k;
+  v.g = g;
   v.err = 0;
-  v.L = v.g;
+  v.L = g;
   v.tm = INFINITY;
-  v.sample = 0;
-  if (v.g < 1 || v.g > P.k) { v.err = COSINE_REQ_BAD_DRAFT_LEN; return v; }
-  const PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
-  int err = 0, L = v.g;
-  for (int j0 = 0; j0 <= v.g; j0 += 32) {  // positions in rounds of 32 (k <= 64)
-    const int j = j0 + lane;
-    const bool in = j <= v.g;
-    const int st = in ? pds[j].status : 0;
-    const bool rej = in && j < v.g && !pds[j].accept;
-    const unsigned me = __ballot_sync(0xffffffffu, st != 0);
-    const unsigned mr = __ballot_sync(0xffffffffu, rej);
-    if (!err && me) err = __shfl_sync(0xffffffffu, st, __ffs(me) - 1);
-    if (L == v.g && mr) L = j0 + __ffs(mr) - 1;
-  }
-  float tm = INFINITY;
-  for (int j0 = 0; j0 <= L; j0 += 32) {
-    const int j = j0 + lane;
-    tm = fmin_(tm, (j <= L) ? pds[j].m_fa : INFINITY);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tm = fminf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-  v.err = err;
-  v.L = L;
-  v.tm = tm;
-  v.sample = (!err && !P.greedy) ? 1 : 0;
+  for (int j = 0; j <= g; ++j)
+    if (!v.err && pds[j].status) v.err = pds[j].status;
+  for (int j = 0; j < g; ++j)
+    if (!pds[j].accept) { v.L = j; break; }
+  for (int j = 0; j <= v.L; ++j) v.tm = fmin_(v.tm, pds[j].m_fa);
+  v.sample = (!v.err && !P.greedy) ? 1 : 0;
   return v;
 }
 
-__device__ __forceinline__ Decision sample_decision(const SplitParams& P, int b, const ReqView& v) {
-  const PosDec& pl = P.pdec[(int64_t)b * (P.k + 1) + v.L];
+__device__ __forceinline__ Decision sample_decision(const SplitParams& P, uint64_t rid, const PosDec& pl,
+                                                    const ReqView& v) {
   const bool resid = v.L < v.g;
   Decision d;
   d.need = 1;
   d.kind = resid ? ((P.weight_mode == COSINE_W_POINT) ? kWPoint : kWResidual) : kWBonus;
   d.xstar = pl.xstar;
   d.node = (uint32_t)v.L;
-  d.u = philox_u24(P.seed, P.rids[b], (uint32_t)v.L, P.step, kTagSample);
+  d.u = philox_u24(P.seed, rid, (uint32_t)v.L, P.step, kTagSample);
   d.M = pl.M;
   d.invS = (float)(1.0 / pl.S);
   d.k2 = P.k2f;
@@ -562,125 +539,227 @@ __device__ __forceinline__ Decision sample_decision(const SplitParams& P, int b,
   return d;
 }
 
-// Kernel B2a: residual / bonus mass of every 256-group segment of the sampled row.
-// One warp per segment (2048 vocabulary entries), lane-strided 128-bit loads.
+// Raw (1 + N) row groups of one vocabulary group, loaded before any arithmetic so that every
+// load of an iteration is in flight together (the weights are computed afterwards).
+template <typename TT, typename TQ, int NMAX>
+struct RowGroups {
+  Group<TT> t;
+  Group<TQ> d[NMAX];
+  __device__ __forceinline__ void load(const TT* trow, const TQ* drow, int64_t ld_q, int Nd, bool need_t,
+                                       bool need_q, int64_t gi) {
+    if (need_t) t.load(trow, gi);
+    if (need_q) {
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n)
+        if (n < Nd) d[n].load(drow + (int64_t)n * ld_q, gi);
+    }
+  }
+};
+
+// Sampling weights of a FULL group from already-loaded rows (same arithmetic as group_weights).
 template <typename TT, typename TQ, bool kLogits, int NMAX>
-__global__ void __launch_bounds__(kThreads, 4) segsum_kernel(const SplitParams P) {
+__device__ __forceinline__ float group_mass(const RowGroups<TT, TQ, NMAX>& rg, const Decision& d, int kind,
+                                            int Nd, int64_t gi) {
+  float q[8], t[8], w[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) q[e] = 0.f;
+  const bool need_q = (kind == kWResidual);
+  if (need_q) {
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n < Nd) {
+        float f[8];
+        rg.d[n].unpack(f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float qv = kLogits ? ex2((f[e] - d.dm[n]) * d.k2) : f[e];
+          q[e] = fmaf(d.a[n], qv, q[e]);
+        }
+      }
+    }
+  }
+  rg.t.unpack(t);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float pe = ex2((t[e] - d.M) * d.k2);
+    float x;
+    if (kind == kWBonus) {
+      x = pe;
+    } else {
+      const float p = pe * d.invS;
+      if (kind == kWResidual) x = fmaxf(p - q[e], 0.f);
+      else if (kind == kWPoint) x = (gi * kGroup + e == (int64_t)d.xstar) ? fmaxf(p - 1.f, 0.f) : p;
+      else x = p;  // kWProb
+    }
+    w[e] = x;
+  }
+  return sum8(w);
+}
+
+// Kernel B2 (resample_kernel): CTA (request b, block of kSegTilesPerCta 2048-entry tiles).
+//  1. it reads the request's position decisions (kernel B1) and derives the first rejection L
+//     (P:132);
+//  2. the CTA streams its tiles of the (1+N) rows at L — same mapping as kernel A, two tiles of
+//     loads in flight — and writes each tile's residual (or bonus) mass;
+//  3. the LAST CTA of the request (device-scope counter) sums the tile masses in tile order,
+//     finds the crossing tile, scans it block-wide (reading #10) and writes the outputs.
+constexpr int kSegTilesPerCta = 8;
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
-  const int64_t seg = (int64_t)(blockIdx.x % P.spr) * kWarps + warp;
+  const int part = blockIdx.x % P.spr;
+  const int64_t tile0 = (int64_t)part * kSegTilesPerCta;
+  __shared__ __align__(16) PosDec s_pd[kMaxPos];
   __shared__ ReqView s_v;
   __shared__ Decision s_d;
+  __shared__ double s_red[kWarps][kSegTilesPerCta];
+  __shared__ double s_scan[kWarps];
+  __shared__ int64_t s_wi[kWarps];
+  __shared__ int64_t s_found;
+  __shared__ float s_margin;
+  __shared__ int s_last;
+
   asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B1's decisions (PDL)
-  if (warp == 0) {
-    const ReqView v = request_view(P, b);
-    if (lane == 0) {
-      s_v = v;
-      if (v.sample) s_d = sample_decision(P, b, v);
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
+  if (g < 1 || g > P.k) {
+    if (part == 0 && tid == 0) {
+      P.accept_len[b] = -1;
+      for (int j = 0; j <= P.k; ++j) out[j] = -1;
+      P.status[b] = COSINE_REQ_BAD_DRAFT_LEN;
     }
+    return;
+  }
+  const uint64_t rid = P.rids[b];
+  const PosDec* gpd = P.pdec + (int64_t)b * (P.k + 1);
+  // the request's decisions (kernel B1): positions 0..g, one round of loads
+  {
+    const int nw = (int)(sizeof(PosDec) / 4);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(gpd);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(s_pd);
+    for (int w = tid; w < (g + 1) * nw; w += kThreads) dst[w] = src[w];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const ReqView v = request_view(P, s_pd, g);
+    s_v = v;
+    if (v.sample) s_d = sample_decision(P, rid, s_pd[v.L], v);
   }
   __syncthreads();
   const ReqView v = s_v;
-  if (!v.sample || seg >= P.nseg) return;
-  const Decision d = s_d;
-  const int Nd = (v.L < v.g) ? P.N : 0;
-  const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
-  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
-  const int64_t g0 = seg * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
-  double acc = 0.0;
-  for (int64_t gi = g0 + lane; gi < g1; gi += 64) {  // two groups of loads in flight per lane
-    float w0[8], w1[8];
-    const bool two = gi + 32 < g1;
-    group_weights<TT, TQ, kLogits, NMAX>(P, d, d.kind, trow, drow, Nd, gi, w0);
-    if (two) group_weights<TT, TQ, kLogits, NMAX>(P, d, d.kind, trow, drow, Nd, gi + 32, w1);
-    acc += (double)sum8(w0);
-    if (two) acc += (double)sum8(w1);
-  }
-  acc = warp_sum(acc);
-  if (lane == 0) P.segsum[(int64_t)b * P.nseg + seg] = acc;
-}
-
-// Kernel B2b: one warp per request: Z = sum of the segment masses (segment order), the
-// crossing segment, a warp scan of that segment only; then the request's outputs.
-template <typename TT, typename TQ, bool kLogits, int NMAX>
-__global__ void __launch_bounds__(kThreads) finish_kernel(const SplitParams P) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B2a's segment masses (PDL)
-  const int bl = blockIdx.x * kWarps + warp;
-  if (bl >= P.nb) return;
-  const int b = P.b_off + bl;
-  const ReqView v = request_view(P, b);
-  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
-  const PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
-  if (v.err) {
-    for (int j = lane; j <= P.k; j += 32) out[j] = -1;
-    if (lane == 0) { P.accept_len[b] = -1; P.status[b] = v.err; }
+  if (!v.sample) {  // a per-request error, or greedy (y = argmax of row L, reading #7)
+    if (part == 0) {
+      for (int j = tid; j <= P.k; j += kThreads)
+        out[j] = v.err ? -1 : ((j < v.L) ? s_pd[j].xstar : (j == v.L ? (int32_t)s_pd[v.L].amax : -1));
+      if (tid == 0) {
+        P.accept_len[b] = v.err ? -1 : v.L;
+        P.status[b] = v.err ? v.err : ((v.tm < 1e-6f) ? COSINE_INFO_NEAR_TIE : 0);
+        if (!v.err && P.dbg.tie_margin) P.dbg.tie_margin[b] = v.tm;
+      }
+    }
     return;
   }
-  int64_t y = -1;
-  float margin = INFINITY, zmass = NAN;
-  int deg = 0;
-  if (!v.sample) {
-    y = pds[v.L].amax;  // greedy: argmax of row L (reading #7)
-  } else {
-    const Decision d = sample_decision(P, b, v);
-    const int Nd = (v.L < v.g) ? P.N : 0;
-    const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
-    const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
-    const double* ss = P.segsum + (int64_t)b * P.nseg;
-    // Z = sum of the segment masses in segment order: lanes load, ordered warp scan
-    double Z = 0.0;
-    for (int64_t s0 = 0; s0 < P.nseg; s0 += 32) {
-      const double x = (s0 + lane < P.nseg) ? ss[s0 + lane] : 0.0;
-      Z += __shfl_sync(0xffffffffu, warp_sum_ordered(x), 31);
+  const Decision d = s_d;
+  const int kind0 = d.kind;
+  const int Nd = (v.L < v.g) ? P.N : 0;
+  const bool need_q = (kind0 == kWResidual);
+  const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
+  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
+  const int ntiles = (int)min((int64_t)kSegTilesPerCta, P.nseg - tile0);
+#pragma unroll 1
+  for (int j = 0; j < ntiles; ++j) {  // one tile of (1+N) loads per thread in flight
+    const int64_t g0 = (tile0 + j) * kTileGroups + tid;
+    double m0 = 0.0;
+    if (g0 < P.gfull) {
+      RowGroups<TT, TQ, NMAX> r0;
+      r0.load(trow, drow, P.ld_q, Nd, true, need_q, g0);
+      m0 = (double)group_mass<TT, TQ, kLogits, NMAX>(r0, d, kind0, Nd, g0);
+    } else if (g0 < P.ngroups) {  // the row's partial last group
+      float w[8];
+      group_weights<TT, TQ, kLogits, NMAX>(P, d, kind0, trow, drow, Nd, g0, w);
+      m0 = (double)sum8(w);
     }
-    int kind = d.kind;
-    int64_t sstar = -1;
+    m0 = warp_sum(m0);
+    if (lane == 0) s_red[warp][j] = m0;
+  }
+  __syncthreads();
+  if (tid < ntiles) {
+    double z = 0.0;
+    for (int w = 0; w < kWarps; ++w) z += s_red[w][tid];
+    P.segsum[(int64_t)b * P.nseg + tile0 + tid] = z;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int old = atomicAdd(&P.counters[b], 1);
+    s_last = (old == P.spr - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---------------- the last CTA of the request: crossing tile, scan, outputs ----------------
+  __threadfence();
+  __shared__ int64_t s_tstar;
+  __shared__ double s_tc, s_Z;
+  __shared__ int s_kind, s_deg;
+  if (tid == 0) {
+    P.counters[b] = 0;  // ready for the next call
+    const double* ss = P.segsum + (int64_t)b * P.nseg;
+    double Z = 0.0;
+    for (int64_t t = 0; t < P.nseg; ++t) Z += __ldcg(ss + t);
+    int kind = kind0, dg = 0;
+    int64_t tstar = -1;
     double tc = 0.0;
     if (!(Z > 0.0) && (kind == kWResidual || kind == kWPoint)) {
-      // all mass cancelled: resample from o (reading #11); rare path, the warp recomputes
-      kind = kWProb;
-      deg = 1;
-      double acc = 0.0;
-      for (int64_t gi = lane; gi < P.ngroups; gi += 32) {
-        float w[8];
-        group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
-        acc += (double)sum8(w);
-      }
-      Z = warp_sum(acc);
-      float mg = 0.f;
-      y = warp_scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, 0, P.ngroups, d.u * Z, Z, &mg);
-      margin = mg;
+      kind = kWProb;  // all mass cancelled: resample from o (reading #11)
+      dg = 1;
     } else if (Z > 0.0) {
       const double t = d.u * Z;
       double O = 0.0;
-      for (int64_t s0 = 0; s0 < P.nseg && sstar < 0; s0 += 32) {
-        const double x = (s0 + lane < P.nseg) ? ss[s0 + lane] : 0.0;
-        const double incl = O + warp_sum_ordered(x);  // O + inclusive prefix, in segment order
-        const unsigned m = __ballot_sync(0xffffffffu, (s0 + lane < P.nseg) && incl > t);
-        if (m) {
-          const int src = __ffs(m) - 1;
-          sstar = s0 + src;
-          tc = t - __shfl_sync(0xffffffffu, incl - x, src);
-        }
-        O = __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (sstar >= 0) {
-        float mg = 0.f;
-        y = warp_scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sstar * kTileGroups,
-                                                   min(P.ngroups, (sstar + 1) * kTileGroups), tc, Z, &mg);
-        margin = mg;
+      for (int64_t s2 = 0; s2 < P.nseg; ++s2) {
+        const double z = __ldcg(ss + s2);
+        if (O + z > t) { tstar = s2; tc = t - O; break; }
+        O += z;
       }
     }
-    zmass = (float)((kind == kWBonus) ? Z * (double)d.invS : Z);
+    s_Z = Z;
+    s_kind = kind;
+    s_deg = dg;
+    s_tstar = tstar;
+    s_tc = tc;
   }
-  for (int j = lane; j <= P.k; j += 32) out[j] = (j < v.L) ? pds[j].xstar : (j == v.L ? (int32_t)y : -1);
-  if (lane == 0) {
+  __syncthreads();
+  const int kind = s_kind, deg = s_deg;
+  double Z = s_Z;
+  int64_t y = -1;
+  float margin = INFINITY;
+  if (deg) {  // rare: the whole row from o, block-wide
+    double acc = 0.0;
+    for (int64_t gi = tid; gi < P.ngroups; gi += kThreads) {
+      float w[8];
+      group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
+      acc += (double)sum8(w);
+    }
+    Z = block_sum(acc, s_scan);
+    if (tid == 0) s_Z = Z;
+    __syncthreads();
+    Z = s_Z;
+    y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, 0, P.ngroups, d.u * Z, Z, s_scan,
+                                          s_wi, &s_found, &s_margin);
+    margin = s_margin;
+  } else if (s_tstar >= 0) {
+    const int64_t sb = s_tstar * kTileGroups;
+    y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sb, min(P.ngroups, sb + kTileGroups),
+                                          s_tc, Z, s_scan, s_wi, &s_found, &s_margin);
+    margin = s_margin;
+  }
+  for (int j = tid; j <= P.k; j += kThreads) out[j] = (j < v.L) ? s_pd[j].xstar : (j == v.L ? (int32_t)y : -1);
+  if (tid == 0) {
     P.accept_len[b] = v.L;
     const float tm = fmin_(v.tm, margin);
     P.status[b] = (deg ? COSINE_INFO_DEGENERATE_RESIDUAL : 0) | (tm < 1e-6f ? COSINE_INFO_NEAR_TIE : 0) |
                   (y < 0 ? 0xff : 0);
-    if (P.dbg.residual_mass) P.dbg.residual_mass[b] = zmass;
+    if (P.dbg.residual_mass) P.dbg.residual_mass[b] = (float)((kind == kWBonus) ? Z * (double)d.invS : Z);
     if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
   }
 }

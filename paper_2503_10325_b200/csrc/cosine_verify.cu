@@ -1085,13 +1085,11 @@ void pick_split2(bool logits, int N, SplitFn* f) {
   if (logits) {
     f[0] = N <= 4 ? stats_kernel<TT, TQ, true, 4> : stats_kernel<TT, TQ, true, 8>;
     f[1] = decide_kernel<TT, TQ, true>;
-    f[2] = N <= 4 ? segsum_kernel<TT, TQ, true, 4> : segsum_kernel<TT, TQ, true, 8>;
-    f[3] = N <= 4 ? finish_kernel<TT, TQ, true, 4> : finish_kernel<TT, TQ, true, 8>;
+    f[2] = N <= 4 ? resample_kernel<TT, TQ, true, 4> : resample_kernel<TT, TQ, true, 8>;
   } else {
     f[0] = N <= 4 ? stats_kernel<TT, TQ, false, 4> : stats_kernel<TT, TQ, false, 8>;
     f[1] = decide_kernel<TT, TQ, false>;
-    f[2] = N <= 4 ? segsum_kernel<TT, TQ, false, 4> : segsum_kernel<TT, TQ, false, 8>;
-    f[3] = N <= 4 ? finish_kernel<TT, TQ, false, 4> : finish_kernel<TT, TQ, false, 8>;
+    f[2] = N <= 4 ? resample_kernel<TT, TQ, false, 4> : resample_kernel<TT, TQ, false, 8>;
   }
 }
 void pick_split(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, SplitFn* f) {
@@ -1125,6 +1123,7 @@ struct cosine_ctx_s {
   UnitRec* recs = nullptr;
   PartRec* parts = nullptr;
   PosDec* pdec = nullptr;
+  int32_t* counters = nullptr;
   double* segsum = nullptr;
   size_t segsum_cap = 0;
   cudaStream_t aux = nullptr;
@@ -1212,7 +1211,7 @@ cosine_status_t launch(cosine_ctx_t ctx, cudaStream_t stream, Params& P, int64_t
 // latter launched with programmatic dependent launch so its launch overlaps A's tail.
 cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S,
                              cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
-  SplitFn fn[4];
+  SplitFn fn[3];
   pick_split(tt, tq, logits, S.N, fn);
   const int64_t units = (int64_t)S.B * (S.k + 1);
   // kernel A: ~8 groups (64 elements per row) per thread, at least ~8 CTAs per SM of work
@@ -1226,63 +1225,51 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   S.C = C;
   S.cg = (S.ngroups + C - 1) / C;
   S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
-  S.spr = (int)((S.nseg + kWarps - 1) / kWarps);
+  S.spr = (int)((S.nseg + kSegTilesPerCta - 1) / kSegTilesPerCta);
   S.parts = ctx->parts;
   S.pdec = ctx->pdec;
   S.segsum = ctx->segsum;
+  S.counters = ctx->counters;
   if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
-  // Batch pipelining: kernel A of chunk j+1 (HBM-bound) overlaps the latency-bound decision /
-  // sampling kernels of chunk j, which run on the context's high-priority internal stream.
-  int nch = 1;  // batch pipelining measured no gain on B200 (kernel A saturates every slot)
-  const char* nc_env = getenv("COSINE_CHUNKS");
-  if (nc_env) nch = std::max(1, std::min(kMaxChunks, std::min(S.B, atoi(nc_env))));
   cudaLaunchConfig_t lc;
   memset(&lc, 0, sizeof(lc));
   lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaError_t e = cudaSuccess;
-  int launches = 0;
-  for (int j = 0; j < nch && e == cudaSuccess; ++j) {
-    S.b_off = (int)((int64_t)S.B * j / nch);
-    S.nb = (int)((int64_t)S.B * (j + 1) / nch) - S.b_off;
-    const int64_t cu = (int64_t)S.nb * (S.k + 1);
-    lc.stream = stream;
-    lc.attrs = nullptr;
-    lc.numAttrs = 0;
-    lc.gridDim = dim3((unsigned)(cu * C), 1, 1);
-    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-    if (ctx->prof_on) {
-      if (ctx->prof_n == ctx->prof_ev.size()) {
-        cudaEvent_t a0, a1;
-        cudaEventCreate(&a0);
-        cudaEventCreate(&a1);
-        ctx->prof_ev.emplace_back(a0, a1);
-      }
-      pe0 = ctx->prof_ev[ctx->prof_n].first;
-      pe1 = ctx->prof_ev[ctx->prof_n].second;
-      ctx->prof_n++;
-      cudaEventRecord(pe0, stream);
+  S.b_off = 0;
+  S.nb = S.B;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (ctx->prof_on) {
+    if (ctx->prof_n == ctx->prof_ev.size()) {
+      cudaEvent_t a0, a1;
+      cudaEventCreate(&a0);
+      cudaEventCreate(&a1);
+      ctx->prof_ev.emplace_back(a0, a1);
     }
-    e = cudaLaunchKernelEx(&lc, fn[0], S);  // A_j on the caller's stream
-    if (pe1) cudaEventRecord(pe1, stream);
-    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[j], stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->ev[j], 0);
-    const unsigned grids[3] = {(unsigned)((cu + kWarps - 1) / kWarps), (unsigned)(S.nb * S.spr),
-                               (unsigned)((S.nb + kWarps - 1) / kWarps)};
-    lc.stream = ctx->aux;
-    for (int q = 0; q < 3 && e == cudaSuccess; ++q) {
-      lc.gridDim = dim3(grids[q], 1, 1);
-      lc.attrs = q ? at : nullptr;  // B2a, B2b: programmatic dependents of their predecessor
-      lc.numAttrs = q ? 1 : 0;
-      e = cudaLaunchKernelEx(&lc, fn[1 + q], S);
-    }
-    launches += 4;
+    pe0 = ctx->prof_ev[ctx->prof_n].first;
+    pe1 = ctx->prof_ev[ctx->prof_n].second;
+    ctx->prof_n++;
+    cudaEventRecord(pe0, stream);
   }
-  if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[kMaxChunks], ctx->aux);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ctx->ev[kMaxChunks], 0);  // join
+  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+  cudaError_t e = cudaLaunchKernelEx(&lc, fn[0], S);  // kernel A
+  if (pe1) cudaEventRecord(pe1, stream);
+  if (e == cudaSuccess) {  // kernel B1 (decisions), a programmatic dependent of A
+    lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+    lc.attrs = pe1 ? nullptr : at;  // (an event record between the two breaks PDL anyway)
+    lc.numAttrs = pe1 ? 0 : 1;
+    e = cudaLaunchKernelEx(&lc, fn[1], S);
+  }
+  if (e == cudaSuccess) {  // kernel B2 (first rejection + resample), dependent of B1
+    lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, fn[2], S);
+  }
+  const int launches = 3;
   if (e != cudaSuccess) {
     cudaGetLastError();
     ctx->last_launches = 0;
@@ -1365,6 +1352,8 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   const size_t nu = nb * (size_t)(cfg->max_draft_len + 1);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->parts, nu * kMaxC * sizeof(PartRec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, nb * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, nb * sizeof(int32_t));
   ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
   if (e == cudaSuccess) {
@@ -1387,6 +1376,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     cudaFree(ctx->first_rej);
     cudaFree(ctx->parts);
     cudaFree(ctx->pdec);
+    cudaFree(ctx->counters);
     cudaFree(ctx->segsum);
     for (int j = 0; j <= kMaxChunks; ++j)
       if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
@@ -1407,6 +1397,7 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->first_rej);
   cudaFree(ctx->parts);
   cudaFree(ctx->pdec);
+  cudaFree(ctx->counters);
   cudaFree(ctx->segsum);
   for (int j = 0; j <= kMaxChunks; ++j)
     if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
