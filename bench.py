@@ -32,6 +32,8 @@ WORKLOADS = {
     "c1": "c1: batch=1, 2 drafters, k=4, vocab=32000, fp32 logits/probs, CONF fusion, T=1",
     "c2": "c2: batch=64, 3 drafters, k=8, vocab=32000 (Llama-2), bf16 logits/probs, CONF fusion, T=1",
     "c3": "c3: batch=256, 4 drafters, k=8, vocab=128256 (Llama-3), bf16 logits/probs, CONF fusion, T=1",
+    "c4": "c4: tree-shaped drafts, 64-node tree per request (schedule 4,2,2,1,1,1,1,1), batch=128, "
+          "4 drafters, vocab=128256, bf16, CONF fusion, T=1",
 }
 
 
@@ -198,6 +200,8 @@ def run_ours(args):
     B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
     esz = torch.tensor([], dtype=dt).element_size()
     dev = torch.device("cuda", local)
+    if args.config == "c4":
+        return run_tree(args, c, dev, world, rank, local)
     rids = sharding.weak_request_ids(B, rank)  # weak scaling: a full batch per rank, global ids
     inp = synth.linear_inputs(B, k, N, V, dtype=dt, seed=args.seed + 7919 * rank, device=dev,
                               rid_base=rids.start)
@@ -322,6 +326,74 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     ver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_tree(args, c, dev, world, rank, local):
+    """c4: one cosine_verify_tree call per step; verified draft tokens = B x 64."""
+    import torch
+    import torch.distributed as dist
+    import paper_2503_10325_b200 as cv
+    from paper_2503_10325_b200 import sharding, synth
+    B, N, V, dt = c["B"], c["N"], c["V"], c["dtype"]
+    t = synth.tree_inputs(B, N, V, dtype=dt, seed=args.seed + 7919 * rank, device=dev,
+                          rid_base=sharding.weak_request_ids(B, rank).start)
+    nn, I = t["J"] + 1, t["I"]
+    esz = torch.tensor([], dtype=dt).element_size()
+    ctx = cv.cosine_verify_init(V, device=local, max_batch=B, max_draft_len=1, max_drafters=N, seed=args.seed,
+                                target_dtype=dt, draft_dtype=dt, max_tree_nodes=nn)
+    al = torch.empty(B, dtype=torch.int32, device=dev)
+    an = torch.empty(B, nn, dtype=torch.int32, device=dev)
+    ot = torch.empty(B, nn, dtype=torch.int32, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        cv.cosine_verify_tree(ctx, t["parent"], t["node_token"], t["internal_row"], t["target"], t["draft"],
+                              t["node_draft_tokens"], t["request_ids"], al, an, ot, st, temperature=1.0)
+        return cv.cosine_last_launch_count(ctx)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        launches += step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sampler.stop_ev.set()
+    sampler.join()
+    ms = sharding.max_over_ranks(e0.elapsed_time(e1), device=dev) / args.steps
+    tokens = B * t["J"] * world
+    alg = synth.tree_algorithmic_bytes(B, nn, I, N, V, esz, esz)
+    peak, peak_src = peaks()
+    acc = al.float().mean().item()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tokens / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOADS["c4"], "batch_per_gpu": B, "global_batch": B * world,
+                       "tree_nodes": t["J"], "internal_nodes": I, "drafters": N, "vocab": V,
+                       "parallelism": f"batch-sharded x{world}", "mean_accept_len": acc,
+                       "l2": f"inputs {alg / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": alg, "accounting": "all nodes read once (whole call)",
+                         "frac_of_8tbs": alg / (ms / 1e3) / 1e9 / 8000.0},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": sampler.result(),
+        }
+        print(json.dumps(line), flush=True)
+    cv.cosine_verify_destroy(ctx)
     if world > 1:
         dist.destroy_process_group()
 

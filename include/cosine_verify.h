@@ -61,6 +61,7 @@ typedef enum {
 #define COSINE_REQ_NONFINITE_INPUT 3      /* NaN / +inf logit; NaN, inf or negative prob      */
 #define COSINE_REQ_EMPTY_ROW 4            /* all -inf logits, or a probability row summing to 0 */
 #define COSINE_REQ_BAD_DRAFT_LEN 5        /* draft_len[b] outside [1, k]                      */
+#define COSINE_REQ_BAD_TREE 6             /* tree: parent order, duplicate sibling tokens, internal rows */
 #define COSINE_INFO_DEGENERATE_RESIDUAL 0x100 /* Z == 0: resampled from o (reading #11) */
 #define COSINE_INFO_NEAR_TIE 0x200        /* a decision margin < 1e-6 (reading #18)          */
 
@@ -83,7 +84,7 @@ typedef struct {
   int32_t max_batch;       /* largest B of any call                                          */
   int32_t max_draft_len;   /* largest k                                                      */
   int32_t max_drafters;    /* largest N (<= 8)                                               */
-  int32_t max_tree_nodes;  /* reserved (tree verification), 0 if unused                      */
+  int32_t max_tree_nodes;  /* largest J + 1 of cosine_verify_tree, 0 if unused              */
   cosine_dtype_t target_dtype;
   cosine_dtype_t draft_dtype;
   cosine_draft_kind_t draft_kind;
@@ -175,6 +176,32 @@ cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream,
                                        const float* draft_norm, int32_t N,
                                        const uint32_t* node_ids, const uint64_t* request_ids,
                                        uint32_t step, int32_t* out_token, int32_t* status);
+
+/*
+ * cosine_verify_tree — tree-shaped drafts ("merge them into a tree topology", P:414-415;
+ * the algorithm is DESIGN.md reading #13, the paper does not give it): multi-candidate recursive
+ * rejection.  One tree per request with J+1 nodes, node 0 = the root (last verified token).
+ *   parent [B][J+1] int32 (parent[0] = -1, 0 <= parent[j] < j; children of a node are visited in
+ *                  ascending node id = draw order);  node_token [B][J+1] int32 (root ignored)
+ *   internal_row [B][J+1] int32: row of `draft` holding node j's drafter distributions, -1 iff j
+ *                  is a leaf;  target [B][J+1][ld_t]: row j = the target's logits after the path
+ *                  to node j;  draft [B][I][N][ld_q];  node_draft_tokens [B][I][N] (the drafters'
+ *                  own tokens at each internal node, for Eq. 4 confidences)
+ *   temperature > 0;  weight_mode CONF / WINNER / UNIFORM (POINT is undefined for several children)
+ * Outputs: accept_len [B] = depth of the accepted path (-1 on error); accepted_nodes [B][J+1] node
+ *   ids of the accepted path, -1 padded; out_tokens [B][J+1] = tokens of the path then the final
+ *   token, -1 padded; status [B].  Requires cfg.max_tree_nodes >= J + 1.
+ * Every node's rows are read once; each rejection costs one more pass over its node's rows.
+ */
+cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                   int32_t I, int32_t N, const int32_t* parent,
+                                   const int32_t* node_token, const int32_t* internal_row,
+                                   const void* target, int64_t ld_t, float temperature,
+                                   const void* draft, int64_t ld_q,
+                                   const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, cosine_weight_mode_t weight_mode,
+                                   int32_t* accept_len, int32_t* accepted_nodes,
+                                   int32_t* out_tokens, int32_t* status);
 
 /* Number of kernels the last successful call on ctx enqueued (for launch accounting). */
 int32_t cosine_last_launch_count(cosine_ctx_t ctx);

@@ -636,6 +636,7 @@ int orc_verify_tree(int32_t B, int32_t J, int32_t I, int32_t N, int64_t V,
           c[n] = qn[(size_t)n * (size_t)V + (size_t)X[n]];
         }
         orc_fusion_weights(N, c, weight_mode, w, &gap);
+        if (weight_mode == ORC_W_WINNER) tm = dmin(tm, gap); /* the only argmax in a tree */
         for (int64_t v = 0; v < V; ++v) {
           double s = 0.0;
           for (int n = 0; n < N; ++n) s += w[n] * qn[(size_t)n * (size_t)V + (size_t)v];

@@ -69,6 +69,9 @@ _lib.cosine_sample_residual.argtypes = [_P, _P, _i32, _P, _i64, _f32, _P, _P, _P
                                         _i32, _P, _P, _u32, _P, _P]
 _lib.cosine_sample_residual.restype = ctypes.c_int
 
+_lib.cosine_verify_tree.argtypes = [_P, _P, _i32, _i32, _i32, _i32, _P, _P, _P, _P, _i64, _f32, _P, _i64,
+                                    _P, _P, _u32, ctypes.c_int, _P, _P, _P, _P]
+_lib.cosine_verify_tree.restype = ctypes.c_int
 _lib.cosine_profile_enable.argtypes = [_P, _i32]
 _lib.cosine_profile_enable.restype = ctypes.c_int
 _lib.cosine_profile_read.argtypes = [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]
@@ -76,7 +79,8 @@ _lib.cosine_profile_read.restype = ctypes.c_int
 
 EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_error",
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
-                    "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read")
+                    "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
+                    "cosine_verify_tree")
 
 
 class CosineError(RuntimeError):
@@ -118,11 +122,13 @@ class Context:
 
 def cosine_verify_init(vocab_size: int, *, device: int = 0, max_batch: int, max_draft_len: int,
                        max_drafters: int, target_dtype=torch.bfloat16, draft_dtype=torch.bfloat16,
-                       draft_kind: int = DRAFT_PROBS, seed: int = 0, cluster_size: int = 0):
+                       draft_kind: int = DRAFT_PROBS, seed: int = 0, cluster_size: int = 0,
+                       max_tree_nodes: int = 0):
     """Create a context on `device`; returns a Context."""
     cfg = cosine_config_t(device=device, vocab_size=vocab_size, vocab_begin=0, vocab_end=vocab_size,
                           max_batch=max_batch, max_draft_len=max_draft_len, max_drafters=max_drafters,
-                          max_tree_nodes=0, target_dtype=_DT[target_dtype], draft_dtype=_DT[draft_dtype],
+                          max_tree_nodes=max_tree_nodes, target_dtype=_DT[target_dtype],
+                          draft_dtype=_DT[draft_dtype],
                           draft_kind=draft_kind, seed=seed, nranks=1, rank=0, nccl_unique_id=None,
                           cluster_size=cluster_size)
     h = _P()
@@ -176,6 +182,20 @@ def cosine_verify_batch(ctx, target_logits, draft, draft_tokens, request_ids, ac
                                   _ptr(draft_tokens), _ptr(draft_len), _ptr(request_ids), step,
                                   weight_mode, select_mode, _ptr(accept_len), _ptr(out_tokens),
                                   _ptr(status), ctypes.byref(dbg) if dbg is not None else None)
+    _check(rc, ctx)
+
+
+def cosine_verify_tree(ctx, parent, node_token, internal_row, target, draft, node_draft_tokens,
+                       request_ids, accept_len, accepted_nodes, out_tokens, status, *, temperature=1.0,
+                       step=0, weight_mode=W_CONF, stream=None):
+    """parent / node_token / internal_row [B][J+1], target [B][J+1][ld_t], draft [B][I][N][ld_q]."""
+    B, nn, ld_t = target.shape
+    I, N, ld_q = draft.shape[1], draft.shape[2], draft.shape[3]
+    rc = _lib.cosine_verify_tree(ctx, _stream(stream, target.device), B, nn - 1, I, N, _ptr(parent),
+                                 _ptr(node_token), _ptr(internal_row), _ptr(target), ld_t, temperature,
+                                 _ptr(draft), ld_q, _ptr(node_draft_tokens), _ptr(request_ids), step,
+                                 weight_mode, _ptr(accept_len), _ptr(accepted_nodes), _ptr(out_tokens),
+                                 _ptr(status))
     _check(rc, ctx)
 
 

@@ -56,6 +56,9 @@ struct SplitParams {
   int64_t nseg;
   int spr;         // B2a CTAs per request
   int b_off, nb;   // this launch covers requests [b_off, b_off + nb) (batch pipelining)
+  // tree mode (cosine_verify_tree): a unit is a node (b, j); rows via internal_row
+  int tree, nn, I;           // nodes per request (J + 1), internal (drafter) rows per request
+  const int32_t* irow;       // [B][nn] drafter row of node j, -1 for a leaf
 };
 
 
@@ -133,13 +136,24 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
   const int rank = (int)(blockIdx.x % C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = P.N;
-  const int b = P.b_off + (int)(unit / (P.k + 1));
-  const int i = (int)(unit % (P.k + 1));
-  const int g = P.draft_len ? P.draft_len[b] : P.k;
-  if (g < 1 || g > P.k || i > g) return;  // rows past gamma_b are never read
-  const int Nd = (i < g) ? N : 0;
-  const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t;
-  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
+  int Nd;
+  const TT* trow;
+  const TQ* drow;
+  if (P.tree) {  // node (b, j): target row j, the N drafter rows of its internal row (if any)
+    const int b = (int)(unit / P.nn);
+    const int ir = P.irow[unit];
+    Nd = (ir >= 0 && ir < P.I) ? N : 0;
+    trow = (const TT*)P.target + unit * P.ld_t;
+    drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? ir : 0)) * N * P.ld_q;
+  } else {
+    const int b = P.b_off + (int)(unit / (P.k + 1));
+    const int i = (int)(unit % (P.k + 1));
+    const int g = P.draft_len ? P.draft_len[b] : P.k;
+    if (g < 1 || g > P.k || i > g) return;  // rows past gamma_b are never read
+    Nd = (i < g) ? N : 0;
+    trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t;
+    drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
+  }
 
   __shared__ float s_wf[kWarps][1 + kMaxN];
   __shared__ float s_wv[kWarps];

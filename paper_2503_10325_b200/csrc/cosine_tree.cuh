@@ -1,0 +1,478 @@
+// cosine_tree.cuh — tree-shaped drafts: multi-candidate
+// recursive rejection over a draft tree ("merge them into a tree topology"),
+// DESIGN.md reading #13: at node j the children are tested in slot order with
+// u = U(rid, child, ACCEPT) against o_r(x) / q_r(x); on a rejection o_{r+1} = norm(max(0, o_r - q_r))
+// (a full pass over node j's rows) and q_{r+1} = q_r without x, renormalised; when the children are
+// exhausted y ~ o_r (U(rid, j, SAMPLE)); at a leaf y ~ o_j (the bonus).
+//
+// Kernels: the streaming stats_kernel in tree mode (every node's target row and, for internal
+// nodes, its N drafter rows, read once) -> tree_decide_kernel (one warp per node: statistics,
+// Eq. 4 fusion at the node, o_j(x_c) and q_j(x_c) of each child) -> tree_walk_kernel (one
+// 1024-thread CTA per request: the sequential walk; full passes only on rejections and for the
+// final draw).
+#pragma once
+
+namespace cosine {
+
+struct NodeDec {  // per node (b, j)
+  int32_t status;  // data error of the node (token > non-finite > empty > zero probability)
+  float M, gap;    // max logit, Eq. 4 fusion margin (internal nodes)
+  double S;
+  float a[kMaxN], dm[kMaxN];  // w_n / sigma_n, drafter maxima (LOGITS)
+};
+struct ChildPQ {  // o_parent(x_c) and q_parent(x_c) of node c's token (before any rejection)
+  double p, q;
+};
+
+struct TreeParams {
+  SplitParams S;  // shapes, rows, stats scratch (tree mode)
+  const int32_t* parent;       // [B][nn]
+  const int32_t* node_token;   // [B][nn]
+  const int32_t* node_draft_tokens;  // [B][I][N]
+  NodeDec* ndec;               // [B][nn]
+  ChildPQ* cpq;                // [B][nn]
+  int32_t* accepted_nodes;     // [B][nn]
+};
+
+// ---------------- kernel T1: one warp per node ----------------
+template <typename TT, typename TQ, bool kLogits>
+__global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams T) {
+  const SplitParams& P = T.S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
+  __shared__ float s_gx[kWarps][kMaxN * kMaxN];
+  __shared__ int32_t s_tok[kWarps][kMaxN];
+  __shared__ double s_w[kWarps][kMaxN], s_sig[kWarps][kMaxN];
+  __shared__ float s_dmax[kWarps][kMaxN];
+  __shared__ int s_zero[kWarps];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the stats kernel's partial records (PDL)
+  if (unit >= (int64_t)P.B * T.S.nn) return;
+  const int nn = P.nn, N = P.N, C = P.C;
+  const int b = (int)(unit / nn), j = (int)(unit % nn);
+  const int ir = P.irow[unit];
+  const bool has_d = ir >= 0 && ir < P.I;
+  const double k2 = (double)P.k2f;
+  const TT* trow = (const TT*)P.target + unit * P.ld_t;
+  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (has_d ? ir : 0)) * N * P.ld_q;
+  if (lane == 0) s_zero[warp] = 0;
+  if (has_d && lane < N * N) {  // d_m(X_n) for the confidences at this node
+    const int n = lane % N, m = lane / N;
+    const int32_t tk = T.node_draft_tokens[((int64_t)b * P.I + ir) * N + n];
+    float v = 0.f;
+    if (tk >= 0 && (int64_t)tk < P.V) v = load_one(drow + (int64_t)m * P.ld_q, tk);
+    s_gx[warp][m * kMaxN + n] = v;
+    if (m == 0) s_tok[warp][n] = tk;
+  }
+  // combine the partial records (chunk r in lane r)
+  const PartRec* parts = P.parts + unit * C;
+  const bool own = lane < C;
+  const float tmax = own ? parts[lane].tmax : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
+  const float M = warp_max(tmax);
+  const double tsum = own ? parts[lane].tsum : 0.0;
+  const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
+  bool t_nf = !isfinite(S) || !isfinite(M), t_empty = false, d_nf = false, d_empty = false;
+  t_empty = !t_nf && !(S > 0.0);
+  double sig[kMaxN];
+  float dmax[kMaxN];
+  if (has_d) {
+    if (bad & 2) d_nf = true;
+    for (int n = 0; n < N; ++n) {
+      double sv;
+      float mx = kNegBig;
+      const double ds = own ? parts[lane].dsum[n] : 0.0;
+      if (kLogits) {
+        const float dmr = own ? parts[lane].dmax[n] : kNegBig;
+        mx = warp_max(dmr);
+        sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
+        if (!isfinite(mx)) d_nf = true;
+      } else {
+        sv = warp_sum(ds);
+      }
+      sig[n] = sv;
+      dmax[n] = mx;
+      if (!isfinite(sv)) d_nf = true;
+      else if (!(sv > 0.0)) d_empty = true;
+    }
+  }
+  __syncwarp();
+  NodeDec nd;
+  nd.M = M;
+  nd.S = S;
+  nd.gap = INFINITY;
+  for (int n = 0; n < kMaxN; ++n) { nd.a[n] = 0.f; nd.dm[n] = 0.f; }
+  int stc = 0;
+  bool ok_for_children = false;
+  if (lane == 0) {
+    bool tok_bad = false, zero = false;
+    if (has_d)
+      for (int n = 0; n < N; ++n)
+        if (s_tok[warp][n] < 0 || (int64_t)s_tok[warp][n] >= P.V) tok_bad = true;
+    if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
+    else if (t_nf || d_nf) stc = COSINE_REQ_NONFINITE_INPUT;
+    else if (t_empty || d_empty) stc = COSINE_REQ_EMPTY_ROW;
+    auto qval = [&](int m, double dv) {
+      return kLogits ? exp2(dv * k2 - (double)dmax[m] * k2) / sig[m] : dv / sig[m];
+    };
+    double c[kMaxN], w[kMaxN];
+    if (!stc && has_d) {
+      for (int n = 0; n < N; ++n) {
+        c[n] = qval(n, (double)s_gx[warp][n * kMaxN + n]);  // c_n = q_n(X_n) at this node
+        if (c[n] == 0.0) zero = true;
+      }
+      if (zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+    }
+    if (!stc && has_d) {  // Eq. 4 fusion weights at the node (reading #2)
+      int ns = 0;
+      for (int n = 1; n < N; ++n)
+        if (c[n] > c[ns]) ns = n;
+      double second = -1.0;
+      for (int n = 0; n < N; ++n)
+        if (n != ns && c[n] > second) second = c[n];
+      nd.gap = (N > 1) ? (float)((c[ns] - second) / c[ns]) : INFINITY;
+      if (P.weight_mode == COSINE_W_CONF) {
+        double sc = 0.0;
+        for (int n = 0; n < N; ++n) sc += c[n];
+        for (int n = 0; n < N; ++n) w[n] = c[n] / sc;
+      } else if (P.weight_mode == COSINE_W_UNIFORM) {
+        for (int n = 0; n < N; ++n) w[n] = 1.0 / (double)N;
+      } else {
+        for (int n = 0; n < N; ++n) w[n] = (n == ns) ? 1.0 : 0.0;
+      }
+      for (int n = 0; n < N; ++n) {
+        nd.a[n] = (float)(w[n] / sig[n]);
+        nd.dm[n] = dmax[n];
+        s_w[warp][n] = w[n];
+        s_sig[warp][n] = sig[n];
+        s_dmax[warp][n] = dmax[n];
+      }
+      ok_for_children = true;
+    }
+  }
+  ok_for_children = __shfl_sync(0xffffffffu, ok_for_children, 0);
+  __syncwarp();
+  // o_j(x_c), q_j(x_c) of every child c of j (lane-parallel over candidate node ids)
+  for (int c = j + 1 + lane; c < nn; c += 32) {
+    if (T.parent[(int64_t)b * nn + c] != j) continue;
+    const int32_t x = T.node_token[(int64_t)b * nn + c];
+    ChildPQ pq;
+    pq.p = 0.0;
+    pq.q = 0.0;
+    if (x >= 0 && (int64_t)x < P.V && ok_for_children) {
+      pq.p = exp2((double)load_one(trow, x) * k2 - (double)M * k2) / S;
+      double q = 0.0;
+      for (int m = 0; m < N; ++m) {
+        const double dv = (double)load_one(drow + (int64_t)m * P.ld_q, x);
+        const double qm = kLogits ? exp2(dv * k2 - (double)s_dmax[warp][m] * k2) / s_sig[warp][m]
+                                  : dv / s_sig[warp][m];
+        q += s_w[warp][m] * qm;
+      }
+      pq.q = q;
+      if (q == 0.0) atomicOr(&s_zero[warp], 1);  // a child the fused q cannot draw
+    }
+    T.cpq[(int64_t)b * nn + c] = pq;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (!stc && s_zero[warp]) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+    nd.status = stc;
+    T.ndec[unit] = nd;
+  }
+}
+
+// ---------------- the walk ----------------
+constexpr int kTreeThreads = 1024;
+constexpr int kTreeWarps = kTreeThreads / 32;
+constexpr int kTreeMaxRej = 64;
+
+struct TreeState {  // the current node's o_r, q_r as a recursion over r rejections
+  float M, invS, k2;
+  float a[kMaxN], dm[kMaxN];
+  int r;
+  int32_t xs[kTreeMaxRej];   // rejected tokens, in order
+  double Zs[kTreeMaxRej];    // residual masses (0 = degenerate: o kept, reading #11)
+  double qsc[kTreeMaxRej];   // 1 / (1 - q_t(x_t))
+};
+
+// o_r(v) (mode 1) or max(0, o_r(v) - q_r(v)) (mode 0) for the 8 entries of a group.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeState& st, int mode,
+                                             const TT* trow, const TQ* drow, int Nd, int64_t gi,
+                                             float w[8]) {
+  float t[8], q[8];
+  const bool full = gi < P.gfull;
+  if (full) {
+    Group<TT> tv;
+    tv.load(trow, gi);
+    tv.unpack(t);
+  } else {
+    load_partial(trow, gi, P.V, -INFINITY, t);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) q[e] = 0.f;
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) {
+    if (n < Nd) {
+      float f[8];
+      const TQ* row = drow + (int64_t)n * P.ld_q;
+      if (full) {
+        Group<TQ> dv;
+        dv.load(row, gi);
+        dv.unpack(f);
+      } else {
+        load_partial(row, gi, P.V, kLogits ? -INFINITY : 0.f, f);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float qv = kLogits ? ex2((f[e] - st.dm[n]) * st.k2) : f[e];
+        q[e] = fmaf(st.a[n], qv, q[e]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int64_t v = gi * kGroup + e;
+    double pv = (double)(ex2((t[e] - st.M) * st.k2) * st.invS);
+    double qv = (double)q[e];
+    for (int s = 0; s < st.r; ++s) {
+      const double dd = pv - qv;
+      if (st.Zs[s] > 0.0) pv = (dd > 0.0 ? dd : 0.0) / st.Zs[s];
+      qv = (v == (int64_t)st.xs[s]) ? 0.0 : qv * st.qsc[s];
+    }
+    const double x = (mode == 1) ? pv : (pv - qv > 0.0 ? pv - qv : 0.0);
+    w[e] = (v < P.V) ? (float)x : 0.f;
+  }
+}
+
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreeParams T) {
+  const SplitParams& P = T.S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  const int nn = P.nn, N = P.N;
+  __shared__ TreeState st;
+  __shared__ int s_act, s_node, s_Nd;
+  __shared__ double s_part[kTreeWarps];
+  __shared__ double s_tile[kMaxSeg];
+  __shared__ double s_u;
+  __shared__ int64_t s_y;
+  __shared__ float s_margin;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // tree_decide_kernel's records (PDL)
+  const int32_t* par = T.parent + (int64_t)b * nn;
+  const int32_t* tok = T.node_token + (int64_t)b * nn;
+  const int32_t* irw = P.irow + (int64_t)b * nn;
+  const NodeDec* nds = T.ndec + (int64_t)b * nn;
+  const ChildPQ* cpq = T.cpq + (int64_t)b * nn;
+  int32_t* out = P.out_tokens + (int64_t)b * nn;
+  int32_t* acc = T.accepted_nodes + (int64_t)b * nn;
+  const uint64_t rid = P.rids[b];
+  // thread-0 walk state
+  int err = 0, j = 0, depth = 0, ci = 0, deg = 0;
+  float tm = INFINITY;
+  bool need_init = true;
+  if (tid == 0) {
+    // structure first (parent order, token range, distinct siblings, internal rows), then the
+    // node data errors in node order (reading #12, #13)
+    if (par[0] != -1) err = COSINE_REQ_BAD_TREE;
+    for (int c = 1; c < nn && !err; ++c) {
+      if (par[c] < 0 || par[c] >= c) err = COSINE_REQ_BAD_TREE;
+      else if (tok[c] < 0 || (int64_t)tok[c] >= P.V) err = COSINE_REQ_TOKEN_OUT_OF_RANGE;
+      for (int c2 = 1; c2 < c && !err; ++c2)
+        if (par[c2] == par[c] && tok[c2] == tok[c]) err = COSINE_REQ_BAD_TREE;
+    }
+    for (int c = 0; c < nn && !err; ++c) {
+      bool has_child = false;
+      for (int c2 = c + 1; c2 < nn; ++c2)
+        if (par[c2] == c) { has_child = true; break; }
+      if (has_child != (irw[c] >= 0) || irw[c] >= P.I) err = COSINE_REQ_BAD_TREE;
+    }
+    for (int c = 0; c < nn && !err; ++c)
+      if (nds[c].status) err = nds[c].status;
+    s_act = err ? 0 : -1;
+  }
+  __syncthreads();
+  if (s_act == 0) {
+    for (int c = tid; c < nn; c += kTreeThreads) { out[c] = -1; acc[c] = -1; }
+    if (tid == 0) { P.accept_len[b] = -1; P.status[b] = err; }
+    return;
+  }
+  for (;;) {
+    if (tid == 0) {
+      // advance the walk until the block is needed for a pass (act 1) or the final draw (act 2)
+      int act = -1;
+      while (act < 0) {
+        if (need_init) {  // arriving at node j: o_0, q_0 of the node
+          const NodeDec& nd = nds[j];
+          st.M = nd.M;
+          st.invS = (float)(1.0 / nd.S);
+          st.k2 = P.k2f;
+          for (int n = 0; n < kMaxN; ++n) { st.a[n] = nd.a[n]; st.dm[n] = nd.dm[n]; }
+          st.r = 0;
+          ci = j + 1;
+          need_init = false;
+          if (irw[j] >= 0 && P.weight_mode == COSINE_W_WINNER) tm = fmin_(tm, nd.gap);  // reading #18
+        }
+        int c = ci;
+        while (c < nn && par[c] != j) ++c;
+        if (irw[j] < 0 || c >= nn || st.r >= kTreeMaxRej) {
+          act = 2;  // children exhausted (or a leaf): y ~ o_r with U(rid, j, SAMPLE)
+          break;
+        }
+        ci = c + 1;
+        const int32_t x = tok[c];
+        double pv = cpq[c].p, qv = cpq[c].q;
+        for (int s = 0; s < st.r; ++s) {  // o_r(x), q_r(x)
+          const double dd = pv - qv;
+          if (st.Zs[s] > 0.0) pv = (dd > 0.0 ? dd : 0.0) / st.Zs[s];
+          qv = (x == st.xs[s]) ? 0.0 : qv * st.qsc[s];
+        }
+        const double u = philox_u24(P.seed, rid, (uint32_t)c, P.step, kTagAccept);
+        tm = fmin_(tm, (float)fabs(u - pv / qv));
+        if (u * qv < pv) {  // accept: move to the child
+          out[depth] = x;
+          acc[depth] = c;
+          depth++;
+          j = c;
+          need_init = true;
+          continue;
+        }
+        // reject: o_{r+1} = norm(max(0, o_r - q_r)) needs its mass: a full pass
+        st.xs[st.r] = x;
+        st.qsc[st.r] = (qv < 1.0) ? 1.0 / (1.0 - qv) : 1.0;
+        act = 1;
+      }
+      s_act = act;
+      s_node = j;
+      s_Nd = (irw[j] >= 0) ? N : 0;
+      if (act == 2) s_u = philox_u24(P.seed, rid, (uint32_t)j, P.step, kTagSample);
+    }
+    __syncthreads();
+    const int act = s_act, jn = s_node, Nd = s_Nd;
+    const TT* trow = (const TT*)P.target + ((int64_t)b * nn + jn) * P.ld_t;
+    const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? irw[jn] : 0)) * N * P.ld_q;
+    if (act == 1) {
+      double accum = 0.0;
+      for (int64_t gi = tid; gi < P.ngroups; gi += kTreeThreads) {
+        float w[8];
+        tree_weights<TT, TQ, kLogits, NMAX>(P, st, 0, trow, drow, Nd, gi, w);
+        accum += (double)sum8(w);
+      }
+      accum = warp_sum(accum);
+      if (lane == 0) s_part[warp] = accum;
+      __syncthreads();
+      if (tid == 0) {
+        double Z = 0.0;
+        for (int w2 = 0; w2 < kTreeWarps; ++w2) Z += s_part[w2];
+        if (!(Z > 0.0)) deg = 1;  // all mass cancelled: o kept (reading #11)
+        st.Zs[st.r] = Z;
+        st.r++;
+      }
+      __syncthreads();
+      continue;
+    }
+    // act == 2: y ~ o_r of node jn: tile masses (one warp per tile), crossing tile, warp scan
+    const int64_t ntile = (P.ngroups + kTileGroups - 1) / kTileGroups;
+    for (int64_t tI = warp; tI < ntile; tI += kTreeWarps) {
+      double m = 0.0;
+      const int64_t g0 = tI * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
+      for (int64_t gi = g0 + lane; gi < g1; gi += 32) {
+        float w[8];
+        tree_weights<TT, TQ, kLogits, NMAX>(P, st, 1, trow, drow, Nd, gi, w);
+        m += (double)sum8(w);
+      }
+      m = warp_sum(m);
+      if (lane == 0) s_tile[tI] = m;
+    }
+    __syncthreads();
+    __shared__ int64_t s_tstar;
+    __shared__ double s_tc, s_Z;
+    if (tid == 0) {
+      double Z = 0.0;
+      for (int64_t t2 = 0; t2 < ntile; ++t2) Z += s_tile[t2];
+      const double t = s_u * Z;
+      int64_t tstar = -1;
+      double tc = 0.0, O = 0.0;
+      for (int64_t t2 = 0; t2 < ntile && Z > 0.0; ++t2) {
+        if (O + s_tile[t2] > t) { tstar = t2; tc = t - O; break; }
+        O += s_tile[t2];
+      }
+      s_tstar = tstar;
+      s_tc = tc;
+      s_Z = Z;
+      s_y = -1;
+      s_margin = 0.f;
+    }
+    __syncthreads();
+    if (warp == 0 && s_tstar >= 0) {
+      const int64_t g0 = s_tstar * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
+      double base = 0.0;
+      int64_t y = -1;
+      float mg = 0.f;
+      for (int64_t t0 = g0; t0 < g1 && y < 0; t0 += 32) {
+        const int64_t gi = t0 + lane;
+        float w[8];
+        double s = 0.0;
+        if (gi < g1) {
+          tree_weights<TT, TQ, kLogits, NMAX>(P, st, 1, trow, drow, Nd, gi, w);
+          s = (double)sum8(w);
+        }
+        double incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += nb;
+        }
+        const double excl = base + incl - s;
+        const bool hit = gi < g1 && s > 0.0 && excl <= s_tc && s_tc < excl + s;
+        const unsigned msk = __ballot_sync(0xffffffffu, hit);
+        if (msk) {
+          const int src = __ffs(msk) - 1;
+          if (lane == src) {
+            double cum = excl;
+            int ef = -1;
+            for (int e = 0; e < 8; ++e) {
+              const double prev = cum;
+              cum += (double)w[e];
+              if (cum > s_tc) { ef = e; mg = (float)(fmin(s_tc - prev, cum - s_tc) / s_Z); break; }
+            }
+            if (ef < 0)
+              for (int e = 7; e >= 0; --e)
+                if (w[e] > 0.f) { ef = e; break; }
+            y = gi * kGroup + ef;
+          }
+          y = __shfl_sync(0xffffffffu, y, src);
+          mg = __shfl_sync(0xffffffffu, mg, src);
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (y < 0) {  // rounding fallback: the last positive entry of the tile (reading #10)
+        int64_t last = -1;
+        for (int64_t gi = g0 + lane; gi < g1; gi += 32) {
+          float w[8];
+          tree_weights<TT, TQ, kLogits, NMAX>(P, st, 1, trow, drow, Nd, gi, w);
+          for (int e = 0; e < 8; ++e)
+            if (w[e] > 0.f) last = max(last, gi * kGroup + e);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        y = last;
+        mg = 0.f;
+      }
+      if (lane == 0) { s_y = y; s_margin = mg; }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      out[depth] = (int32_t)s_y;
+      for (int c = depth + 1; c < nn; ++c) out[c] = -1;
+      for (int c = depth; c < nn; ++c) acc[c] = -1;
+      P.accept_len[b] = depth;
+      tm = fmin_(tm, s_margin);
+      P.status[b] = (deg ? COSINE_INFO_DEGENERATE_RESIDUAL : 0) | (tm < 1e-6f ? COSINE_INFO_NEAR_TIE : 0) |
+                    (s_y < 0 ? 0xff : 0);
+      if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
+    }
+    return;
+  }
+}
+
+}  // namespace cosine

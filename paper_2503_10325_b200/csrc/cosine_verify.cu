@@ -1069,6 +1069,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
 
 }  // namespace cosine
 #include "cosine_split.cuh"
+#include "cosine_tree.cuh"
 namespace cosine {
 
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
@@ -1092,6 +1093,24 @@ void pick_split2(bool logits, int N, SplitFn* f) {
     f[2] = N <= 4 ? resample_kernel<TT, TQ, false, 4> : resample_kernel<TT, TQ, false, 8>;
   }
 }
+using TreeFn = void (*)(TreeParams);
+template <typename TT, typename TQ>
+void pick_tree2(bool logits, int N, TreeFn* f) {
+  if (logits) {
+    f[0] = tree_decide_kernel<TT, TQ, true>;
+    f[1] = N <= 4 ? tree_walk_kernel<TT, TQ, true, 4> : tree_walk_kernel<TT, TQ, true, 8>;
+  } else {
+    f[0] = tree_decide_kernel<TT, TQ, false>;
+    f[1] = N <= 4 ? tree_walk_kernel<TT, TQ, false, 4> : tree_walk_kernel<TT, TQ, false, 8>;
+  }
+}
+void pick_tree(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, TreeFn* f) {
+  if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_tree2<__nv_bfloat16, __nv_bfloat16>(logits, N, f);
+  if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_tree2<__nv_bfloat16, float>(logits, N, f);
+  if (tt == COSINE_F32 && tq == COSINE_BF16) return pick_tree2<float, __nv_bfloat16>(logits, N, f);
+  return pick_tree2<float, float>(logits, N, f);
+}
+
 void pick_split(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, SplitFn* f) {
   if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_split2<__nv_bfloat16, __nv_bfloat16>(logits, N, f);
   if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_split2<__nv_bfloat16, float>(logits, N, f);
@@ -1124,6 +1143,8 @@ struct cosine_ctx_s {
   PartRec* parts = nullptr;
   PosDec* pdec = nullptr;
   int32_t* counters = nullptr;
+  NodeDec* ndec = nullptr;
+  ChildPQ* cpq = nullptr;
   double* segsum = nullptr;
   size_t segsum_cap = 0;
   cudaStream_t aux = nullptr;
@@ -1326,6 +1347,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad vocabulary range");
   if (cfg->vocab_end - cfg->vocab_begin > (int64_t)0x7fffffff)
     return fail(nullptr, COSINE_ERR_UNSUPPORTED, "vocabulary wider than 2^31 - 1");
+  if (cfg->max_tree_nodes < 0) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "max_tree_nodes < 0");
   if (cfg->max_batch < 0 || cfg->max_draft_len < 1 || cfg->max_draft_len > kMaxPos - 1 ||
       cfg->max_drafters < 1 || cfg->max_drafters > kMaxN)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad max_* sizes (max_draft_len <= 64, max_drafters <= 8)");
@@ -1349,7 +1371,10 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   cudaError_t e = cudaMalloc(&ctx->recs, nb * (size_t)(cfg->max_draft_len + 1) * sizeof(UnitRec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->done, nb * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->first_rej, nb * sizeof(int32_t));
-  const size_t nu = nb * (size_t)(cfg->max_draft_len + 1);
+  const size_t nu = nb * (size_t)std::max(cfg->max_draft_len + 1, std::max(cfg->max_tree_nodes, 1));
+  const size_t nt = nb * (size_t)std::max(cfg->max_tree_nodes, 1);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->ndec, nt * sizeof(NodeDec));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->cpq, nt * sizeof(ChildPQ));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->parts, nu * kMaxC * sizeof(PartRec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, nb * sizeof(int32_t));
@@ -1377,6 +1402,8 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     cudaFree(ctx->parts);
     cudaFree(ctx->pdec);
     cudaFree(ctx->counters);
+    cudaFree(ctx->ndec);
+    cudaFree(ctx->cpq);
     cudaFree(ctx->segsum);
     for (int j = 0; j <= kMaxChunks; ++j)
       if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
@@ -1398,6 +1425,8 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->parts);
   cudaFree(ctx->pdec);
   cudaFree(ctx->counters);
+  cudaFree(ctx->ndec);
+  cudaFree(ctx->cpq);
   cudaFree(ctx->segsum);
   for (int j = 0; j <= kMaxChunks; ++j)
     if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
@@ -1542,6 +1571,91 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   }
   return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
                 ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+}
+
+cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                   int32_t I, int32_t N, const int32_t* parent,
+                                   const int32_t* node_token, const int32_t* internal_row,
+                                   const void* target, int64_t ld_t, float temperature,
+                                   const void* draft, int64_t ld_q,
+                                   const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, cosine_weight_mode_t weight_mode,
+                                   int32_t* accept_len, int32_t* accepted_nodes,
+                                   int32_t* out_tokens, int32_t* status) {
+  cosine_status_t s = check_common(ctx, B, 1, N);
+  if (s != COSINE_OK) return s;
+  if (J < 0 || J + 1 > ctx->cfg.max_tree_nodes)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "J + 1 exceeds max_tree_nodes");
+  if (I < 0 || I > J + 1) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "I outside [0, J + 1]");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, target, ld_t, ctx->cfg.target_dtype, "target")) != COSINE_OK) return s;
+  if (I > 0 && (s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
+  if (!parent || !node_token || !internal_row || (I > 0 && !node_draft_tokens) || !request_ids ||
+      !accept_len || !accepted_nodes || !out_tokens || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature > 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "tree verification needs a finite temperature > 0");
+  if ((int)weight_mode < 0 || (int)weight_mode > 2)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "tree weight mode must be CONF, WINNER or UNIFORM");
+  const int64_t ngroups = (ctx->V + kGroup - 1) / kGroup;
+  if ((ngroups + kTileGroups - 1) / kTileGroups > kMaxSeg)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary too wide for the tree sampler");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P0;
+  fill_common(P0, ctx, B, 1, N, temperature);
+  TreeParams T;
+  memset(&T, 0, sizeof(T));
+  SplitParams& S = T.S;
+  S.B = B; S.k = 1; S.N = N;
+  S.V = P0.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P0.ngroups; S.gfull = P0.gfull;
+  S.k2f = P0.k2f; S.k2d = P0.k2d; S.greedy = 0; S.weight_mode = weight_mode;
+  S.target = target; S.draft = draft; S.rids = request_ids; S.seed = P0.seed; S.step = step;
+  S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status;
+  S.tree = 1; S.nn = J + 1; S.I = I; S.irow = internal_row;
+  S.parts = ctx->parts;
+  T.parent = parent; T.node_token = node_token; T.node_draft_tokens = node_draft_tokens;
+  T.ndec = ctx->ndec; T.cpq = ctx->cpq; T.accepted_nodes = accepted_nodes;
+  const int64_t units = (int64_t)B * (J + 1);
+  int C = 1;
+  if (ctx->cfg.cluster_size > 0) {
+    C = ctx->cfg.cluster_size;
+  } else {
+    while (C < kMaxC && S.ngroups > (int64_t)C * kThreads * 8) C *= 2;
+    while (C < kMaxC && units * C < 148 * 8 && S.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  }
+  S.C = C;
+  S.cg = (S.ngroups + C - 1) / C;
+  SplitFn sf[3];
+  pick_split(ctx->cfg.target_dtype, ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS, N, sf);
+  TreeFn tf[2];
+  pick_tree(ctx->cfg.target_dtype, ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS, N, tf);
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+  cudaError_t e = cudaLaunchKernelEx(&lc, sf[0], S);  // every node's rows, once
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, tf[0], T);
+  }
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)B, 1, 1);
+    lc.blockDim = dim3(kTreeThreads, 1, 1);
+    e = cudaLaunchKernelEx(&lc, tf[1], T);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("tree kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 3;
+  return COSINE_OK;
 }
 
 cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B,

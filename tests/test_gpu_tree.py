@@ -1,0 +1,99 @@
+"""GPU parity of cosine_verify_tree (reading #13) against orc_verify_tree."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2503_10325_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_tree(t, *, seed=3, step=0, wm=0, T=1.0, dtype=torch.float32):
+    import paper_2503_10325_b200 as cv
+    dev = torch.device("cuda", 0)
+    B, nn, _ = t["target"].shape
+    N = t["draft"].shape[2]
+    ctx = cv.cosine_verify_init(t["V"], max_batch=B, max_draft_len=1, max_drafters=N, seed=seed,
+                                target_dtype=t["target"].dtype, draft_dtype=t["draft"].dtype,
+                                max_tree_nodes=nn)
+    al = torch.empty(B, dtype=torch.int32, device=dev)
+    an = torch.empty(B, nn, dtype=torch.int32, device=dev)
+    ot = torch.empty(B, nn, dtype=torch.int32, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    d = {k: (v.to(dev) if torch.is_tensor(v) else v) for k, v in t.items()}
+    cv.cosine_verify_tree(ctx, d["parent"], d["node_token"], d["internal_row"], d["target"], d["draft"],
+                          d["node_draft_tokens"], d["request_ids"], al, an, ot, st, temperature=T, step=step,
+                          weight_mode=wm)
+    torch.cuda.synchronize()
+    launches = cv.cosine_last_launch_count(ctx)
+    cv.cosine_verify_destroy(ctx)
+    return dict(accept_len=al.cpu().numpy(), accepted_nodes=an.cpu().numpy(), out_tokens=ot.cpu().numpy(),
+                status=st.cpu().numpy(), launches=launches)
+
+
+def _oracle_tree(t, *, seed=3, step=0, wm=0, T=1.0, subset=None):
+    sel = slice(None) if subset is None else subset
+    return oracle.verify_tree(t["parent"][sel].cpu(), t["node_token"][sel].cpu(), t["internal_row"][sel].cpu(),
+                              t["target"][sel].cpu(), t["draft"][sel].cpu(), t["node_draft_tokens"][sel].cpu(),
+                              t["request_ids"][sel].cpu(), temperature=T, seed=seed, step=step,
+                              weight_mode=wm, vocab=t["V"])
+
+
+def _compare(g, r, subset=None):
+    idx = np.arange(len(r["accept_len"])) if subset is None else np.asarray(subset)
+    np.testing.assert_array_equal(g["status"][idx] & 0xff, r["status"] & 0xff)
+    mism = (g["accept_len"][idx] != r["accept_len"]) | (g["out_tokens"][idx] != r["out_tokens"]).any(1) | \
+           (g["accepted_nodes"][idx] != r["accepted_nodes"]).any(1)
+    flagged = r["tie_margin"] < 1e-6
+    assert not (mism & ~flagged).any(), np.nonzero(mism & ~flagged)[0][:5]
+    return int(mism.sum()), int(flagged.sum())
+
+
+@pytest.mark.parametrize("schedule,cap,V,wm", [((2, 2, 1), 12, 1003, 0), ((3, 1, 1, 1), 20, 777, 1),
+                                               ((4, 2, 2, 1, 1, 1, 1, 1), 64, 2049, 2)])
+def test_tree_small(cuda_ok, schedule, cap, V, wm):
+    t = synth.tree_inputs(24, 3, V, schedule=schedule, cap=cap, dtype=torch.float32, seed=V, sigma=2.0)
+    g = _gpu_tree(t, wm=wm, step=1)
+    r = _oracle_tree(t, wm=wm, step=1)
+    _compare(g, r)
+    assert g["launches"] == 3
+
+
+def test_chain_tree_equals_linear_on_gpu(cuda_ok):
+    # a chain tree is the linear path (same Philox stream), here on the GPU
+    from . import parity
+    inp = synth.linear_inputs(32, 5, 2, 3001, dtype=torch.float32, seed=7, sigma=3.0)
+    g_lin = parity.gpu_verify(inp, seed=21)
+    B, k = 32, 5
+    t = dict(parent=torch.arange(-1, k, dtype=torch.int32).expand(B, k + 1).contiguous(),
+             node_token=torch.cat([torch.zeros(B, 1, dtype=torch.int32),
+                                   torch.as_tensor(g_lin["fused_tokens"])], 1).contiguous(),
+             internal_row=torch.tensor(list(range(k)) + [-1], dtype=torch.int32).expand(B, k + 1).contiguous(),
+             target=inp["target"], draft=inp["draft"], node_draft_tokens=inp["draft_tokens"],
+             request_ids=inp["request_ids"], V=inp["V"])
+    g_tree = _gpu_tree(t, seed=21)
+    np.testing.assert_array_equal(g_tree["accept_len"], g_lin["accept_len"])
+    np.testing.assert_array_equal(g_tree["out_tokens"], g_lin["out_tokens"])
+
+
+def test_bad_tree_and_errors(cuda_ok):
+    t = synth.tree_inputs(6, 2, 500, schedule=(2, 1), cap=6, dtype=torch.float32, seed=9, sigma=2.0)
+    t["parent"][1, 3] = 5                      # parent after child
+    t["node_token"][2, 2] = t["node_token"][2, 1]  # duplicate sibling token
+    t["node_token"][3, 4] = 500                # token out of range
+    t["target"][4, 2, 7] = float("nan")        # non-finite logit
+    g = _gpu_tree(t)
+    r = _oracle_tree(t)
+    np.testing.assert_array_equal(g["status"] & 0xff, r["status"] & 0xff)
+    assert list(r["status"][:5] & 0xff) == [0, 6, 6, 2, 3]
+    _compare(g, r)
+
+
+def test_c4_full_size_sampled_requests(cuda_ok):
+    c = synth.CONFIGS["c4"]
+    t = synth.tree_inputs(c["B"], c["N"], c["V"], dtype=c["dtype"], seed=44, device="cuda")
+    g = _gpu_tree(t, seed=5)
+    subset = np.arange(0, c["B"], 25)
+    r = _oracle_tree(t, seed=5, subset=torch.as_tensor(subset))
+    _compare(g, r, subset=subset)
