@@ -84,7 +84,7 @@ typedef struct {
   int32_t max_batch;       /* largest B of any call                                          */
   int32_t max_draft_len;   /* largest k                                                      */
   int32_t max_drafters;    /* largest N (<= 8)                                               */
-  int32_t max_tree_nodes;  /* largest J + 1 of cosine_verify_tree, 0 if unused              */
+  int32_t max_tree_nodes;  /* largest J + 1 of cosine_verify_tree (<= 1024), 0 if unused   */
   cosine_dtype_t target_dtype;
   cosine_dtype_t draft_dtype;
   cosine_draft_kind_t draft_kind;

@@ -5,6 +5,7 @@ package itself refuses to import until the library exists).
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -15,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libcosine_verify.so")
 SOURCES = [os.path.join(CSRC, "cosine_verify.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "cosine_kernels.cuh"), os.path.join(CSRC, "cosine_split.cuh"), os.path.join(INCLUDE, "cosine_verify.h")]
+DEPS = SOURCES + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(INCLUDE, "*.h")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -181,9 +181,10 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
 }
 
 // ---------------- the walk ----------------
-constexpr int kTreeThreads = 1024;
+constexpr int kTreeThreads = 512;
 constexpr int kTreeWarps = kTreeThreads / 32;
 constexpr int kTreeMaxRej = 64;
+constexpr int kTreeMaxNodes = 1024;  // nodes per tree (the walk stages the tree in shared memory)
 
 struct TreeState {  // the current node's o_r, q_r as a recursion over r rejections
   float M, invS, k2;
@@ -191,19 +192,25 @@ struct TreeState {  // the current node's o_r, q_r as a recursion over r rejecti
   int r;
   int32_t xs[kTreeMaxRej];   // rejected tokens, in order
   double Zs[kTreeMaxRej];    // residual masses (0 = degenerate: o kept, reading #11)
-  double qsc[kTreeMaxRej];   // 1 / (1 - q_t(x_t))
+  float invZ[kTreeMaxRej];   // 1 / Z (0 when degenerate)
+  float qsc[kTreeMaxRej];    // 1 / (1 - q_t(x_t))
 };
 
-// o_r(v) (mode 1) or max(0, o_r(v) - q_r(v)) (mode 0) for the 8 entries of a group.
+// For the 8 entries of a group, after rr recursion steps: mode 0 -> max(0, o_rr - q_rr) (the
+// unnormalised residual, whose mass is Z_{rr+1}); mode 1 -> o_rr.
 template <typename TT, typename TQ, bool kLogits, int NMAX>
-__device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeState& st, int mode,
+__device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeState& st, int mode, int rr,
                                              const TT* trow, const TQ* drow, int Nd, int64_t gi,
                                              float w[8]) {
   float t[8], q[8];
   const bool full = gi < P.gfull;
-  if (full) {
-    Group<TT> tv;
+  Group<TT> tv;
+  Group<TQ> dv[NMAX];
+  if (full) {  // every load of the group first
     tv.load(trow, gi);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n)
+      if (n < Nd) dv[n].load(drow + (int64_t)n * P.ld_q, gi);
     tv.unpack(t);
   } else {
     load_partial(trow, gi, P.V, -INFINITY, t);
@@ -214,14 +221,8 @@ __device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeSta
   for (int n = 0; n < NMAX; ++n) {
     if (n < Nd) {
       float f[8];
-      const TQ* row = drow + (int64_t)n * P.ld_q;
-      if (full) {
-        Group<TQ> dv;
-        dv.load(row, gi);
-        dv.unpack(f);
-      } else {
-        load_partial(row, gi, P.V, kLogits ? -INFINITY : 0.f, f);
-      }
+      if (full) dv[n].unpack(f);
+      else load_partial(drow + (int64_t)n * P.ld_q, gi, P.V, kLogits ? -INFINITY : 0.f, f);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float qv = kLogits ? ex2((f[e] - st.dm[n]) * st.k2) : f[e];
@@ -232,15 +233,37 @@ __device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeSta
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int64_t v = gi * kGroup + e;
-    double pv = (double)(ex2((t[e] - st.M) * st.k2) * st.invS);
-    double qv = (double)q[e];
-    for (int s = 0; s < st.r; ++s) {
-      const double dd = pv - qv;
-      if (st.Zs[s] > 0.0) pv = (dd > 0.0 ? dd : 0.0) / st.Zs[s];
-      qv = (v == (int64_t)st.xs[s]) ? 0.0 : qv * st.qsc[s];
+    float pv = ex2((t[e] - st.M) * st.k2) * st.invS;
+    float qv = q[e];
+    for (int s2 = 0; s2 < rr; ++s2) {
+      if (st.invZ[s2] > 0.f) pv = fmaxf(pv - qv, 0.f) * st.invZ[s2];
+      qv = (v == (int64_t)st.xs[s2]) ? 0.f : qv * st.qsc[s2];
     }
-    const double x = (mode == 1) ? pv : (pv - qv > 0.0 ? pv - qv : 0.0);
-    w[e] = (v < P.V) ? (float)x : 0.f;
+    const float x = (mode == 1) ? pv : fmaxf(pv - qv, 0.f);
+    w[e] = (v < P.V) ? x : 0.f;
+  }
+}
+
+// Per-tile masses of the weights (one warp per 256-group tile, two groups of loads in flight).
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__device__ __forceinline__ void tree_tile_masses(const SplitParams& P, const TreeState& st, int mode, int rr,
+                                                 const TT* trow, const TQ* drow, int Nd, double* s_tile) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ntile = (P.ngroups + kTileGroups - 1) / kTileGroups;
+  for (int64_t tI = warp; tI < ntile; tI += kTreeWarps) {
+    const int64_t g0 = tI * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
+    double m = 0.0;
+    for (int64_t gi = g0 + lane; gi < g1; gi += 64) {
+      float w0[8], w1[8];
+      tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi, w0);
+      m += (double)sum8(w0);
+      if (gi + 32 < g1) {
+        tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi + 32, w1);
+        m += (double)sum8(w1);
+      }
+    }
+    m = warp_sum(m);
+    if (lane == 0) s_tile[tI] = m;
   }
 }
 
@@ -252,42 +275,55 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
   const int nn = P.nn, N = P.N;
   __shared__ TreeState st;
   __shared__ int s_act, s_node, s_Nd;
-  __shared__ double s_part[kTreeWarps];
   __shared__ double s_tile[kMaxSeg];
   __shared__ double s_u;
   __shared__ int64_t s_y;
   __shared__ float s_margin;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // tree_decide_kernel's records (PDL)
-  const int32_t* par = T.parent + (int64_t)b * nn;
-  const int32_t* tok = T.node_token + (int64_t)b * nn;
-  const int32_t* irw = P.irow + (int64_t)b * nn;
+  __shared__ int32_t par[kTreeMaxNodes], tok[kTreeMaxNodes], irw[kTreeMaxNodes];
+  __shared__ int32_t s_e1[kTreeMaxNodes], s_e2[kTreeMaxNodes];
+  for (int c = tid; c < nn; c += kTreeThreads) {
+    par[c] = T.parent[(int64_t)b * nn + c];
+    tok[c] = T.node_token[(int64_t)b * nn + c];
+    irw[c] = P.irow[(int64_t)b * nn + c];
+  }
+  __syncthreads();
   const NodeDec* nds = T.ndec + (int64_t)b * nn;
   const ChildPQ* cpq = T.cpq + (int64_t)b * nn;
   int32_t* out = P.out_tokens + (int64_t)b * nn;
   int32_t* acc = T.accepted_nodes + (int64_t)b * nn;
   const uint64_t rid = P.rids[b];
+  // structure checks, one node per thread: (1) parent order, token range, distinct siblings;
+  // (2) internal rows exactly for the nodes with children; then (3) node data errors — the
+  // first error in that order wins (reading #12, #13; same order as the oracle)
+  for (int c = tid; c < nn; c += kTreeThreads) {
+    int e1 = 0, e2 = 0;
+    if (c == 0) {
+      if (par[0] != -1) e1 = COSINE_REQ_BAD_TREE;
+    } else if (par[c] < 0 || par[c] >= c) {
+      e1 = COSINE_REQ_BAD_TREE;
+    } else if (tok[c] < 0 || (int64_t)tok[c] >= P.V) {
+      e1 = COSINE_REQ_TOKEN_OUT_OF_RANGE;
+    } else {
+      for (int c2 = 1; c2 < c; ++c2)
+        if (par[c2] == par[c] && tok[c2] == tok[c]) { e1 = COSINE_REQ_BAD_TREE; break; }
+    }
+    bool has_child = false;
+    for (int c2 = c + 1; c2 < nn; ++c2)
+      if (par[c2] == c) { has_child = true; break; }
+    if (has_child != (irw[c] >= 0) || irw[c] >= P.I) e2 = COSINE_REQ_BAD_TREE;
+    s_e1[c] = e1;
+    s_e2[c] = e2;
+  }
+  __syncthreads();
   // thread-0 walk state
   int err = 0, j = 0, depth = 0, ci = 0, deg = 0;
   float tm = INFINITY;
   bool need_init = true;
   if (tid == 0) {
-    // structure first (parent order, token range, distinct siblings, internal rows), then the
-    // node data errors in node order (reading #12, #13)
-    if (par[0] != -1) err = COSINE_REQ_BAD_TREE;
-    for (int c = 1; c < nn && !err; ++c) {
-      if (par[c] < 0 || par[c] >= c) err = COSINE_REQ_BAD_TREE;
-      else if (tok[c] < 0 || (int64_t)tok[c] >= P.V) err = COSINE_REQ_TOKEN_OUT_OF_RANGE;
-      for (int c2 = 1; c2 < c && !err; ++c2)
-        if (par[c2] == par[c] && tok[c2] == tok[c]) err = COSINE_REQ_BAD_TREE;
-    }
-    for (int c = 0; c < nn && !err; ++c) {
-      bool has_child = false;
-      for (int c2 = c + 1; c2 < nn; ++c2)
-        if (par[c2] == c) { has_child = true; break; }
-      if (has_child != (irw[c] >= 0) || irw[c] >= P.I) err = COSINE_REQ_BAD_TREE;
-    }
-    for (int c = 0; c < nn && !err; ++c)
-      if (nds[c].status) err = nds[c].status;
+    for (int c = 0; c < nn && !err; ++c) err = s_e1[c];
+    for (int c = 0; c < nn && !err; ++c) err = s_e2[c];
+    for (int c = 0; c < nn && !err; ++c) err = nds[c].status;
     s_act = err ? 0 : -1;
   }
   __syncthreads();
@@ -350,42 +386,40 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
     const int act = s_act, jn = s_node, Nd = s_Nd;
     const TT* trow = (const TT*)P.target + ((int64_t)b * nn + jn) * P.ld_t;
     const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? irw[jn] : 0)) * N * P.ld_q;
-    if (act == 1) {
-      double accum = 0.0;
-      for (int64_t gi = tid; gi < P.ngroups; gi += kTreeThreads) {
-        float w[8];
-        tree_weights<TT, TQ, kLogits, NMAX>(P, st, 0, trow, drow, Nd, gi, w);
-        accum += (double)sum8(w);
-      }
-      accum = warp_sum(accum);
-      if (lane == 0) s_part[warp] = accum;
+    const int64_t ntile = (P.ngroups + kTileGroups - 1) / kTileGroups;
+    if (act == 1) {  // Z_{r+1}: per-tile masses of max(0, o_r - q_r), kept for the final draw
+      tree_tile_masses<TT, TQ, kLogits, NMAX>(P, st, 0, st.r, trow, drow, Nd, s_tile);
       __syncthreads();
       if (tid == 0) {
         double Z = 0.0;
-        for (int w2 = 0; w2 < kTreeWarps; ++w2) Z += s_part[w2];
+        for (int64_t t2 = 0; t2 < ntile; ++t2) Z += s_tile[t2];
         if (!(Z > 0.0)) deg = 1;  // all mass cancelled: o kept (reading #11)
         st.Zs[st.r] = Z;
+        st.invZ[st.r] = (Z > 0.0) ? (float)(1.0 / Z) : 0.f;
         st.r++;
       }
       __syncthreads();
       continue;
     }
-    // act == 2: y ~ o_r of node jn: tile masses (one warp per tile), crossing tile, warp scan
-    const int64_t ntile = (P.ngroups + kTileGroups - 1) / kTileGroups;
-    for (int64_t tI = warp; tI < ntile; tI += kTreeWarps) {
-      double m = 0.0;
-      const int64_t g0 = tI * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
-      for (int64_t gi = g0 + lane; gi < g1; gi += 32) {
-        float w[8];
-        tree_weights<TT, TQ, kLogits, NMAX>(P, st, 1, trow, drow, Nd, gi, w);
-        m += (double)sum8(w);
-      }
-      m = warp_sum(m);
-      if (lane == 0) s_tile[tI] = m;
-    }
-    __syncthreads();
+    // act == 2: y ~ o_R of node jn (reading #10).  After R >= 1 rejections o_R is the residual of
+    // the last pass, whose tile masses are still in s_tile: scan its crossing tile with weights
+    // max(0, o_{R-1} - q_{R-1}) and t = u Z_R (the oracle's unnormalised form).  A leaf (the
+    // bonus) or a degenerate last step needs a pass over o_R first.
     __shared__ int64_t s_tstar;
     __shared__ double s_tc, s_Z;
+    __shared__ int s_mode, s_rr;
+    if (tid == 0) {
+      const int R = st.r;
+      const bool reuse = R >= 1 && st.Zs[R - 1] > 0.0;
+      s_mode = reuse ? 0 : 1;
+      s_rr = reuse ? R - 1 : R;
+    }
+    __syncthreads();
+    const int mode = s_mode, rr = s_rr;
+    if (mode == 1) {
+      tree_tile_masses<TT, TQ, kLogits, NMAX>(P, st, 1, rr, trow, drow, Nd, s_tile);
+      __syncthreads();
+    }
     if (tid == 0) {
       double Z = 0.0;
       for (int64_t t2 = 0; t2 < ntile; ++t2) Z += s_tile[t2];
@@ -413,7 +447,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
         float w[8];
         double s = 0.0;
         if (gi < g1) {
-          tree_weights<TT, TQ, kLogits, NMAX>(P, st, 1, trow, drow, Nd, gi, w);
+          tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi, w);
           s = (double)sum8(w);
         }
         double incl = s;
@@ -449,7 +483,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
         int64_t last = -1;
         for (int64_t gi = g0 + lane; gi < g1; gi += 32) {
           float w[8];
-          tree_weights<TT, TQ, kLogits, NMAX>(P, st, 1, trow, drow, Nd, gi, w);
+          tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi, w);
           for (int e = 0; e < 8; ++e)
             if (w[e] > 0.f) last = max(last, gi * kGroup + e);
         }

@@ -1347,7 +1347,8 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad vocabulary range");
   if (cfg->vocab_end - cfg->vocab_begin > (int64_t)0x7fffffff)
     return fail(nullptr, COSINE_ERR_UNSUPPORTED, "vocabulary wider than 2^31 - 1");
-  if (cfg->max_tree_nodes < 0) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "max_tree_nodes < 0");
+  if (cfg->max_tree_nodes < 0 || cfg->max_tree_nodes > kTreeMaxNodes)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "max_tree_nodes outside [0, 1024]");
   if (cfg->max_batch < 0 || cfg->max_draft_len < 1 || cfg->max_draft_len > kMaxPos - 1 ||
       cfg->max_drafters < 1 || cfg->max_drafters > kMaxN)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad max_* sizes (max_draft_len <= 64, max_drafters <= 8)");
