@@ -71,6 +71,9 @@ struct Group<__nv_bfloat16> {
   __device__ __forceinline__ void load(const __nv_bfloat16* row, int64_t g) {
     a = ld_stream(row + g * kGroup);
   }
+  __device__ __forceinline__ void load_s(const __nv_bfloat16* srow, int g) {  // shared memory
+    a = *reinterpret_cast<const uint4*>(srow + g * kGroup);
+  }
   __device__ __forceinline__ void unpack(float f[8]) const {
     f[0] = __uint_as_float(a.x << 16); f[1] = __uint_as_float(a.x & 0xffff0000u);
     f[2] = __uint_as_float(a.y << 16); f[3] = __uint_as_float(a.y & 0xffff0000u);
@@ -88,6 +91,10 @@ struct Group<float> {
   __device__ __forceinline__ void load(const float* row, int64_t g) {
     a = ld_stream(row + g * kGroup);
     b = ld_stream(row + g * kGroup + 4);
+  }
+  __device__ __forceinline__ void load_s(const float* srow, int g) {  // shared memory
+    a = *reinterpret_cast<const uint4*>(srow + g * kGroup);
+    b = *reinterpret_cast<const uint4*>(srow + g * kGroup + 4);
   }
   __device__ __forceinline__ void unpack(float f[8]) const {
     f[0] = __uint_as_float(a.x); f[1] = __uint_as_float(a.y);
@@ -184,6 +191,23 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Bulk async copies (TMA, non-tensor): global -> this CTA's shared memory, completion counted in
+// bytes on an mbarrier (PTX ISA: cp.async.bulk, mbarrier.expect_tx).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 }  // namespace cosine

@@ -181,10 +181,24 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
 }
 
 // ---------------- the walk ----------------
+// One 512-thread CTA per request.  A full pass over node j's rows (target + N drafters) streams
+// them through a kTreeStages-deep ring of shared-memory tiles filled by bulk async copies (TMA,
+// cp.async.bulk + mbarrier), so one SM keeps ~160 KB in flight without spending registers on it;
+// the threads only read shared memory.  Per-tile masses are kept for the final draw.
 constexpr int kTreeThreads = 512;
 constexpr int kTreeWarps = kTreeThreads / 32;
 constexpr int kTreeMaxRej = 64;
 constexpr int kTreeMaxNodes = 1024;  // nodes per tree (the walk stages the tree in shared memory)
+constexpr int kTreeStages = 4;
+
+// Tile geometry: one tile = kTG groups of every row of the node; a row's slice is <= kRowB bytes.
+__host__ __device__ constexpr int tree_row_bytes(int nmax) { return nmax <= 4 ? 8192 : 4096; }
+__host__ __device__ constexpr int tree_tile_groups(int nmax, int esize_max) {
+  return tree_row_bytes(nmax) / (kGroup * esize_max);
+}
+__host__ __device__ constexpr int tree_walk_smem(int nmax) {
+  return kTreeStages * (1 + nmax) * tree_row_bytes(nmax);
+}
 
 struct TreeState {  // the current node's o_r, q_r as a recursion over r rejections
   float M, invS, k2;
@@ -196,33 +210,26 @@ struct TreeState {  // the current node's o_r, q_r as a recursion over r rejecti
   float qsc[kTreeMaxRej];    // 1 / (1 - q_t(x_t))
 };
 
-// For the 8 entries of a group, after rr recursion steps: mode 0 -> max(0, o_rr - q_rr) (the
-// unnormalised residual, whose mass is Z_{rr+1}); mode 1 -> o_rr.
+// The 8 weights of local group g of a staged tile, after rr recursion steps: mode 0 ->
+// max(0, o_rr - q_rr) (the unnormalised residual, whose mass is Z_{rr+1}); mode 1 -> o_rr.
 template <typename TT, typename TQ, bool kLogits, int NMAX>
-__device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeState& st, int mode, int rr,
-                                             const TT* trow, const TQ* drow, int Nd, int64_t gi,
-                                             float w[8]) {
+__device__ __forceinline__ void tree_weights_s(const TreeState& st, int mode, int rr,
+                                               const unsigned char* stage, int Nd, int g,
+                                               int vbase, int V, float w[8]) {
+  constexpr int kRowB = tree_row_bytes(NMAX);
   float t[8], q[8];
-  const bool full = gi < P.gfull;
   Group<TT> tv;
-  Group<TQ> dv[NMAX];
-  if (full) {  // every load of the group first
-    tv.load(trow, gi);
-#pragma unroll
-    for (int n = 0; n < NMAX; ++n)
-      if (n < Nd) dv[n].load(drow + (int64_t)n * P.ld_q, gi);
-    tv.unpack(t);
-  } else {
-    load_partial(trow, gi, P.V, -INFINITY, t);
-  }
+  tv.load_s(reinterpret_cast<const TT*>(stage), g);
+  tv.unpack(t);
 #pragma unroll
   for (int e = 0; e < 8; ++e) q[e] = 0.f;
 #pragma unroll
   for (int n = 0; n < NMAX; ++n) {
     if (n < Nd) {
+      Group<TQ> dv;
+      dv.load_s(reinterpret_cast<const TQ*>(stage + (1 + n) * kRowB), g);
       float f[8];
-      if (full) dv[n].unpack(f);
-      else load_partial(drow + (int64_t)n * P.ld_q, gi, P.V, kLogits ? -INFINITY : 0.f, f);
+      dv.unpack(f);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float qv = kLogits ? ex2((f[e] - st.dm[n]) * st.k2) : f[e];
@@ -230,66 +237,84 @@ __device__ __forceinline__ void tree_weights(const SplitParams& P, const TreeSta
       }
     }
   }
+  float pv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) pv[e] = ex2((t[e] - st.M) * st.k2) * st.invS;
+  for (int s2 = 0; s2 < rr; ++s2) {
+    const float iz = st.invZ[s2], qs = st.qsc[s2];
+    const int xr = st.xs[s2] - vbase;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (iz > 0.f) pv[e] = fmaxf(pv[e] - q[e], 0.f) * iz;
+      q[e] = (e == xr) ? 0.f : q[e] * qs;
+    }
+  }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const int64_t v = gi * kGroup + e;
-    float pv = ex2((t[e] - st.M) * st.k2) * st.invS;
-    float qv = q[e];
-    for (int s2 = 0; s2 < rr; ++s2) {
-      if (st.invZ[s2] > 0.f) pv = fmaxf(pv - qv, 0.f) * st.invZ[s2];
-      qv = (v == (int64_t)st.xs[s2]) ? 0.f : qv * st.qsc[s2];
-    }
-    const float x = (mode == 1) ? pv : fmaxf(pv - qv, 0.f);
-    w[e] = (v < P.V) ? x : 0.f;
+    const float x = (mode == 1) ? pv[e] : fmaxf(pv[e] - q[e], 0.f);
+    w[e] = (vbase + e < V) ? x : 0.f;
   }
 }
 
-// Per-tile masses of the weights (one warp per 256-group tile, two groups of loads in flight).
-template <typename TT, typename TQ, bool kLogits, int NMAX>
-__device__ __forceinline__ void tree_tile_masses(const SplitParams& P, const TreeState& st, int mode, int rr,
-                                                 const TT* trow, const TQ* drow, int Nd, double* s_tile) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t ntile = (P.ngroups + kTileGroups - 1) / kTileGroups;
-  for (int64_t tI = warp; tI < ntile; tI += kTreeWarps) {
-    const int64_t g0 = tI * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
-    double m = 0.0;
-    for (int64_t gi = g0 + lane; gi < g1; gi += 64) {
-      float w0[8], w1[8];
-      tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi, w0);
-      m += (double)sum8(w0);
-      if (gi + 32 < g1) {
-        tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi + 32, w1);
-        m += (double)sum8(w1);
-      }
-    }
-    m = warp_sum(m);
-    if (lane == 0) s_tile[tI] = m;
+template <typename TT, typename TQ, int NMAX>
+struct TreeRing {  // the shared-memory tile ring of one CTA
+  static constexpr int kRowB = tree_row_bytes(NMAX);
+  static constexpr int kEsz = sizeof(TT) > sizeof(TQ) ? (int)sizeof(TT) : (int)sizeof(TQ);
+  static constexpr int kTG = tree_tile_groups(NMAX, kEsz);
+  static constexpr int kStageB = (1 + NMAX) * kRowB;
+  unsigned char* base;
+  uint64_t* full;
+  // Thread 0: fill stage `stg` with tile `t` of the node's rows (bytes up to V, rounded to 16).
+  __device__ __forceinline__ void issue(int stg, int64_t t, const SplitParams& P, const TT* trow,
+                                        const TQ* drow, int Nd) const {
+    const int64_t g0 = t * kTG;
+    const int64_t e0 = g0 * kGroup, e1 = min((int64_t)P.V, (g0 + kTG) * kGroup);
+    const uint32_t bt = (uint32_t)((((e1 - e0) * (int64_t)sizeof(TT)) + 15) & ~(int64_t)15);
+    const uint32_t bq = (uint32_t)((((e1 - e0) * (int64_t)sizeof(TQ)) + 15) & ~(int64_t)15);
+    unsigned char* dst = base + stg * kStageB;
+    mbar_expect_tx(&full[stg], bt + (uint32_t)Nd * bq);
+    bulk_g2s(dst, trow + e0, bt, &full[stg]);
+    for (int n = 0; n < Nd; ++n) bulk_g2s(dst + (1 + n) * kRowB, drow + (int64_t)n * P.ld_q + e0, bq, &full[stg]);
   }
-}
+};
 
 template <typename TT, typename TQ, bool kLogits, int NMAX>
 __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreeParams T) {
+  using Ring = TreeRing<TT, TQ, NMAX>;
+  constexpr int kTG = Ring::kTG;
   const SplitParams& P = T.S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
   const int nn = P.nn, N = P.N;
+  extern __shared__ __align__(128) unsigned char tree_smem[];
+  __shared__ __align__(8) uint64_t s_full[kTreeStages];
   __shared__ TreeState st;
   __shared__ int s_act, s_node, s_Nd;
   __shared__ double s_tile[kMaxSeg];
+  __shared__ double s_wp[2][kTreeWarps];
   __shared__ double s_u;
   __shared__ int64_t s_y;
   __shared__ float s_margin;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // tree_decide_kernel's records (PDL)
   __shared__ int32_t par[kTreeMaxNodes], tok[kTreeMaxNodes], irw[kTreeMaxNodes];
-  __shared__ int32_t s_e1[kTreeMaxNodes], s_e2[kTreeMaxNodes];
-  for (int c = tid; c < nn; c += kTreeThreads) {
+  __shared__ int32_t s_e1[kTreeMaxNodes], s_e2[kTreeMaxNodes], s_e3[kTreeMaxNodes];
+  __shared__ double s_cp[kTreeMaxNodes], s_cq[kTreeMaxNodes];
+  const Ring ring{tree_smem, s_full};
+  if (tid == 0) {
+    for (int i = 0; i < kTreeStages; ++i) mbar_init(&s_full[i], 1);
+    fence_mbar_init_cluster();
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // tree_decide_kernel's records (PDL)
+  const NodeDec* nds = T.ndec + (int64_t)b * nn;
+  const ChildPQ* cpq = T.cpq + (int64_t)b * nn;
+  for (int c = tid; c < nn; c += kTreeThreads) {  // the tree and its per-node records, staged
     par[c] = T.parent[(int64_t)b * nn + c];
     tok[c] = T.node_token[(int64_t)b * nn + c];
     irw[c] = P.irow[(int64_t)b * nn + c];
+    s_e3[c] = nds[c].status;
+    s_cp[c] = cpq[c].p;
+    s_cq[c] = cpq[c].q;
   }
   __syncthreads();
-  const NodeDec* nds = T.ndec + (int64_t)b * nn;
-  const ChildPQ* cpq = T.cpq + (int64_t)b * nn;
   int32_t* out = P.out_tokens + (int64_t)b * nn;
   int32_t* acc = T.accepted_nodes + (int64_t)b * nn;
   const uint64_t rid = P.rids[b];
@@ -323,7 +348,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
   if (tid == 0) {
     for (int c = 0; c < nn && !err; ++c) err = s_e1[c];
     for (int c = 0; c < nn && !err; ++c) err = s_e2[c];
-    for (int c = 0; c < nn && !err; ++c) err = nds[c].status;
+    for (int c = 0; c < nn && !err; ++c) err = s_e3[c];
     s_act = err ? 0 : -1;
   }
   __syncthreads();
@@ -332,6 +357,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
     if (tid == 0) { P.accept_len[b] = -1; P.status[b] = err; }
     return;
   }
+  const int64_t ntile = (P.ngroups + kTG - 1) / kTG;
+  uint32_t it = 0;  // tiles consumed so far (ring position and mbarrier phase), uniform
   for (;;) {
     if (tid == 0) {
       // advance the walk until the block is needed for a pass (act 1) or the final draw (act 2)
@@ -356,11 +383,11 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
         }
         ci = c + 1;
         const int32_t x = tok[c];
-        double pv = cpq[c].p, qv = cpq[c].q;
+        double pv = s_cp[c], qv = s_cq[c];
         for (int s = 0; s < st.r; ++s) {  // o_r(x), q_r(x)
           const double dd = pv - qv;
           if (st.Zs[s] > 0.0) pv = (dd > 0.0 ? dd : 0.0) / st.Zs[s];
-          qv = (x == st.xs[s]) ? 0.0 : qv * st.qsc[s];
+          qv = (x == st.xs[s]) ? 0.0 : qv * (double)st.qsc[s];
         }
         const double u = philox_u24(P.seed, rid, (uint32_t)c, P.step, kTagAccept);
         tm = fmin_(tm, (float)fabs(u - pv / qv));
@@ -374,7 +401,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
         }
         // reject: o_{r+1} = norm(max(0, o_r - q_r)) needs its mass: a full pass
         st.xs[st.r] = x;
-        st.qsc[st.r] = (qv < 1.0) ? 1.0 / (1.0 - qv) : 1.0;
+        st.qsc[st.r] = (qv < 1.0) ? (float)(1.0 / (1.0 - qv)) : 1.f;
         act = 1;
       }
       s_act = act;
@@ -386,9 +413,41 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
     const int act = s_act, jn = s_node, Nd = s_Nd;
     const TT* trow = (const TT*)P.target + ((int64_t)b * nn + jn) * P.ld_t;
     const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? irw[jn] : 0)) * N * P.ld_q;
-    const int64_t ntile = (P.ngroups + kTileGroups - 1) / kTileGroups;
+    // A pass: per-tile masses of the weights (mode, rr) into s_tile[0 .. ntile).
+    auto pass = [&](int mode, int rr) {
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        for (int i = 0; i < kTreeStages && i < ntile; ++i)
+          ring.issue((int)((it + i) % kTreeStages), i, P, trow, drow, Nd);
+      }
+      for (int64_t t = 0; t < ntile; ++t, ++it) {
+        const int stg = (int)(it % kTreeStages);
+        mbar_wait_parity(&s_full[stg], (it / kTreeStages) & 1u);
+        const unsigned char* sb = ring.base + stg * Ring::kStageB;
+        const int64_t g0 = t * kTG;
+        const int tg = (int)min((int64_t)kTG, P.ngroups - g0);
+        double m = 0.0;
+        for (int g = tid; g < tg; g += kTreeThreads) {
+          float w[8];
+          tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, g, (int)((g0 + g) * kGroup), (int)P.V, w);
+          m += (double)sum8(w);
+        }
+        m = warp_sum(m);
+        if (lane == 0) s_wp[t & 1][warp] = m;
+        __syncthreads();  // the stage is consumed
+        if (tid == 0) {
+          double mt = 0.0;
+          for (int w2 = 0; w2 < kTreeWarps; ++w2) mt += s_wp[t & 1][w2];
+          s_tile[t] = mt;
+          if (t + kTreeStages < ntile) {
+            fence_proxy_async_smem();
+            ring.issue(stg, t + kTreeStages, P, trow, drow, Nd);
+          }
+        }
+      }
+    };
     if (act == 1) {  // Z_{r+1}: per-tile masses of max(0, o_r - q_r), kept for the final draw
-      tree_tile_masses<TT, TQ, kLogits, NMAX>(P, st, 0, st.r, trow, drow, Nd, s_tile);
+      pass(0, st.r);
       __syncthreads();
       if (tid == 0) {
         double Z = 0.0;
@@ -408,6 +467,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
     __shared__ int64_t s_tstar;
     __shared__ double s_tc, s_Z;
     __shared__ int s_mode, s_rr;
+    __shared__ double s_ws[kTreeWarps];
+    __shared__ int s_last[kTreeWarps];
     if (tid == 0) {
       const int R = st.r;
       const bool reuse = R >= 1 && st.Zs[R - 1] > 0.0;
@@ -417,7 +478,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
     __syncthreads();
     const int mode = s_mode, rr = s_rr;
     if (mode == 1) {
-      tree_tile_masses<TT, TQ, kLogits, NMAX>(P, st, 1, rr, trow, drow, Nd, s_tile);
+      pass(1, rr);
       __syncthreads();
     }
     if (tid == 0) {
@@ -435,64 +496,72 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
       s_Z = Z;
       s_y = -1;
       s_margin = 0.f;
+      if (tstar >= 0) {
+        fence_proxy_async_smem();
+        ring.issue((int)(it % kTreeStages), tstar, P, trow, drow, Nd);
+      }
     }
     __syncthreads();
-    if (warp == 0 && s_tstar >= 0) {
-      const int64_t g0 = s_tstar * kTileGroups, g1 = min(P.ngroups, g0 + kTileGroups);
+    if (s_tstar >= 0) {  // the crossing tile, one group per thread: block scan of group masses
+      const int stg = (int)(it % kTreeStages);
+      mbar_wait_parity(&s_full[stg], (it / kTreeStages) & 1u);
+      ++it;
+      const unsigned char* sb = ring.base + stg * Ring::kStageB;
+      const int64_t g0 = s_tstar * kTG;
+      const int tg = (int)min((int64_t)kTG, P.ngroups - g0);
+      const double tc = s_tc;
+      float w[8];
+      double s = 0.0;
+      const bool have = tid < tg;
+      const int vb = (int)((g0 + tid) * kGroup);
+      if (have) {
+        tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, tid, vb, (int)P.V, w);
+        s = (double)sum8(w);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = 0.f;
+      }
+      double incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nb;
+      }
+      if (lane == 31) s_ws[warp] = incl;
+      int last = -1;  // the last positive entry of this thread's group (rounding fallback)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (w[e] > 0.f) last = vb + e;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+      if (lane == 0) s_last[warp] = last;
+      __syncthreads();
       double base = 0.0;
-      int64_t y = -1;
-      float mg = 0.f;
-      for (int64_t t0 = g0; t0 < g1 && y < 0; t0 += 32) {
-        const int64_t gi = t0 + lane;
-        float w[8];
-        double s = 0.0;
-        if (gi < g1) {
-          tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi, w);
-          s = (double)sum8(w);
+      for (int w2 = 0; w2 < warp; ++w2) base += s_ws[w2];
+      const double excl_w = __shfl_up_sync(0xffffffffu, incl, 1);
+      const double lo = base + (lane == 0 ? 0.0 : excl_w), hi = base + incl;
+      if (have && s > 0.0 && lo <= tc && tc < hi) {
+        double cum = lo;
+        int ef = -1;
+        float mg = 0.f;
+        for (int e = 0; e < 8; ++e) {
+          const double prev = cum;
+          cum += (double)w[e];
+          if (cum > tc) { ef = e; mg = (float)(fmin(tc - prev, cum - tc) / s_Z); break; }
         }
-        double incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double nb = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += nb;
-        }
-        const double excl = base + incl - s;
-        const bool hit = gi < g1 && s > 0.0 && excl <= s_tc && s_tc < excl + s;
-        const unsigned msk = __ballot_sync(0xffffffffu, hit);
-        if (msk) {
-          const int src = __ffs(msk) - 1;
-          if (lane == src) {
-            double cum = excl;
-            int ef = -1;
-            for (int e = 0; e < 8; ++e) {
-              const double prev = cum;
-              cum += (double)w[e];
-              if (cum > s_tc) { ef = e; mg = (float)(fmin(s_tc - prev, cum - s_tc) / s_Z); break; }
-            }
-            if (ef < 0)
-              for (int e = 7; e >= 0; --e)
-                if (w[e] > 0.f) { ef = e; break; }
-            y = gi * kGroup + ef;
-          }
-          y = __shfl_sync(0xffffffffu, y, src);
-          mg = __shfl_sync(0xffffffffu, mg, src);
-        }
-        base += __shfl_sync(0xffffffffu, incl, 31);
+        if (ef < 0)
+          for (int e = 7; e >= 0; --e)
+            if (w[e] > 0.f) { ef = e; break; }
+        s_y = vb + ef;
+        s_margin = mg;
       }
-      if (y < 0) {  // rounding fallback: the last positive entry of the tile (reading #10)
-        int64_t last = -1;
-        for (int64_t gi = g0 + lane; gi < g1; gi += 32) {
-          float w[8];
-          tree_weights<TT, TQ, kLogits, NMAX>(P, st, mode, rr, trow, drow, Nd, gi, w);
-          for (int e = 0; e < 8; ++e)
-            if (w[e] > 0.f) last = max(last, gi * kGroup + e);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-        y = last;
-        mg = 0.f;
+      __syncthreads();
+      if (tid == 0 && s_y < 0) {  // rounding fallback: the last positive entry of the tile (reading #10)
+        int lst = -1;
+        for (int w2 = 0; w2 < kTreeWarps; ++w2) lst = max(lst, s_last[w2]);
+        s_y = lst;
+        s_margin = 0.f;
       }
-      if (lane == 0) { s_y = y; s_margin = mg; }
     }
     __syncthreads();
     if (tid == 0) {

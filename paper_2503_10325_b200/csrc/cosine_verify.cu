@@ -1599,7 +1599,10 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
   if ((int)weight_mode < 0 || (int)weight_mode > 2)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "tree weight mode must be CONF, WINNER or UNIFORM");
   const int64_t ngroups = (ctx->V + kGroup - 1) / kGroup;
-  if ((ngroups + kTileGroups - 1) / kTileGroups > kMaxSeg)
+  const int nmax = N <= 4 ? 4 : 8;
+  const int esz = (int)std::max(esize(ctx->cfg.target_dtype), esize(ctx->cfg.draft_dtype));
+  const int tg = tree_tile_groups(nmax, esz);
+  if ((ngroups + tg - 1) / tg > kMaxSeg)
     return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary too wide for the tree sampler");
   DeviceGuard dg(ctx->cfg.device);
   Params P0;
@@ -1648,7 +1651,9 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
   if (e == cudaSuccess) {
     lc.gridDim = dim3((unsigned)B, 1, 1);
     lc.blockDim = dim3(kTreeThreads, 1, 1);
-    e = cudaLaunchKernelEx(&lc, tf[1], T);
+    lc.dynamicSmemBytes = (size_t)tree_walk_smem(nmax);
+    e = cudaFuncSetAttribute(tf[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.dynamicSmemBytes);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&lc, tf[1], T);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
