@@ -181,12 +181,15 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
 }
 
 // ---------------- the walk ----------------
-// One 512-thread CTA per request.  A full pass over node j's rows (target + N drafters) streams
-// them through a kTreeStages-deep ring of shared-memory tiles filled by bulk async copies (TMA,
-// cp.async.bulk + mbarrier), so one SM keeps ~160 KB in flight without spending registers on it;
-// the threads only read shared memory.  Per-tile masses are kept for the final draw.
-constexpr int kTreeThreads = 512;
-constexpr int kTreeWarps = kTreeThreads / 32;
+// One CTA per request: 16 consumer warps + 1 producer warp.  A full pass over node j's rows
+// (target + N drafters) streams them through a kTreeStages-deep ring of shared-memory tiles filled
+// by bulk async copies (TMA, cp.async.bulk) issued by the producer warp; full/empty mbarriers hand
+// the stages over, so one SM keeps ~160 KB in flight without spending registers on it and the
+// consumers never meet at a block barrier inside a pass.  Per-tile masses are kept for the final
+// draw.
+constexpr int kTreeWarps = 16;                      // consumer warps
+constexpr int kTreeThreads = kTreeWarps * 32;       // consumer threads
+constexpr int kTreeBlock = kTreeThreads + 32;       // + the producer warp
 constexpr int kTreeMaxRej = 64;
 constexpr int kTreeMaxNodes = 1024;  // nodes per tree (the walk stages the tree in shared memory)
 constexpr int kTreeStages = 4;
@@ -196,8 +199,9 @@ __host__ __device__ constexpr int tree_row_bytes(int nmax) { return nmax <= 4 ? 
 __host__ __device__ constexpr int tree_tile_groups(int nmax, int esize_max) {
   return tree_row_bytes(nmax) / (kGroup * esize_max);
 }
-__host__ __device__ constexpr int tree_walk_smem(int nmax) {
-  return kTreeStages * (1 + nmax) * tree_row_bytes(nmax);
+// Dynamic shared memory of the walk: the ring, then per-(tile, warp) partial masses.
+__host__ __device__ constexpr int tree_walk_smem(int nmax, int64_t ntile) {
+  return kTreeStages * (1 + nmax) * tree_row_bytes(nmax) + (int)ntile * kTreeWarps * 8;
 }
 
 struct TreeState {  // the current node's o_r, q_r as a recursion over r rejections
@@ -256,6 +260,18 @@ __device__ __forceinline__ void tree_weights_s(const TreeState& st, int mode, in
   }
 }
 
+// Sum of the per-tile masses in a fixed order (one warp): lane l adds tiles l, l + 32, ...
+__device__ __forceinline__ double tile_total(const double* s_tile, int64_t ntile, int lane) {
+  double z = 0.0;
+  for (int64_t t = lane; t < ntile; t += 32) z += s_tile[t];
+  return warp_sum(z);
+}
+
+// Block barrier of the consumer warps only (named barrier 1; the producer warp is elsewhere).
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kTreeThreads) : "memory");
+}
+
 template <typename TT, typename TQ, int NMAX>
 struct TreeRing {  // the shared-memory tile ring of one CTA
   static constexpr int kRowB = tree_row_bytes(NMAX);
@@ -263,10 +279,16 @@ struct TreeRing {  // the shared-memory tile ring of one CTA
   static constexpr int kTG = tree_tile_groups(NMAX, kEsz);
   static constexpr int kStageB = (1 + NMAX) * kRowB;
   unsigned char* base;
-  uint64_t* full;
-  // Thread 0: fill stage `stg` with tile `t` of the node's rows (bytes up to V, rounded to 16).
-  __device__ __forceinline__ void issue(int stg, int64_t t, const SplitParams& P, const TT* trow,
-                                        const TQ* drow, int Nd) const {
+  uint64_t* full;   // count 1: the producer's expect_tx arrival + the copies' bytes
+  uint64_t* empty;  // count kTreeWarps: every consumer warp released the stage
+  // Producer lane: fill ring slot `pos` (stage pos % S, its (pos / S)-th use) with tile `t` of
+  // the node's rows (bytes up to V, rounded to 16), once the consumers released the previous use.
+  __device__ __forceinline__ void fill(uint32_t pos, int64_t t, const SplitParams& P, const TT* trow,
+                                       const TQ* drow, int Nd) const {
+    const int stg = (int)(pos % kTreeStages);
+    const uint32_t use = pos / kTreeStages;
+    if (use > 0) mbar_wait_parity(&empty[stg], (use - 1) & 1u);
+    fence_proxy_async_smem();
     const int64_t g0 = t * kTG;
     const int64_t e0 = g0 * kGroup, e1 = min((int64_t)P.V, (g0 + kTG) * kGroup);
     const uint32_t bt = (uint32_t)((((e1 - e0) * (int64_t)sizeof(TT)) + 15) & ~(int64_t)15);
@@ -279,7 +301,7 @@ struct TreeRing {  // the shared-memory tile ring of one CTA
 };
 
 template <typename TT, typename TQ, bool kLogits, int NMAX>
-__global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreeParams T) {
+__global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreeParams T) {
   using Ring = TreeRing<TT, TQ, NMAX>;
   constexpr int kTG = Ring::kTG;
   const SplitParams& P = T.S;
@@ -287,26 +309,30 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
   const int b = blockIdx.x;
   const int nn = P.nn, N = P.N;
   extern __shared__ __align__(128) unsigned char tree_smem[];
-  __shared__ __align__(8) uint64_t s_full[kTreeStages];
+  __shared__ __align__(8) uint64_t s_full[kTreeStages], s_empty[kTreeStages];
   __shared__ TreeState st;
   __shared__ int s_act, s_node, s_Nd;
   __shared__ double s_tile[kMaxSeg];
-  __shared__ double s_wp[2][kTreeWarps];
   __shared__ double s_u;
   __shared__ int64_t s_y;
   __shared__ float s_margin;
   __shared__ int32_t par[kTreeMaxNodes], tok[kTreeMaxNodes], irw[kTreeMaxNodes];
   __shared__ int32_t s_e1[kTreeMaxNodes], s_e2[kTreeMaxNodes], s_e3[kTreeMaxNodes];
   __shared__ double s_cp[kTreeMaxNodes], s_cq[kTreeMaxNodes];
-  const Ring ring{tree_smem, s_full};
+  const Ring ring{tree_smem, s_full, s_empty};
+  double* s_parts = reinterpret_cast<double*>(tree_smem + kTreeStages * Ring::kStageB);  // [ntile][warps]
+  const bool producer = warp == kTreeWarps;
   if (tid == 0) {
-    for (int i = 0; i < kTreeStages; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < kTreeStages; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], kTreeWarps);
+    }
     fence_mbar_init_cluster();
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // tree_decide_kernel's records (PDL)
   const NodeDec* nds = T.ndec + (int64_t)b * nn;
   const ChildPQ* cpq = T.cpq + (int64_t)b * nn;
-  for (int c = tid; c < nn; c += kTreeThreads) {  // the tree and its per-node records, staged
+  for (int c = tid; c < nn; c += kTreeBlock) {  // the tree and its per-node records, staged
     par[c] = T.parent[(int64_t)b * nn + c];
     tok[c] = T.node_token[(int64_t)b * nn + c];
     irw[c] = P.irow[(int64_t)b * nn + c];
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
   // structure checks, one node per thread: (1) parent order, token range, distinct siblings;
   // (2) internal rows exactly for the nodes with children; then (3) node data errors — the
   // first error in that order wins (reading #12, #13; same order as the oracle)
-  for (int c = tid; c < nn; c += kTreeThreads) {
+  for (int c = tid; c < nn; c += kTreeBlock) {
     int e1 = 0, e2 = 0;
     if (c == 0) {
       if (par[0] != -1) e1 = COSINE_REQ_BAD_TREE;
@@ -353,7 +379,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
   }
   __syncthreads();
   if (s_act == 0) {
-    for (int c = tid; c < nn; c += kTreeThreads) { out[c] = -1; acc[c] = -1; }
+    for (int c = tid; c < nn; c += kTreeBlock) { out[c] = -1; acc[c] = -1; }
     if (tid == 0) { P.accept_len[b] = -1; P.status[b] = err; }
     return;
   }
@@ -413,49 +439,53 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
     const int act = s_act, jn = s_node, Nd = s_Nd;
     const TT* trow = (const TT*)P.target + ((int64_t)b * nn + jn) * P.ld_t;
     const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? irw[jn] : 0)) * N * P.ld_q;
-    // A pass: per-tile masses of the weights (mode, rr) into s_tile[0 .. ntile).
+    // A pass: per-tile masses of the weights (mode, rr) into s_tile[0 .. ntile).  The producer
+    // lane fills ring slots it .. it + ntile - 1; consumer warp w writes its partial of tile t to
+    // s_parts[t][w]; the tile sums (fixed order) follow one block barrier.
     auto pass = [&](int mode, int rr) {
-      if (tid == 0) {
-        fence_proxy_async_smem();
-        for (int i = 0; i < kTreeStages && i < ntile; ++i)
-          ring.issue((int)((it + i) % kTreeStages), i, P, trow, drow, Nd);
-      }
-      for (int64_t t = 0; t < ntile; ++t, ++it) {
-        const int stg = (int)(it % kTreeStages);
-        mbar_wait_parity(&s_full[stg], (it / kTreeStages) & 1u);
-        const unsigned char* sb = ring.base + stg * Ring::kStageB;
-        const int64_t g0 = t * kTG;
-        const int tg = (int)min((int64_t)kTG, P.ngroups - g0);
-        double m = 0.0;
-        for (int g = tid; g < tg; g += kTreeThreads) {
-          float w[8];
-          tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, g, (int)((g0 + g) * kGroup), (int)P.V, w);
-          m += (double)sum8(w);
-        }
-        m = warp_sum(m);
-        if (lane == 0) s_wp[t & 1][warp] = m;
-        __syncthreads();  // the stage is consumed
-        if (tid == 0) {
-          double mt = 0.0;
-          for (int w2 = 0; w2 < kTreeWarps; ++w2) mt += s_wp[t & 1][w2];
-          s_tile[t] = mt;
-          if (t + kTreeStages < ntile) {
-            fence_proxy_async_smem();
-            ring.issue(stg, t + kTreeStages, P, trow, drow, Nd);
+      if (producer) {
+        if (lane == 0)
+          for (int64_t t = 0; t < ntile; ++t) ring.fill(it + (uint32_t)t, t, P, trow, drow, Nd);
+      } else {
+        for (int64_t t = 0; t < ntile; ++t) {
+          const uint32_t pos = it + (uint32_t)t;
+          const int stg = (int)(pos % kTreeStages);
+          mbar_wait_parity(&s_full[stg], (pos / kTreeStages) & 1u);
+          const unsigned char* sb = ring.base + stg * Ring::kStageB;
+          const int64_t g0 = t * kTG;
+          const int tg = (int)min((int64_t)kTG, P.ngroups - g0);
+          double m = 0.0;
+          for (int g = tid; g < tg; g += kTreeThreads) {
+            float w[8];
+            tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, g, (int)((g0 + g) * kGroup), (int)P.V, w);
+            m += (double)sum8(w);
+          }
+          m = warp_sum(m);
+          if (lane == 0) {
+            s_parts[t * kTreeWarps + warp] = m;
+            mbar_arrive(&s_empty[stg]);  // this warp is done with the stage
           }
         }
+      }
+      it += (uint32_t)ntile;
+      __syncthreads();
+      for (int64_t t = tid; t < ntile; t += kTreeBlock) {
+        double mt = 0.0;
+        for (int w2 = 0; w2 < kTreeWarps; ++w2) mt += s_parts[t * kTreeWarps + w2];
+        s_tile[t] = mt;
       }
     };
     if (act == 1) {  // Z_{r+1}: per-tile masses of max(0, o_r - q_r), kept for the final draw
       pass(0, st.r);
       __syncthreads();
-      if (tid == 0) {
-        double Z = 0.0;
-        for (int64_t t2 = 0; t2 < ntile; ++t2) Z += s_tile[t2];
+      if (warp == 0) {
+        const double Z = tile_total(s_tile, ntile, lane);
+        if (lane == 0) {
         if (!(Z > 0.0)) deg = 1;  // all mass cancelled: o kept (reading #11)
         st.Zs[st.r] = Z;
         st.invZ[st.r] = (Z > 0.0) ? (float)(1.0 / Z) : 0.f;
         st.r++;
+        }
       }
       __syncthreads();
       continue;
@@ -481,9 +511,10 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
       pass(1, rr);
       __syncthreads();
     }
+    double Zf = 0.0;
+    if (warp == 0) Zf = tile_total(s_tile, ntile, lane);
     if (tid == 0) {
-      double Z = 0.0;
-      for (int64_t t2 = 0; t2 < ntile; ++t2) Z += s_tile[t2];
+      const double Z = Zf;
       const double t = s_u * Z;
       int64_t tstar = -1;
       double tc = 0.0, O = 0.0;
@@ -496,13 +527,12 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
       s_Z = Z;
       s_y = -1;
       s_margin = 0.f;
-      if (tstar >= 0) {
-        fence_proxy_async_smem();
-        ring.issue((int)(it % kTreeStages), tstar, P, trow, drow, Nd);
-      }
     }
     __syncthreads();
-    if (s_tstar >= 0) {  // the crossing tile, one group per thread: block scan of group masses
+    if (s_tstar >= 0 && producer) {
+      if (lane == 0) ring.fill(it, s_tstar, P, trow, drow, Nd);
+      ++it;
+    } else if (s_tstar >= 0) {  // the crossing tile, one group per thread: block scan of group masses
       const int stg = (int)(it % kTreeStages);
       mbar_wait_parity(&s_full[stg], (it / kTreeStages) & 1u);
       ++it;
@@ -535,7 +565,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
       if (lane == 0) s_last[warp] = last;
-      __syncthreads();
+      consumer_sync();
       double base = 0.0;
       for (int w2 = 0; w2 < warp; ++w2) base += s_ws[w2];
       const double excl_w = __shfl_up_sync(0xffffffffu, incl, 1);
@@ -555,7 +585,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) tree_walk_kernel(const TreePa
         s_y = vb + ef;
         s_margin = mg;
       }
-      __syncthreads();
+      consumer_sync();
       if (tid == 0 && s_y < 0) {  // rounding fallback: the last positive entry of the tile (reading #10)
         int lst = -1;
         for (int w2 = 0; w2 < kTreeWarps; ++w2) lst = max(lst, s_last[w2]);

@@ -1650,9 +1650,18 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
   }
   if (e == cudaSuccess) {
     lc.gridDim = dim3((unsigned)B, 1, 1);
-    lc.blockDim = dim3(kTreeThreads, 1, 1);
-    lc.dynamicSmemBytes = (size_t)tree_walk_smem(nmax);
-    e = cudaFuncSetAttribute(tf[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.dynamicSmemBytes);
+    lc.blockDim = dim3(kTreeBlock, 1, 1);
+    lc.dynamicSmemBytes = (size_t)tree_walk_smem(nmax, (ngroups + tg - 1) / tg);
+    cudaFuncAttributes fa;
+    int optin = 0;
+    e = cudaFuncGetAttributes(&fa, tf[1]);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);
+    if (e == cudaSuccess && fa.sharedSizeBytes + lc.dynamicSmemBytes > (size_t)optin) {
+      ctx->last_launches = 2;
+      return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary too wide for the tree walk's shared memory");
+    }
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tf[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.dynamicSmemBytes);
     if (e == cudaSuccess) e = cudaLaunchKernelEx(&lc, tf[1], T);
   }
   if (e != cudaSuccess) {
