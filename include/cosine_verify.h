@@ -89,9 +89,12 @@ typedef struct {
   cosine_dtype_t draft_dtype;
   cosine_draft_kind_t draft_kind;
   uint64_t seed;           /* Philox key                                                     */
-  int32_t nranks;          /* 1 = unsharded (batch sharding = independent contexts)          */
-  int32_t rank;
-  const void* nccl_unique_id; /* reserved for vocab sharding (nranks > 1)                    */
+  int32_t nranks;          /* 1 = unsharded (batch sharding = independent contexts);          */
+                           /* > 1 = vocabulary-sharded over nranks GPUs (<= 32), see below    */
+  int32_t rank;            /* this rank, in [0, nranks); shards concatenate in rank order     */
+  const void* nccl_unique_id; /* nranks > 1: COSINE_NCCL_UNIQUE_ID_BYTES from rank 0's        */
+                           /* cosine_nccl_unique_id(), identical on every rank (the caller    */
+                           /* broadcasts it); the context owns the NCCL communicator          */
   int32_t cluster_size;    /* 0 = automatic; else 1, 2, 4 or 8 CTAs per (request, position)  */
 } cosine_config_t;
 
@@ -116,6 +119,26 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
 cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx);
 /* Last error message of ctx (or of the calling thread's last failed init if ctx is NULL). */
 const char* cosine_last_error(cosine_ctx_t ctx);
+
+/*
+ * Vocabulary-sharded mode (SURVEY §8(e) "Vocab", config c5; logits from a tensor-parallel LM
+ * head).  Rank g's context has [vocab_begin, vocab_end) = its column shard; the
+ * shards of ranks 0..nranks-1 must tile [0, vocab_size) in rank order.  Every rank calls
+ * cosine_verify_batch collectively (same B, k, N, draft_tokens, draft_len, request_ids, step,
+ * modes, temperature) with ITS columns of every row (ld >= the shard width; token ids stay
+ * global); the outputs are identical on every rank and equal to the unsharded call on the full
+ * rows up to flagged near-ties.  Three NCCL all-gathers on `stream`: per-(request, position)
+ * row statistics and candidate gathers (~N^2 + 4N + 8 words), the local masses of the final
+ * draw (B doubles), the owner's token (B x 16 bytes).  ARGMAX selection only;
+ * cosine_fuse_drafts / cosine_sample_residual / cosine_verify_tree return COSINE_ERR_UNSUPPORTED
+ * on a sharded context.
+ *
+ * cosine_nccl_unique_id — write a fresh NCCL unique id (COSINE_NCCL_UNIQUE_ID_BYTES bytes, host
+ * memory) to `out`; call on rank 0 and broadcast.  capacity < the id size ->
+ * COSINE_ERR_INVALID_ARGUMENT; NCCL failure -> COSINE_ERR_NCCL.
+ */
+#define COSINE_NCCL_UNIQUE_ID_BYTES 128
+cosine_status_t cosine_nccl_unique_id(void* out, int64_t capacity);
 
 /*
  * cosine_fuse_drafts — Eq. 4 token fusion only (Alg. 1 TokenFusion P:376-381).

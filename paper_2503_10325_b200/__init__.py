@@ -14,12 +14,14 @@ from ._lib import (  # noqa: F401
     BF16, F32, DRAFT_LOGITS, DRAFT_PROBS, INFO_DEGENERATE, INFO_NEAR_TIE, SEL_ARGMAX, SEL_SAMPLE,
     W_CONF, W_POINT, W_UNIFORM, W_WINNER, Context, CosineError, cosine_fuse_drafts,
     cosine_last_launch_count, cosine_profile_enable, cosine_profile_read, cosine_sample_residual,
-    cosine_verify_batch, cosine_verify_destroy, cosine_verify_init, cosine_verify_tree,
+    cosine_nccl_unique_id, cosine_verify_batch, cosine_verify_destroy, cosine_verify_init,
+    cosine_verify_tree,
 )
 
 __all__ = [
     "Verifier", "cosine_verify_init", "cosine_verify_destroy", "cosine_fuse_drafts",
     "cosine_verify_batch", "cosine_sample_residual", "cosine_verify_tree", "cosine_last_launch_count",
+    "cosine_nccl_unique_id",
     "CosineError",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE", "DRAFT_PROBS",
     "DRAFT_LOGITS",
@@ -31,12 +33,13 @@ class Verifier:
 
     def __init__(self, vocab_size: int, *, max_batch: int, k: int, N: int, device: int = 0,
                  target_dtype=torch.bfloat16, draft_dtype=torch.bfloat16, draft_kind=DRAFT_PROBS,
-                 seed: int = 0, cluster_size: int = 0, debug: bool = False):
+                 seed: int = 0, cluster_size: int = 0, debug: bool = False, ctx=None):
+        """ctx: an existing context to adopt (e.g. sharding.init_vocab_sharded's)."""
         self.V, self.k, self.N, self.device = vocab_size, k, N, device
-        self.ctx = cosine_verify_init(vocab_size, device=device, max_batch=max_batch,
-                                      max_draft_len=k, max_drafters=N, target_dtype=target_dtype,
-                                      draft_dtype=draft_dtype, draft_kind=draft_kind, seed=seed,
-                                      cluster_size=cluster_size)
+        self.ctx = ctx if ctx is not None else cosine_verify_init(
+            vocab_size, device=device, max_batch=max_batch, max_draft_len=k, max_drafters=N,
+            target_dtype=target_dtype, draft_dtype=draft_dtype, draft_kind=draft_kind, seed=seed,
+            cluster_size=cluster_size)
         dev = torch.device("cuda", device)
         self.accept_len = torch.empty(max_batch, dtype=torch.int32, device=dev)
         self.out_tokens = torch.empty(max_batch, k + 1, dtype=torch.int32, device=dev)

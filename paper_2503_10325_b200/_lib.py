@@ -72,6 +72,8 @@ _lib.cosine_sample_residual.restype = ctypes.c_int
 _lib.cosine_verify_tree.argtypes = [_P, _P, _i32, _i32, _i32, _i32, _P, _P, _P, _P, _i64, _f32, _P, _i64,
                                     _P, _P, _u32, ctypes.c_int, _P, _P, _P, _P]
 _lib.cosine_verify_tree.restype = ctypes.c_int
+_lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
+_lib.cosine_nccl_unique_id.restype = ctypes.c_int
 _lib.cosine_profile_enable.argtypes = [_P, _i32]
 _lib.cosine_profile_enable.restype = ctypes.c_int
 _lib.cosine_profile_read.argtypes = [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]
@@ -80,7 +82,8 @@ _lib.cosine_profile_read.restype = ctypes.c_int
 EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_error",
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
-                    "cosine_verify_tree")
+                    "cosine_verify_tree", "cosine_nccl_unique_id")
+NCCL_UNIQUE_ID_BYTES = 128
 
 
 class CosineError(RuntimeError):
@@ -115,21 +118,39 @@ class Context:
         self.cfg = cfg
         self.device = cfg.device
         self.vocab_size = cfg.vocab_size
+        self.nranks, self.rank = cfg.nranks, cfg.rank
+        self.vocab_begin, self.vocab_end = cfg.vocab_begin, cfg.vocab_end
 
     def __repr__(self):
-        return f"Context(V={self.vocab_size}, device={self.device})"
+        return (f"Context(V={self.vocab_size}, shard=[{self.vocab_begin}, {self.vocab_end}), "
+                f"rank={self.rank}/{self.nranks}, device={self.device})")
+
+
+def cosine_nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 calls this and broadcasts the bytes)."""
+    buf = ctypes.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    _check(_lib.cosine_nccl_unique_id(buf, NCCL_UNIQUE_ID_BYTES), None)
+    return buf.raw
 
 
 def cosine_verify_init(vocab_size: int, *, device: int = 0, max_batch: int, max_draft_len: int,
                        max_drafters: int, target_dtype=torch.bfloat16, draft_dtype=torch.bfloat16,
                        draft_kind: int = DRAFT_PROBS, seed: int = 0, cluster_size: int = 0,
-                       max_tree_nodes: int = 0):
-    """Create a context on `device`; returns a Context."""
-    cfg = cosine_config_t(device=device, vocab_size=vocab_size, vocab_begin=0, vocab_end=vocab_size,
-                          max_batch=max_batch, max_draft_len=max_draft_len, max_drafters=max_drafters,
-                          max_tree_nodes=max_tree_nodes, target_dtype=_DT[target_dtype],
-                          draft_dtype=_DT[draft_dtype],
-                          draft_kind=draft_kind, seed=seed, nranks=1, rank=0, nccl_unique_id=None,
+                       max_tree_nodes: int = 0, nranks: int = 1, rank: int = 0,
+                       vocab_begin: int = 0, vocab_end: int | None = None,
+                       nccl_unique_id: bytes | None = None):
+    """Create a context on `device`; returns a Context.  nranks > 1: vocabulary-sharded over
+    nranks GPUs, this rank holding columns [vocab_begin, vocab_end) (collective init)."""
+    vocab_end = vocab_size if vocab_end is None else vocab_end
+    uid = None
+    if nccl_unique_id is not None:
+        uid = ctypes.create_string_buffer(bytes(nccl_unique_id), NCCL_UNIQUE_ID_BYTES)
+    cfg = cosine_config_t(device=device, vocab_size=vocab_size, vocab_begin=vocab_begin,
+                          vocab_end=vocab_end, max_batch=max_batch, max_draft_len=max_draft_len,
+                          max_drafters=max_drafters, max_tree_nodes=max_tree_nodes,
+                          target_dtype=_DT[target_dtype], draft_dtype=_DT[draft_dtype],
+                          draft_kind=draft_kind, seed=seed, nranks=nranks, rank=rank,
+                          nccl_unique_id=ctypes.cast(uid, _P) if uid is not None else None,
                           cluster_size=cluster_size)
     h = _P()
     _check(_lib.cosine_verify_init(ctypes.byref(cfg), ctypes.byref(h)), None)

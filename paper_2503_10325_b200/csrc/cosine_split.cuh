@@ -59,6 +59,17 @@ struct SplitParams {
   // tree mode (cosine_verify_tree): a unit is a node (b, j); rows via internal_row
   int tree, nn, I;           // nodes per request (J + 1), internal (drafter) rows per request
   const int32_t* irow;       // [B][nn] drafter row of node j, -1 for a leaf
+  // vocabulary-sharded mode (nranks > 1, cosine_shard.cuh): this rank holds columns
+  // [v0, v0 + V) of every row of a Vg-wide vocabulary; V, ngroups, gfull are the local ones
+  int shard, G, rank;
+  int64_t v0, Vg;
+  int rec_words;             // 32-bit words per ShardRec (depends on N)
+  uint32_t* rec_send;        // [units][rec_words] this rank's records
+  const uint32_t* rec_all;   // [G][units][rec_words] every rank's (all-gather)
+  double* zsend;             // [B] local mass of the final draw
+  const double* zall;        // [G][B]
+  struct YRec* ysend;        // [B] the owner's token (-1 elsewhere)
+  const struct YRec* yall;   // [G][B]
 };
 
 
@@ -343,90 +354,47 @@ struct PosDec {  // decisions of one position (shared memory of every CTA of the
   float sig[kMaxN], c[kMaxN], w[kMaxN];
 };
 
-// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131):
-// lane r combines chunk r's partial record (fixed-order shuffle reductions, fp64), lanes gather
-// o(X_n) and q_m(X_n), lane 0 writes the decision to *out (and the diagnostics if asked).
-template <typename TT, typename TQ, bool kLogits>
-__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
-                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
-  const int lane = threadIdx.x & 31;
-  const int N = P.N, C = P.C;
-  const int64_t unit = (int64_t)b * (P.k + 1) + i;
-  const bool has_d = i < g;
-  const bool greedy = P.greedy != 0;
-  const double k2 = (double)P.k2f;
-  const int ng = has_d ? N * (N + 1) : 0;
-  if (lane < ng) {
-    const int n = lane % N, m = lane / N;
-    const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
-    float v = 0.f;
-    if (tk >= 0 && (int64_t)tk < P.V) {
-      if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
-      else v = load_one((const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t, tk);
-    }
-    s_gxw[m * kMaxN + n] = v;
-    if (m == 0) s_tokw[n] = tk;
-  }
-  // ---- combine the partial records (chunk r in lane r) ----
-  const PartRec* parts = P.parts + unit * C;
-  const bool own = lane < C;
-  const float tmax = own ? parts[lane].tmax : kNegBig;
-  const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
-  PosDec pd;
+__device__ __forceinline__ void init_posdec(PosDec& pd) {
   pd.status = 0; pd.accept = 1; pd.xstar = -1; pd.amax = -1; pd.m_fa = INFINITY; pd.M = 0.f; pd.S = 0.0;
   pd.px = pd.qx = pd.u = NAN;
   for (int n = 0; n < kMaxN; ++n) { pd.a[n] = 0.f; pd.dm[n] = 0.f; pd.sig[n] = NAN; pd.c[n] = NAN; pd.w[n] = NAN; }
-  bool t_nf = false, t_empty = false, d_nf = false, d_empty = false, tok_bad = false, zero = false;
-  if (greedy) {
-    float bv = own ? tmax : -INFINITY;
-    int64_t bi = own ? parts[lane].targ : -1;
-    warp_argmax(bv, bi);
-    t_nf = (bad & 1) != 0;
-    t_empty = (bi < 0);
-    pd.amax = bi;
-    pd.M = bv;
-  } else {
-    const float M = warp_max(tmax);
-    const double tsum = own ? parts[lane].tsum : 0.0;
-    const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
-    pd.M = M;
-    pd.S = S;
-    t_nf = !isfinite(S) || !isfinite(M);
-    t_empty = !t_nf && !(S > 0.0);
-  }
-  double sig[kMaxN];
-  float dmax[kMaxN];
+}
+
+__device__ __forceinline__ void write_pos_debug(const SplitParams& P, int b, int i, bool has_d, const PosDec& pd) {
+  const cosine_debug_t& D = P.dbg;
+  const int64_t unit = (int64_t)b * (P.k + 1) + i;
+  if (D.row_max) D.row_max[unit] = pd.M;
+  if (D.row_sumexp) D.row_sumexp[unit] = P.greedy ? 0.f : (float)pd.S;
   if (has_d) {
-    if (bad & 2) d_nf = true;
-    for (int n = 0; n < N; ++n) {
-      double sv;
-      float mx = kNegBig;
-      const double ds = own ? parts[lane].dsum[n] : 0.0;
-      if (kLogits) {
-        const float dmr = own ? parts[lane].dmax[n] : kNegBig;
-        mx = warp_max(dmr);
-        sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
-        if (!isfinite(mx)) d_nf = true;
-      } else {
-        sv = warp_sum(ds);
-      }
-      sig[n] = sv;
-      dmax[n] = mx;
-      if (!isfinite(sv)) d_nf = true;
-      else if (!(sv > 0.0)) d_empty = true;
+    const int64_t o1 = (int64_t)b * P.k + i;
+    if (D.p_x) D.p_x[o1] = (float)pd.px;
+    if (D.q_x) D.q_x[o1] = (float)pd.qx;
+    if (D.accept_u) D.accept_u[o1] = (float)pd.u;
+    if (D.fused_tokens) D.fused_tokens[o1] = pd.xstar;
+    for (int n = 0; n < P.N; ++n) {
+      if (D.draft_norm) D.draft_norm[o1 * P.N + n] = pd.sig[n];
+      if (D.conf) D.conf[o1 * P.N + n] = pd.c[n];
+      if (D.weights) D.weights[o1 * P.N + n] = pd.w[n];
     }
   }
-  __syncwarp();
-  if (lane != 0) return;
-  const float* gx = s_gxw;
-  const int32_t* tok = s_tokw;
-  if (has_d)
-    for (int n = 0; n < N; ++n)
-      if (tok[n] < 0 || (int64_t)tok[n] >= P.V) tok_bad = true;
+}
+
+// Lane 0 of a decision warp: the position's decision from the combined row statistics (pd.M,
+// pd.S / pd.amax already set), the drafter normalisers sig / dmax and the gathered values
+// gx[m * kMaxN + n] = d_m(X_n) (m < N) and l(X_n) (m == N) (Eq. 4 fusion P:406-411, acceptance
+// P:130-131).  Shared by the single-GPU and the vocabulary-sharded decision kernels.
+template <bool kLogits>
+__device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i, bool has_d, bool tok_bad,
+                                             bool nonfinite, bool empty, const float* gx, const int32_t* tok,
+                                             const double* sig, const float* dmax, PosDec& pd) {
+  const int N = P.N;
+  const bool greedy = P.greedy != 0;
+  const double k2 = (double)P.k2f;
+  bool zero = false;
   int stc = 0;
   if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
-  else if (t_nf || d_nf) stc = COSINE_REQ_NONFINITE_INPUT;
-  else if (t_empty || d_empty) stc = COSINE_REQ_EMPTY_ROW;
+  else if (nonfinite) stc = COSINE_REQ_NONFINITE_INPUT;
+  else if (empty) stc = COSINE_REQ_EMPTY_ROW;
   // q_n(x) of a gathered drafter value (PROBS: d / sigma; LOGITS: softmax at the same k2)
   auto qval = [&](int m, double dv) {
     return kLogits ? exp2(dv * k2 - (double)dmax[m] * k2) / sig[m] : dv / sig[m];
@@ -483,23 +451,87 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
       pd.w[n] = (float)w[n];
     }
   }
-  *out = pd;
-  if (!write_debug) return;
-  const cosine_debug_t& D = P.dbg;
-  if (D.row_max) D.row_max[unit] = pd.M;
-  if (D.row_sumexp) D.row_sumexp[unit] = greedy ? 0.f : (float)pd.S;
+}
+
+// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131):
+// lane r combines chunk r's partial record (fixed-order shuffle reductions, fp64), lanes gather
+// o(X_n) and q_m(X_n), lane 0 writes the decision to *out (and the diagnostics if asked).
+template <typename TT, typename TQ, bool kLogits>
+__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
+                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
+  const int lane = threadIdx.x & 31;
+  const int N = P.N, C = P.C;
+  const int64_t unit = (int64_t)b * (P.k + 1) + i;
+  const bool has_d = i < g;
+  const bool greedy = P.greedy != 0;
+  const double k2 = (double)P.k2f;
+  const int ng = has_d ? N * (N + 1) : 0;
+  if (lane < ng) {
+    const int n = lane % N, m = lane / N;
+    const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
+    float v = 0.f;
+    if (tk >= 0 && (int64_t)tk < P.V) {
+      if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
+      else v = load_one((const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t, tk);
+    }
+    s_gxw[m * kMaxN + n] = v;
+    if (m == 0) s_tokw[n] = tk;
+  }
+  // ---- combine the partial records (chunk r in lane r) ----
+  const PartRec* parts = P.parts + unit * C;
+  const bool own = lane < C;
+  const float tmax = own ? parts[lane].tmax : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
+  PosDec pd;
+  init_posdec(pd);
+  bool t_nf = false, t_empty = false, d_nf = false, d_empty = false, tok_bad = false;
+  if (greedy) {
+    float bv = own ? tmax : -INFINITY;
+    int64_t bi = own ? parts[lane].targ : -1;
+    warp_argmax(bv, bi);
+    t_nf = (bad & 1) != 0;
+    t_empty = (bi < 0);
+    pd.amax = bi;
+    pd.M = bv;
+  } else {
+    const float M = warp_max(tmax);
+    const double tsum = own ? parts[lane].tsum : 0.0;
+    const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
+    pd.M = M;
+    pd.S = S;
+    t_nf = !isfinite(S) || !isfinite(M);
+    t_empty = !t_nf && !(S > 0.0);
+  }
+  double sig[kMaxN];
+  float dmax[kMaxN];
   if (has_d) {
-    const int64_t o1 = (int64_t)b * P.k + i;
-    if (D.p_x) D.p_x[o1] = (float)pd.px;
-    if (D.q_x) D.q_x[o1] = (float)pd.qx;
-    if (D.accept_u) D.accept_u[o1] = (float)pd.u;
-    if (D.fused_tokens) D.fused_tokens[o1] = pd.xstar;
+    if (bad & 2) d_nf = true;
     for (int n = 0; n < N; ++n) {
-      if (D.draft_norm) D.draft_norm[o1 * N + n] = pd.sig[n];
-      if (D.conf) D.conf[o1 * N + n] = pd.c[n];
-      if (D.weights) D.weights[o1 * N + n] = pd.w[n];
+      double sv;
+      float mx = kNegBig;
+      const double ds = own ? parts[lane].dsum[n] : 0.0;
+      if (kLogits) {
+        const float dmr = own ? parts[lane].dmax[n] : kNegBig;
+        mx = warp_max(dmr);
+        sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
+        if (!isfinite(mx)) d_nf = true;
+      } else {
+        sv = warp_sum(ds);
+      }
+      sig[n] = sv;
+      dmax[n] = mx;
+      if (!isfinite(sv)) d_nf = true;
+      else if (!(sv > 0.0)) d_empty = true;
     }
   }
+  __syncwarp();
+  if (lane != 0) return;
+  if (has_d)
+    for (int n = 0; n < N; ++n)
+      if (s_tokw[n] < 0 || (int64_t)s_tokw[n] >= P.V) tok_bad = true;
+  decide_lane0<kLogits>(P, b, i, has_d, tok_bad, t_nf || d_nf, t_empty || d_empty, s_gxw, s_tokw, sig, dmax, pd);
+  *out = pd;
+  if (write_debug) write_pos_debug(P, b, i, has_d, pd);
 }
 
 // Kernel B1: one warp per (request, position) -> PosDec in global memory (+ diagnostics).
@@ -543,7 +575,7 @@ __device__ __forceinline__ Decision sample_decision(const SplitParams& P, uint64
   Decision d;
   d.need = 1;
   d.kind = resid ? ((P.weight_mode == COSINE_W_POINT) ? kWPoint : kWResidual) : kWBonus;
-  d.xstar = pl.xstar;
+  d.xstar = pl.xstar - (int32_t)P.v0;  // local column (vocabulary-sharded mode)
   d.node = (uint32_t)v.L;
   d.u = philox_u24(P.seed, rid, (uint32_t)v.L, P.step, kTagSample);
   d.M = pl.M;
@@ -638,6 +670,10 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   const int g = P.draft_len ? P.draft_len[b] : P.k;
   int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
   if (g < 1 || g > P.k) {
+    if (P.shard) {  // the outputs come from shard_finish_kernel
+      if (part == 0 && tid == 0) P.zsend[b] = 0.0;
+      return;
+    }
     if (part == 0 && tid == 0) {
       P.accept_len[b] = -1;
       for (int j = 0; j <= P.k; ++j) out[j] = -1;
@@ -663,6 +699,10 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   __syncthreads();
   const ReqView v = s_v;
   if (!v.sample) {  // a per-request error, or greedy (y = argmax of row L, reading #7)
+    if (P.shard) {
+      if (part == 0 && tid == 0) P.zsend[b] = 0.0;
+      return;
+    }
     if (part == 0) {
       for (int j = tid; j <= P.k; j += kThreads)
         out[j] = v.err ? -1 : ((j < v.L) ? s_pd[j].xstar : (j == v.L ? (int32_t)s_pd[v.L].amax : -1));
@@ -716,6 +756,16 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   __shared__ int64_t s_tstar;
   __shared__ double s_tc, s_Z;
   __shared__ int s_kind, s_deg;
+  if (P.shard) {  // vocabulary-sharded: this rank's mass, in tile order; shard_sample_kernel goes on
+    if (tid == 0) {
+      P.counters[b] = 0;
+      const double* ss = P.segsum + (int64_t)b * P.nseg;
+      double Z = 0.0;
+      for (int64_t t = 0; t < P.nseg; ++t) Z += __ldcg(ss + t);
+      P.zsend[b] = Z;
+    }
+    return;
+  }
   if (tid == 0) {
     P.counters[b] = 0;  // ready for the next call
     const double* ss = P.segsum + (int64_t)b * P.nseg;

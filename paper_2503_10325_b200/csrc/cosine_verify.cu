@@ -16,6 +16,7 @@
 
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1070,6 +1071,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
 }  // namespace cosine
 #include "cosine_split.cuh"
 #include "cosine_tree.cuh"
+#include "cosine_shard.cuh"
 namespace cosine {
 
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
@@ -1118,6 +1120,24 @@ void pick_split(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, SplitF
   return pick_split2<float, float>(logits, N, f);
 }
 template <typename TT, typename TQ>
+void pick_shard2(bool logits, int N, SplitFn* f) {
+  if (logits) {
+    f[0] = shard_pack_kernel<TT, TQ, true>;
+    f[1] = shard_decide_kernel<true>;
+    f[2] = N <= 4 ? shard_sample_kernel<TT, TQ, true, 4> : shard_sample_kernel<TT, TQ, true, 8>;
+  } else {
+    f[0] = shard_pack_kernel<TT, TQ, false>;
+    f[1] = shard_decide_kernel<false>;
+    f[2] = N <= 4 ? shard_sample_kernel<TT, TQ, false, 4> : shard_sample_kernel<TT, TQ, false, 8>;
+  }
+}
+void pick_shard(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, SplitFn* f) {
+  if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_shard2<__nv_bfloat16, __nv_bfloat16>(logits, N, f);
+  if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_shard2<__nv_bfloat16, float>(logits, N, f);
+  if (tt == COSINE_F32 && tq == COSINE_BF16) return pick_shard2<float, __nv_bfloat16>(logits, N, f);
+  return pick_shard2<float, float>(logits, N, f);
+}
+template <typename TT, typename TQ>
 KernelFn pick_kernel2(bool logits, int N) {
   if (logits) return N <= 4 ? unit_kernel<TT, TQ, true, 4> : unit_kernel<TT, TQ, true, 8>;
   return N <= 4 ? unit_kernel<TT, TQ, false, 4> : unit_kernel<TT, TQ, false, 8>;
@@ -1158,6 +1178,14 @@ struct cosine_ctx_s {
   std::string err;
   int32_t last_launches = 0;
   int32_t last_cluster = 0, last_ncl = 0;
+  // vocabulary-sharded mode (nranks > 1)
+  ncclComm_t comm = nullptr;
+  uint32_t* rec_send = nullptr;
+  uint32_t* rec_all = nullptr;
+  double* zsend = nullptr;
+  double* zall = nullptr;
+  YRec* ysend = nullptr;
+  YRec* yall = nullptr;
 };
 
 static thread_local std::string g_init_error;
@@ -1301,6 +1329,93 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   return COSINE_OK;
 }
 
+// Vocabulary-sharded verification (cosine_shard.cuh): 7 kernels and 3 all-gathers on `stream`.
+cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, cosine_dtype_t tt,
+                             cosine_dtype_t tq, bool logits) {
+  SplitFn fa[3], fs[3];
+  pick_split(tt, tq, logits, S.N, fa);
+  pick_shard(tt, tq, logits, S.N, fs);
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  int C = 1;
+  if (ctx->cfg.cluster_size > 0) {
+    C = ctx->cfg.cluster_size;
+  } else {
+    while (C < kMaxC && S.ngroups > (int64_t)C * kThreads * 8) C *= 2;
+    while (C < kMaxC && units * C < 148 * 8 && S.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  }
+  S.C = C;
+  S.cg = (S.ngroups + C - 1) / C;
+  S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
+  S.spr = (int)((S.nseg + kSegTilesPerCta - 1) / kSegTilesPerCta);
+  S.parts = ctx->parts;
+  S.pdec = ctx->pdec;
+  S.segsum = ctx->segsum;
+  S.counters = ctx->counters;
+  S.b_off = 0;
+  S.nb = S.B;
+  S.shard = 1;
+  S.G = ctx->cfg.nranks;
+  S.rank = ctx->cfg.rank;
+  S.v0 = ctx->cfg.vocab_begin;
+  S.Vg = ctx->cfg.vocab_size;
+  S.rec_words = shard_rec_words(S.N);
+  S.rec_send = ctx->rec_send;
+  S.rec_all = ctx->rec_all;
+  S.zsend = ctx->zsend;
+  S.zall = ctx->zall;
+  S.ysend = ctx->ysend;
+  S.yall = ctx->yall;
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  const unsigned unit_blocks = (unsigned)((units + kWarps - 1) / kWarps);
+  auto launch = [&](SplitFn f, unsigned grid, bool pdl) {
+    lc.gridDim = dim3(grid, 1, 1);
+    lc.attrs = pdl ? at : nullptr;
+    lc.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&lc, f, S);
+  };
+  const char* stage = "stats";
+  cudaError_t e = launch(fa[0], (unsigned)(units * C), false);  // local row statistics
+  if (e == cudaSuccess) { stage = "pack"; e = launch(fs[0], unit_blocks, true); }
+  ncclResult_t r = ncclSuccess;
+  if (e == cudaSuccess) {
+    r = ncclAllGather(ctx->rec_send, ctx->rec_all, (size_t)units * S.rec_words * 4, ncclUint8, ctx->comm, stream);
+  }
+  if (e == cudaSuccess && r == ncclSuccess) { stage = "decide"; e = launch(fs[1], unit_blocks, false); }
+  if (e == cudaSuccess && r == ncclSuccess) { stage = "resample"; e = launch(fa[2], (unsigned)(S.B * S.spr), false); }
+  if (e == cudaSuccess && r == ncclSuccess)
+    r = ncclAllGather(ctx->zsend, ctx->zall, (size_t)S.B * sizeof(double), ncclUint8, ctx->comm, stream);
+  if (e == cudaSuccess && r == ncclSuccess) { stage = "sample"; e = launch(fs[2], (unsigned)S.B, false); }
+  if (e == cudaSuccess && r == ncclSuccess)
+    r = ncclAllGather(ctx->ysend, ctx->yall, (size_t)S.B * sizeof(YRec), ncclUint8, ctx->comm, stream);
+  if (e == cudaSuccess && r == ncclSuccess) {
+    stage = "finish";
+    lc.gridDim = dim3((unsigned)((S.B + kThreads - 1) / kThreads), 1, 1);
+    lc.attrs = nullptr;
+    lc.numAttrs = 0;
+    e = cudaLaunchKernelEx(&lc, shard_finish_kernel, S);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("sharded verify (") + stage + "): " + cudaGetErrorString(e));
+  }
+  if (r != ncclSuccess) {
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_NCCL, std::string("sharded verify all-gather: ") + ncclGetErrorString(r));
+  }
+  ctx->last_launches = 7;
+  ctx->last_cluster = C;
+  return COSINE_OK;
+}
+
 void fill_common(Params& P, const cosine_ctx_t ctx, int B, int k, int N, float T) {
   memset(&P, 0, sizeof(P));
   P.B = B;
@@ -1357,8 +1472,12 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     return fail(nullptr, COSINE_ERR_UNSUPPORTED, "dtype must be COSINE_BF16 or COSINE_F32");
   if (cfg->draft_kind != COSINE_DRAFT_PROBS && cfg->draft_kind != COSINE_DRAFT_LOGITS)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad draft_kind");
-  if (cfg->nranks != 1 || cfg->rank != 0 || cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab_size)
-    return fail(nullptr, COSINE_ERR_UNSUPPORTED, "vocabulary sharding (nranks > 1) is not built in this version");
+  if (cfg->nranks < 1 || cfg->nranks > 32 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks must be in [1, 32] and rank in [0, nranks)");
+  if (cfg->nranks == 1 && (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab_size))
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "an unsharded context covers [0, vocab_size)");
+  if (cfg->nranks > 1 && !cfg->nccl_unique_id)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks > 1 needs nccl_unique_id (cosine_nccl_unique_id on rank 0)");
   if (cfg->cluster_size != 0 && cfg->cluster_size != 1 && cfg->cluster_size != 2 &&
       cfg->cluster_size != 4 && cfg->cluster_size != 8 && cfg->cluster_size != 16)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cluster_size must be 0, 1, 2, 4, 8 or 16");
@@ -1393,9 +1512,33 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     init_scratch<<<(unsigned)((nb + 255) / 256), 256>>>(ctx->done, ctx->first_rej, (int)nb);
     e = cudaGetLastError();
   }
+  if (e == cudaSuccess && cfg->nranks > 1) {  // vocabulary-sharded: exchange buffers + communicator
+    const size_t units = nb * (size_t)(cfg->max_draft_len + 1);
+    const size_t rb = units * (size_t)shard_rec_words(cfg->max_drafters) * 4;
+    e = cudaMalloc(&ctx->rec_send, rb);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->rec_all, rb * (size_t)cfg->nranks);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->zsend, nb * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->zall, nb * sizeof(double) * (size_t)cfg->nranks);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->ysend, nb * sizeof(YRec));
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->yall, nb * sizeof(YRec) * (size_t)cfg->nranks);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    std::string msg = std::string("init: ") + cudaGetErrorString(e);
+  ncclResult_t nr = ncclSuccess;
+  if (e == cudaSuccess && cfg->nranks > 1) {
+    ncclUniqueId uid;
+    memcpy(&uid, cfg->nccl_unique_id, sizeof(uid));
+    nr = ncclCommInitRank(&ctx->comm, cfg->nranks, uid, cfg->rank);
+    if (nr != ncclSuccess) ctx->comm = nullptr;
+  }
+  if (e != cudaSuccess || nr != ncclSuccess) {
+    std::string msg = (e != cudaSuccess) ? std::string("init: ") + cudaGetErrorString(e)
+                                         : std::string("init: ncclCommInitRank: ") + ncclGetErrorString(nr);
+    cudaFree(ctx->rec_send);
+    cudaFree(ctx->rec_all);
+    cudaFree(ctx->zsend);
+    cudaFree(ctx->zall);
+    cudaFree(ctx->ysend);
+    cudaFree(ctx->yall);
     cudaGetLastError();
     cudaFree(ctx->recs);
     cudaFree(ctx->done);
@@ -1410,6 +1553,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
       if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     delete ctx;
+    if (e == cudaSuccess) return fail(nullptr, COSINE_ERR_NCCL, msg);
     return fail(nullptr, e == cudaErrorMemoryAllocation ? COSINE_ERR_OUT_OF_MEMORY : COSINE_ERR_CUDA, msg);
   }
   *out = ctx;
@@ -1429,6 +1573,13 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->ndec);
   cudaFree(ctx->cpq);
   cudaFree(ctx->segsum);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  cudaFree(ctx->rec_send);
+  cudaFree(ctx->rec_all);
+  cudaFree(ctx->zsend);
+  cudaFree(ctx->zall);
+  cudaFree(ctx->ysend);
+  cudaFree(ctx->yall);
   for (int j = 0; j <= kMaxChunks; ++j)
     if (ctx->ev[j]) cudaEventDestroy(ctx->ev[j]);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
@@ -1437,6 +1588,16 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
     cudaEventDestroy(pe.second);
   }
   delete ctx;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_nccl_unique_id(void* out, int64_t capacity) {
+  if (!out || capacity < (int64_t)sizeof(ncclUniqueId))
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "unique id buffer smaller than COSINE_NCCL_UNIQUE_ID_BYTES");
+  ncclUniqueId uid;
+  const ncclResult_t r = ncclGetUniqueId(&uid);
+  if (r != ncclSuccess) return fail(nullptr, COSINE_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(out, &uid, sizeof(uid));
   return COSINE_OK;
 }
 
@@ -1481,6 +1642,8 @@ cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int
                                    float* fused_q, int64_t ld_fq, int32_t* status) {
   cosine_status_t s = check_common(ctx, B, k, N);
   if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_fuse_drafts runs on unsharded contexts (nranks == 1)");
   if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
   if ((s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
   if (!draft_tokens || !request_ids || !fused_tokens || !status)
@@ -1558,6 +1721,20 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   P.status = status;
   if (debug) P.dbg = *debug;
   const char* force_v2 = getenv("COSINE_FORCE_CLUSTER_KERNEL");
+  if (ctx->cfg.nranks > 1) {  // vocabulary-sharded (cosine_shard.cuh)
+    if (select_mode != COSINE_SEL_ARGMAX)
+      return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary sharding takes ARGMAX selection");
+    SplitParams S;
+    memset(&S, 0, sizeof(S));
+    S.B = B; S.k = k; S.N = N;
+    S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+    S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+    S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+    S.rids = request_ids; S.seed = P.seed; S.step = step;
+    S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
+    return launch_shard(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                        ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+  }
   if (select_mode == COSINE_SEL_ARGMAX && !(force_v2 && force_v2[0] == '1')) {
     SplitParams S;
     memset(&S, 0, sizeof(S));
@@ -1585,6 +1762,8 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
                                    int32_t* out_tokens, int32_t* status) {
   cosine_status_t s = check_common(ctx, B, 1, N);
   if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_verify_tree runs on unsharded contexts (nranks == 1)");
   if (J < 0 || J + 1 > ctx->cfg.max_tree_nodes)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "J + 1 exceeds max_tree_nodes");
   if (I < 0 || I > J + 1) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "I outside [0, J + 1]");
@@ -1683,6 +1862,8 @@ cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream,
   const int Nc = draft_rows ? N : 1;
   cosine_status_t s = check_common(ctx, B, 1, Nc);
   if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_sample_residual runs on unsharded contexts (nranks == 1)");
   if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
   if ((s = check_rows(ctx, target_rows, ld_t, ctx->cfg.target_dtype, "target_rows")) != COSINE_OK) return s;
   if (draft_rows) {

@@ -73,3 +73,43 @@ def test_shard_ranges():
     assert list(sharding.weak_request_ids(4, 2)) == [8, 9, 10, 11]
     with pytest.raises(ValueError):
         sharding.shard_range(4, 2, 2)
+
+
+def _vocab_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_10325_b200 import sharding
+    # the unique-id broadcast of init_vocab_sharded, with a stand-in id (no NCCL on CPU)
+    obj = [bytes(range(128)) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    shards = [sharding.vocab_shard(128256, world, r) for r in range(world)]
+    if rank == 0:
+        q.put((obj[0], shards))
+    else:
+        q.put((obj[0], None))
+    dist.destroy_process_group()
+
+
+def test_two_rank_vocab_shard_plumbing():
+    """Host logic of the vocabulary-sharded mode: both ranks receive rank 0's id bytes, and the
+    column shards tile [0, V) in rank order (c5: 8 x 16032)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vocab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(g[0] == bytes(range(128)) for g in got)
+    shards = [g[1] for g in got if g[1] is not None][0]
+    assert shards == [(0, 64128), (64128, 128256)]
+    from paper_2503_10325_b200 import sharding
+    for V, G in [(128256, 8), (5003, 3), (32000, 4), (17, 2)]:
+        sh = [sharding.vocab_shard(V, G, r) for r in range(G)]
+        assert sh[0][0] == 0 and sh[-1][1] == V
+        assert all(sh[r][1] == sh[r + 1][0] and sh[r][0] < sh[r][1] for r in range(G - 1))
+    assert [sharding.vocab_shard(128256, 8, r)[1] - sharding.vocab_shard(128256, 8, r)[0] for r in range(8)] == [16032] * 8
