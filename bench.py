@@ -34,6 +34,8 @@ WORKLOADS = {
     "c3": "c3: batch=256, 4 drafters, k=8, vocab=128256 (Llama-3), bf16 logits/probs, CONF fusion, T=1",
     "c4": "c4: tree-shaped drafts, 64-node tree per request (schedule 4,2,2,1,1,1,1,1), batch=128, "
           "4 drafters, vocab=128256, bf16, CONF fusion, T=1",
+    "c5": "c5: batch=1024, 4 drafters, k=8, vocab=128256 (Llama-3) split in N column shards (tensor-parallel "
+          "LM head layout), bf16, CONF fusion, T=1, vocabulary-sharded verification over NCCL",
 }
 
 
@@ -202,6 +204,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if args.config == "c4":
         return run_tree(args, c, dev, world, rank, local)
+    if args.config == "c5":
+        return run_vocab(args, c, dev, world, rank, local)
     rids = sharding.weak_request_ids(B, rank)  # weak scaling: a full batch per rank, global ids
     inp = synth.linear_inputs(B, k, N, V, dtype=dt, seed=args.seed + 7919 * rank, device=dev,
                               rid_base=rids.start)
@@ -394,6 +398,105 @@ def run_tree(args, c, dev, world, rank, local):
         }
         print(json.dumps(line), flush=True)
     cv.cosine_verify_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_vocab(args, c, dev, world, rank, local):
+    """c5: the same B = 1024 requests on every rank, each rank holding 1/N of the vocabulary
+    columns; one collective cosine_verify_batch per step (7 kernels + 3 NCCL
+    all-gathers).  Total work is fixed: strong scaling; value = B k / step time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2503_10325_b200 as cv
+    from paper_2503_10325_b200 import sharding, synth
+    B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
+    esz = torch.tensor([], dtype=dt).element_size()
+    vb, ve = sharding.vocab_shard(V, world, rank)
+    W = ve - vb
+    ld = (W + 7) // 8 * 8
+    # the same global inputs on every rank (seeded), this rank's columns kept, generated in
+    # request slices so that only one slice of the full rows exists at a time
+    tgt = torch.empty(B, k + 1, ld, dtype=dt, device=dev)
+    drf = torch.empty(B, k, N, ld, dtype=dt, device=dev)
+    xs, rids = [], []
+    sl = 64
+    for b0 in range(0, B, sl):
+        part = synth.linear_inputs(sl, k, N, V, dtype=dt, seed=args.seed + b0, device=dev, rid_base=b0)
+        tgt[b0:b0 + sl, :, :W] = part["target"][..., vb:ve]
+        drf[b0:b0 + sl, :, :, :W] = part["draft"][..., vb:ve]
+        xs.append(part["draft_tokens"])
+        rids.append(part["request_ids"])
+        del part
+    toks, rid = torch.cat(xs), torch.cat(rids)
+    if world > 1:
+        ctx = sharding.init_vocab_sharded(V, device=local, max_batch=B, max_draft_len=k, max_drafters=N,
+                                          target_dtype=dt, draft_dtype=dt, seed=args.seed)
+    else:
+        ctx = cv.cosine_verify_init(V, device=local, max_batch=B, max_draft_len=k, max_drafters=N,
+                                    target_dtype=dt, draft_dtype=dt, seed=args.seed)
+    ver = cv.Verifier(V, max_batch=B, k=k, N=N, device=local, ctx=ctx)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ver.verify(tgt, drf, toks, rid, temperature=1.0)
+        return cv.cosine_last_launch_count(ver.ctx)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        launches += step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.stop_ev.set()
+    sampler.join()
+    ms = sharding.max_over_ranks(e0.elapsed_time(e1), device=dev) / args.steps
+    cv.cosine_profile_enable(ver.ctx, True)
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    stats_ms, stats_n = cv.cosine_profile_read(ver.ctx)
+    cv.cosine_profile_enable(ver.ctx, False)
+    kern_s = max(sharding.max_over_ranks(stats_ms / max(stats_n, 1), device=dev) / 1e3, 1e-9)
+    acc = ver.accept_len[:B].float().mean().item()
+    errs = int((ver.status[:B] & 0xff).ne(0).sum().item())
+    alg_rank = (B * (k + 1) * W * esz + B * k * N * W * esz + 4 * B * k * N + 8 * B)
+    alg_total = synth.algorithmic_bytes(B, k, N, V, esz, esz)
+    peak, peak_src = peaks()
+    achieved = alg_rank / kern_s / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": B * k / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOADS["c5"], "global_batch": B, "k": k, "drafters": N, "vocab": V,
+                       "shard_columns": W, "parallelism": f"vocab-sharded x{world}", "mean_accept_len": acc,
+                       "request_errors": errs,
+                       "l2": f"inputs {alg_rank / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "cosine::stats_kernel (local columns)", "kernel_us": kern_s * 1e6,
+                         "algorithmic_bytes_per_launch": alg_rank, "algorithmic_bytes_total": alg_total,
+                         "step_achieved_per_gpu": alg_rank / (ms / 1e3) / 1e9,
+                         "step_frac": alg_rank / (ms / 1e3) / 1e9 / peak},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": sampler.result(),
+        }
+        print(json.dumps(line), flush=True)
+    ver.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -1382,8 +1382,21 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
     return cudaLaunchKernelEx(&lc, f, S);
   };
   const char* stage = "stats";
+  cudaEvent_t pe1 = nullptr;
+  if (ctx->prof_on) {  // live timing of the dominant kernel (as in launch_split)
+    if (ctx->prof_n == ctx->prof_ev.size()) {
+      cudaEvent_t a0, a1;
+      cudaEventCreate(&a0);
+      cudaEventCreate(&a1);
+      ctx->prof_ev.emplace_back(a0, a1);
+    }
+    cudaEventRecord(ctx->prof_ev[ctx->prof_n].first, stream);
+    pe1 = ctx->prof_ev[ctx->prof_n].second;
+    ctx->prof_n++;
+  }
   cudaError_t e = launch(fa[0], (unsigned)(units * C), false);  // local row statistics
-  if (e == cudaSuccess) { stage = "pack"; e = launch(fs[0], unit_blocks, true); }
+  if (pe1) cudaEventRecord(pe1, stream);
+  if (e == cudaSuccess) { stage = "pack"; e = launch(fs[0], unit_blocks, pe1 == nullptr); }
   ncclResult_t r = ncclSuccess;
   if (e == cudaSuccess) {
     r = ncclAllGather(ctx->rec_send, ctx->rec_all, (size_t)units * S.rec_words * 4, ncclUint8, ctx->comm, stream);
