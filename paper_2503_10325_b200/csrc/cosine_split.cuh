@@ -52,6 +52,12 @@ struct SplitParams {
   PartRec* parts;
   struct PosDec* pdec;
   int32_t* counters;  // [B] CTAs of a request done (kernel B), reset by the last one
+  // fine-grained dependencies (single-GPU linear path): kernels B1 and B2 are programmatic
+  // dependents scheduled into the previous kernel's tail wave; B1 waits for its unit's C chunk
+  // records, B2 for its request's g + 1 decisions, instead of for the whole previous grid
+  int fused;
+  int32_t* ucnt;      // [B][k+1] chunk CTAs of a unit done (kernel A), reset by kernel B1
+  int32_t* dcnt;      // [B] units of a request decided (kernel B1), reset by the request's last B2 CTA
   double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
   int64_t nseg;
   int spr;         // B2a CTAs per request
@@ -147,6 +153,11 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
   const int rank = (int)(blockIdx.x % C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = P.N;
+  // every CTA of this grid is resident or done once all passed this point: kernel B (launched
+  // as a programmatic dependent) may then be scheduled into the tail wave (it waits per request)
+#ifndef COSINE_NO_LAUNCH_DEP
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   int Nd;
   const TT* trow;
   const TQ* drow;
@@ -342,6 +353,13 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
       rec->dsum[n] = sacc;
     }
   }
+  if (P.fused) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();  // the record before the count (release)
+      atomicAdd(&P.ucnt[unit], 1);
+    }
+  }
 }
 
 // ============================== kernel B ==============================
@@ -478,16 +496,16 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     if (m == 0) s_tokw[n] = tk;
   }
   // ---- combine the partial records (chunk r in lane r) ----
-  const PartRec* parts = P.parts + unit * C;
+  const PartRec* parts = P.parts + unit * C;  // L2 reads (written by other CTAs, maybe this kernel)
   const bool own = lane < C;
-  const float tmax = own ? parts[lane].tmax : kNegBig;
-  const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
+  const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
   PosDec pd;
   init_posdec(pd);
   bool t_nf = false, t_empty = false, d_nf = false, d_empty = false, tok_bad = false;
   if (greedy) {
     float bv = own ? tmax : -INFINITY;
-    int64_t bi = own ? parts[lane].targ : -1;
+    int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
     warp_argmax(bv, bi);
     t_nf = (bad & 1) != 0;
     t_empty = (bi < 0);
@@ -495,7 +513,7 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     pd.M = bv;
   } else {
     const float M = warp_max(tmax);
-    const double tsum = own ? parts[lane].tsum : 0.0;
+    const double tsum = own ? __ldcg(&parts[lane].tsum) : 0.0;
     const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
     pd.M = M;
     pd.S = S;
@@ -509,9 +527,9 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     for (int n = 0; n < N; ++n) {
       double sv;
       float mx = kNegBig;
-      const double ds = own ? parts[lane].dsum[n] : 0.0;
+      const double ds = own ? __ldcg(&parts[lane].dsum[n]) : 0.0;
       if (kLogits) {
-        const float dmr = own ? parts[lane].dmax[n] : kNegBig;
+        const float dmr = own ? __ldcg(&parts[lane].dmax[n]) : kNegBig;
         mx = warp_max(dmr);
         sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
         if (!isfinite(mx)) d_nf = true;
@@ -541,12 +559,30 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
   __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
   __shared__ int32_t s_tok[kWarps][kMaxN];
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel A's partial records (PDL)
-  if (unit >= (int64_t)P.B * (P.k + 1)) return;
-  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  if (!P.fused) asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel A's records (PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (unit >= (int64_t)P.nb * (P.k + 1)) return;
+  const int b = P.b_off + (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
   const int g = P.draft_len ? P.draft_len[b] : P.k;
   if (g < 1 || g > P.k || i > g) return;
-  warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[unit], true);
+  const int64_t gu = (int64_t)b * (P.k + 1) + i;
+  if (P.fused) {  // this unit's C chunk records (every kernel-A CTA is resident or done by now)
+    if ((threadIdx.x & 31) == 0) {
+      uint32_t n;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.ucnt + gu) : "memory");
+        if ((int)n >= P.C) break;
+        __nanosleep(100);
+      }
+    }
+    __syncwarp();
+  }
+  warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[gu], true);
+  if (P.fused && (threadIdx.x & 31) == 0) {
+    P.ucnt[gu] = 0;  // ready for the next call
+    __threadfence();  // the decision before its count (release)
+    atomicAdd(&P.dcnt[b], 1);
+  }
 }
 
 // The request-level view of the position decisions (first error, first rejection L, margins).
@@ -666,8 +702,25 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   __shared__ float s_margin;
   __shared__ int s_last;
 
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B1's decisions (PDL)
   const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (P.fused) {
+    // kernel A decides the units itself and counts them per request: wait for this request's
+    // g + 1 decisions only (every kernel-A CTA is resident or done once this CTA runs, so the
+    // wait always ends), not for the whole grid
+    if (g >= 1 && g <= P.k) {
+      if (tid == 0) {
+        uint32_t n;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.dcnt + b) : "memory");
+          if ((int)n >= g + 1) break;
+          __nanosleep(200);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B1's decisions (PDL)
+  }
   int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
   if (g < 1 || g > P.k) {
     if (P.shard) {  // the outputs come from shard_finish_kernel
@@ -688,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     const int nw = (int)(sizeof(PosDec) / 4);
     const uint32_t* src = reinterpret_cast<const uint32_t*>(gpd);
     uint32_t* dst = reinterpret_cast<uint32_t*>(s_pd);
-    for (int w = tid; w < (g + 1) * nw; w += kThreads) dst[w] = src[w];
+    for (int w = tid; w < (g + 1) * nw; w += kThreads) dst[w] = __ldcg(src + w);
   }
   __syncthreads();
   if (tid == 0) {
@@ -702,6 +755,10 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     if (P.shard) {
       if (part == 0 && tid == 0) P.zsend[b] = 0.0;
       return;
+    }
+    if (P.fused && tid == 0) {  // the request's last B CTA resets the counters for the next call
+      const int old = atomicAdd(&P.counters[b], 1);
+      if (old == P.spr - 1) { P.counters[b] = 0; P.dcnt[b] = 0; }
     }
     if (part == 0) {
       for (int j = tid; j <= P.k; j += kThreads)
@@ -748,6 +805,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     __threadfence();
     const int old = atomicAdd(&P.counters[b], 1);
     s_last = (old == P.spr - 1);
+    if (s_last && P.fused) P.dcnt[b] = 0;  // every B CTA of the request has passed its wait
   }
   __syncthreads();
   if (!s_last) return;

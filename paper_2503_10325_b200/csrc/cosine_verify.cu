@@ -1288,8 +1288,16 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  S.b_off = 0;
-  S.nb = S.B;
+  // Batch pipelining (experiment, COSINE_CHUNKS=n): the requests are split into n slices; slice
+  // c's statistics stream on `stream` while the decisions + final draws of slice c-1 run on the
+  // high-priority aux stream (fork / join by events, capturable in a CUDA graph).  Measured on
+  // c3 (profiles/r1_ncu_summary.md): 1 slice 486 us, 2 -> 502, 4 -> 527, 8 -> 630 — every slice
+  // boundary adds a stats-kernel tail, more than the hidden B phase saves — so the default is 1.
+  int nch = 1;
+  if (const char* ev = getenv("COSINE_CHUNKS")) nch = atoi(ev);
+  nch = std::max(1, std::min(nch, std::min(kMaxChunks - 1, S.B)));
+  const int cb = (S.B + nch - 1) / nch;
+  nch = (S.B + cb - 1) / cb;
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   if (ctx->prof_on) {
     if (ctx->prof_n == ctx->prof_ev.size()) {
@@ -1303,22 +1311,85 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
     ctx->prof_n++;
     cudaEventRecord(pe0, stream);
   }
-  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
-  cudaError_t e = cudaLaunchKernelEx(&lc, fn[0], S);  // kernel A
-  if (pe1) cudaEventRecord(pe1, stream);
-  if (e == cudaSuccess) {  // kernel B1 (decisions), a programmatic dependent of A
-    lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
-    lc.attrs = pe1 ? nullptr : at;  // (an event record between the two breaks PDL anyway)
-    lc.numAttrs = pe1 ? 0 : 1;
-    e = cudaLaunchKernelEx(&lc, fn[1], S);
+  cudaError_t e = cudaSuccess;
+  int launches = 0;
+  const char* nofuse = getenv("COSINE_NOFUSE");
+  if (nch == 1 && nofuse && nofuse[0] == '1') {  // (experiment) kernel A -> B1 -> B2 with PDL
+    S.b_off = 0;
+    S.nb = S.B;
+    lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+    e = cudaLaunchKernelEx(&lc, fn[0], S);
+    if (pe1) cudaEventRecord(pe1, stream);
+    if (e == cudaSuccess) {
+      lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+      lc.attrs = pe1 ? nullptr : at;
+      lc.numAttrs = pe1 ? 0 : 1;
+      e = cudaLaunchKernelEx(&lc, fn[1], S);
+    }
+    if (e == cudaSuccess) {
+      lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, fn[2], S);
+    }
+    launches = 3;
+  } else if (nch == 1) {
+    // A -> B1 -> B2, each a programmatic dependent of the previous one: B1 / B2 CTAs are
+    // scheduled into the previous grid's tail wave and wait per unit / per request (counters)
+    S.b_off = 0;
+    S.nb = S.B;
+    S.fused = 1;
+    S.dcnt = ctx->counters + std::max(ctx->cfg.max_batch, 1);
+    S.ucnt = ctx->counters + 2 * (size_t)std::max(ctx->cfg.max_batch, 1);
+    lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+    e = cudaLaunchKernelEx(&lc, fn[0], S);  // kernel A
+    if (pe1) cudaEventRecord(pe1, stream);
+    if (e == cudaSuccess) {  // kernel B1 (decisions)
+      lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+      lc.attrs = pe1 ? nullptr : at;  // (an event record between the two breaks PDL)
+      lc.numAttrs = pe1 ? 0 : 1;
+      e = cudaLaunchKernelEx(&lc, fn[1], S);
+    }
+    if (e == cudaSuccess) {  // kernel B2 (first rejection + resample)
+      lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, fn[2], S);
+    }
+    launches = 3;
+  } else {
+    e = cudaEventRecord(ctx->ev[0], stream);  // fork: aux waits for the work already on `stream`
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->ev[0], 0);
+    cudaLaunchConfig_t lb = lc;
+    lb.stream = ctx->aux;
+    for (int c = 0; c < nch && e == cudaSuccess; ++c) {
+      S.b_off = c * cb;
+      S.nb = std::min(cb, S.B - S.b_off);
+      const int64_t cu = (int64_t)S.nb * (S.k + 1);
+      lc.gridDim = dim3((unsigned)(cu * C), 1, 1);
+      lc.attrs = nullptr;
+      lc.numAttrs = 0;
+      e = cudaLaunchKernelEx(&lc, fn[0], S);  // kernel A of slice c on `stream`
+      if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[c + 1], stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->ev[c + 1], 0);
+      if (e == cudaSuccess) {  // B1 + B2 of slice c on aux
+        lb.gridDim = dim3((unsigned)((cu + kWarps - 1) / kWarps), 1, 1);
+        lb.attrs = nullptr;
+        lb.numAttrs = 0;
+        e = cudaLaunchKernelEx(&lb, fn[1], S);
+      }
+      if (e == cudaSuccess) {
+        lb.gridDim = dim3((unsigned)(S.nb * S.spr), 1, 1);
+        lb.attrs = at;
+        lb.numAttrs = 1;
+        e = cudaLaunchKernelEx(&lb, fn[2], S);
+      }
+      launches += 3;
+    }
+    if (pe1 && e == cudaSuccess) cudaEventRecord(pe1, stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[kMaxChunks], ctx->aux);  // join
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ctx->ev[kMaxChunks], 0);
   }
-  if (e == cudaSuccess) {  // kernel B2 (first rejection + resample), dependent of B1
-    lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&lc, fn[2], S);
-  }
-  const int launches = 3;
   if (e != cudaSuccess) {
     cudaGetLastError();
     ctx->last_launches = 0;
@@ -1510,8 +1581,10 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   if (e == cudaSuccess) e = cudaMalloc(&ctx->cpq, nt * sizeof(ChildPQ));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->parts, nu * kMaxC * sizeof(PartRec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, nb * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, nb * sizeof(int32_t));
+  // counters: [B] kernel-B CTAs per request | [B] decided units per request | [B][k+1] chunks per unit
+  const size_t ncnt = 2 * nb + nb * (size_t)(cfg->max_draft_len + 1);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, ncnt * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, ncnt * sizeof(int32_t));
   ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
   if (e == cudaSuccess) {
