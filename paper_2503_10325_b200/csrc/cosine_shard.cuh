@@ -297,17 +297,21 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
     s_Z = Z;
     s_tc = t - Oown;
     s_tstar = -1;
-    if (owner == P.rank && !deg) {  // this rank's crossing tile
+    if (owner == P.rank && !deg && fb) {  // rounding past the total: the last positive tile
       const double* ss = P.segsum + (int64_t)b * P.nseg;
-      double Ol = 0.0;
-      int64_t last = -1;
-      for (int64_t s2 = 0; s2 < P.nseg; ++s2) {
-        const double z = __ldcg(ss + s2);
-        if (z > 0.0) last = s2;
-        if (!fb && Ol + z > s_tc) { s_tstar = s2; s_tc = s_tc - Ol; break; }
-        Ol += z;
-      }
-      if (s_tstar < 0) { s_tstar = last; s_tc = INFINITY; }  // -> the tile's last positive entry
+      for (int64_t s2 = P.nseg - 1; s2 >= 0; --s2)
+        if (__ldcg(ss + s2) > 0.0) { s_tstar = s2; break; }
+      s_tc = INFINITY;
+    }
+  }
+  __syncthreads();
+  if (s_owner == P.rank && !s_deg && !s_fb && threadIdx.x < 32) {  // this rank's crossing tile
+    int64_t ts;
+    double tc;
+    warp_tile_crossing<true>(P.segsum + (int64_t)b * P.nseg, P.nseg, 0.0, &ts, &tc, s_tc);
+    if (threadIdx.x == 0) {
+      s_tstar = ts;
+      s_tc = (ts >= 0) ? tc : INFINITY;
     }
   }
   __syncthreads();

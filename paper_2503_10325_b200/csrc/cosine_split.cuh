@@ -58,6 +58,11 @@ struct SplitParams {
   int fused;
   int32_t* ucnt;      // [B][k+1] chunk CTAs of a unit done (kernel A), reset by kernel B1
   int32_t* dcnt;      // [B] units of a request decided (kernel B1), reset by the request's last B2 CTA
+  // lazy verification (NEXT-1, cosine_verify_batch_lazy): lazy = r + 1 in round r, which
+  // streams position r of the requests still verifying (0 = off); lz[b] = 0 while request b
+  // verifies, -1 once it stopped
+  int lazy;
+  int32_t* lz;
   double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
   int64_t nseg;
   int spr;         // B2a CTAs per request
@@ -161,19 +166,29 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
   int Nd;
   const TT* trow;
   const TQ* drow;
+  int64_t gu;  // the unit's index in the partial-record array
   if (P.tree) {  // node (b, j): target row j, the N drafter rows of its internal row (if any)
     const int b = (int)(unit / P.nn);
     const int ir = P.irow[unit];
     Nd = (ir >= 0 && ir < P.I) ? N : 0;
     trow = (const TT*)P.target + unit * P.ld_t;
     drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? ir : 0)) * N * P.ld_q;
+    gu = unit;
   } else {
-    const int b = P.b_off + (int)(unit / (P.k + 1));
-    const int i = (int)(unit % (P.k + 1));
+    int b, i;
+    if (P.lazy) {  // lazy round r (NEXT-1): position r of the requests still verifying
+      b = (int)unit;
+      i = P.lazy - 1;
+      if (i > 0 && P.lz[b] != 0) return;
+    } else {
+      b = P.b_off + (int)(unit / (P.k + 1));
+      i = (int)(unit % (P.k + 1));
+    }
     const int g = P.draft_len ? P.draft_len[b] : P.k;
     if (g < 1 || g > P.k || i > g) return;  // rows past gamma_b are never read
     Nd = (i < g) ? N : 0;
-    trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t;
+    gu = (int64_t)b * (P.k + 1) + i;
+    trow = (const TT*)P.target + gu * P.ld_t;
     drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
   }
 
@@ -323,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
   }
   __syncthreads();
   if (tid < 32) {  // warp 0 assembles the record: lane j owns field j
-    PartRec* rec = P.parts + ((int64_t)P.b_off * (P.k + 1) + unit) * C + rank;
+    PartRec* rec = P.parts + gu * C + rank;
     if (lane == 0) {
       float bv = Mc;
       int64_t bi = -1;
@@ -357,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
     __syncthreads();
     if (tid == 0) {
       __threadfence();  // the record before the count (release)
-      atomicAdd(&P.ucnt[unit], 1);
+      atomicAdd(&P.ucnt[gu], 1);
     }
   }
 }
@@ -585,6 +600,37 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   }
 }
 
+// Lazy round r (NEXT-1): one warp per request still verifying decides position r (as
+// decide_kernel), then stops the request at its first rejection / error / bonus row.  The
+// positions after the stop are never read; their decision slots are written as "accepted, OK"
+// so that the request view of resample_kernel sees L and the errors of positions <= L only.
+template <typename TT, typename TQ, bool kLogits>
+__global__ void __launch_bounds__(kThreads) lazy_decide_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x * kWarps + warp;
+  __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kWarps][kMaxN];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // this round's partial records (PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (b >= P.B) return;
+  const int r = P.lazy - 1;
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (g < 1 || g > P.k || r > g) return;
+  if (r > 0 && P.lz[b] != 0) return;
+  PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
+  warp_decide<TT, TQ, kLogits>(P, b, r, g, s_gx[warp], s_tok[warp], &pds[r], true);
+  __syncwarp();
+  if (lane != 0) return;
+  const PosDec& pd = pds[r];
+  const bool stop = pd.status != 0 || r == g || !pd.accept;
+  P.lz[b] = stop ? -1 : 0;
+  if (stop) {
+    PosDec ok;
+    init_posdec(ok);
+    for (int j = r + 1; j <= g; ++j) pds[j] = ok;
+  }
+}
+
 // The request-level view of the position decisions (first error, first rejection L, margins).
 struct ReqView {
   int32_t g, err, L, sample;  // sample: T > 0 and no error -> a final inverse-CDF draw at row L
@@ -676,6 +722,55 @@ __device__ __forceinline__ float group_mass(const RowGroups<TT, TQ, NMAX>& rg, c
     w[e] = x;
   }
   return sum8(w);
+}
+
+
+// One warp: Z = sum of the tile masses seg[0 .. nseg) in a fixed order (lane l owns a contiguous
+// run of tiles, then a warp scan), and the crossing tile of t = u * Z: the smallest s with
+// O_s + seg[s] > t (O_s = the masses before s) and tc = t - O_s.  If rounding leaves no crossing
+// in the owning lane's run, tstar = that run's last positive tile with tc = +inf (the scan then
+// takes the tile's last positive entry, reading #10).  All lanes return Z; lane 0 tstar / tc.
+template <bool kGlobal>
+__device__ __forceinline__ double warp_tile_crossing(const double* seg, int64_t nseg, double u,
+                                                     int64_t* tstar, double* tc, double t_abs = -1.0) {
+  const int lane = threadIdx.x & 31;
+  auto at = [&](int64_t s2) { return kGlobal ? __ldcg(seg + s2) : seg[s2]; };
+  const int64_t per = (nseg + 31) / 32;
+  const int64_t s0 = min(nseg, lane * per), s1 = min(nseg, s0 + per);
+  double part = 0.0;
+  for (int64_t s2 = s0; s2 < s1; ++s2) part += at(s2);
+  double incl = part;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += nb;
+  }
+  const double Z = __shfl_sync(0xffffffffu, incl, 31);
+  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.0;
+  const double t = (t_abs >= 0.0) ? t_abs : u * Z;  // t_abs: an absolute target (sharded mode)
+  const unsigned m = __ballot_sync(0xffffffffu, Z > 0.0 && incl > t && s1 > s0);
+  int64_t ts = -1;
+  double c = 0.0;
+  if (m) {
+    const int f = __ffs(m) - 1;
+    if (lane == f) {
+      double O = excl;
+      int64_t lastpos = -1;
+      for (int64_t s2 = s0; s2 < s1; ++s2) {
+        const double z = at(s2);
+        if (z > 0.0) lastpos = s2;
+        if (O + z > t) { ts = s2; c = t - O; break; }
+        O += z;
+      }
+      if (ts < 0) { ts = lastpos; c = INFINITY; }
+    }
+    ts = __shfl_sync(0xffffffffu, ts, f);
+    c = __shfl_sync(0xffffffffu, c, f);
+  }
+  *tstar = ts;
+  *tc = c;
+  return Z;
 }
 
 // Kernel B2 (resample_kernel): CTA (request b, block of kSegTilesPerCta 2048-entry tiles).
@@ -814,42 +909,37 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   __shared__ int64_t s_tstar;
   __shared__ double s_tc, s_Z;
   __shared__ int s_kind, s_deg;
-  if (P.shard) {  // vocabulary-sharded: this rank's mass, in tile order; shard_sample_kernel goes on
-    if (tid == 0) {
-      P.counters[b] = 0;
-      const double* ss = P.segsum + (int64_t)b * P.nseg;
-      double Z = 0.0;
-      for (int64_t t = 0; t < P.nseg; ++t) Z += __ldcg(ss + t);
-      P.zsend[b] = Z;
-    }
-    return;
-  }
-  if (tid == 0) {
-    P.counters[b] = 0;  // ready for the next call
-    const double* ss = P.segsum + (int64_t)b * P.nseg;
-    double Z = 0.0;
-    for (int64_t t = 0; t < P.nseg; ++t) Z += __ldcg(ss + t);
-    int kind = kind0, dg = 0;
+  __shared__ double s_seg[kMaxSeg];
+  const double* ss = P.segsum + (int64_t)b * P.nseg;
+  const bool in_smem = P.nseg <= kMaxSeg;
+  if (in_smem)
+    for (int64_t t = tid; t < P.nseg; t += kThreads) s_seg[t] = __ldcg(ss + t);
+  __syncthreads();
+  if (warp == 0) {
     int64_t tstar = -1;
     double tc = 0.0;
-    if (!(Z > 0.0) && (kind == kWResidual || kind == kWPoint)) {
-      kind = kWProb;  // all mass cancelled: resample from o (reading #11)
-      dg = 1;
-    } else if (Z > 0.0) {
-      const double t = d.u * Z;
-      double O = 0.0;
-      for (int64_t s2 = 0; s2 < P.nseg; ++s2) {
-        const double z = __ldcg(ss + s2);
-        if (O + z > t) { tstar = s2; tc = t - O; break; }
-        O += z;
+    const double Z = in_smem ? warp_tile_crossing<false>(s_seg, P.nseg, d.u, &tstar, &tc)
+                             : warp_tile_crossing<true>(ss, P.nseg, d.u, &tstar, &tc);
+    if (lane == 0) {
+      P.counters[b] = 0;  // ready for the next call
+      if (P.shard) {      // vocabulary-sharded: this rank's mass; shard_sample_kernel goes on
+        P.zsend[b] = Z;
+      } else {
+        int kind = kind0, dg = 0;
+        if (!(Z > 0.0) && (kind == kWResidual || kind == kWPoint)) {
+          kind = kWProb;  // all mass cancelled: resample from o (reading #11)
+          dg = 1;
+          tstar = -1;
+        }
+        s_Z = Z;
+        s_kind = kind;
+        s_deg = dg;
+        s_tstar = tstar;
+        s_tc = tc;
       }
     }
-    s_Z = Z;
-    s_kind = kind;
-    s_deg = dg;
-    s_tstar = tstar;
-    s_tc = tc;
   }
+  if (P.shard) return;
   __syncthreads();
   const int kind = s_kind, deg = s_deg;
   double Z = s_Z;

@@ -1178,6 +1178,7 @@ struct cosine_ctx_s {
   std::string err;
   int32_t last_launches = 0;
   int32_t last_cluster = 0, last_ncl = 0;
+  int32_t* lz = nullptr;  // lazy verification: per-request state
   // vocabulary-sharded mode (nranks > 1)
   ncclComm_t comm = nullptr;
   uint32_t* rec_send = nullptr;
@@ -1500,6 +1501,86 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   return COSINE_OK;
 }
 
+using LazyFn = void (*)(SplitParams);
+template <typename TT, typename TQ>
+LazyFn pick_lazy2(bool logits) {
+  return logits ? lazy_decide_kernel<TT, TQ, true> : lazy_decide_kernel<TT, TQ, false>;
+}
+LazyFn pick_lazy(cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+  if (tt == COSINE_BF16 && tq == COSINE_BF16) return pick_lazy2<__nv_bfloat16, __nv_bfloat16>(logits);
+  if (tt == COSINE_BF16 && tq == COSINE_F32) return pick_lazy2<__nv_bfloat16, float>(logits);
+  if (tt == COSINE_F32 && tq == COSINE_BF16) return pick_lazy2<float, __nv_bfloat16>(logits);
+  return pick_lazy2<float, float>(logits);
+}
+
+// Lazy verification (NEXT-1): rounds r = 0..k of (stats of position r of the requests still
+// verifying -> their decisions), then the final draws.  2 (k + 1) + 1 launches on `stream`.
+cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, cosine_dtype_t tt,
+                            cosine_dtype_t tq, bool logits) {
+  SplitFn fn[3];
+  pick_split(tt, tq, logits, S.N, fn);
+  const LazyFn fd = pick_lazy(tt, tq, logits);
+  int C = 1;
+  if (ctx->cfg.cluster_size > 0) {
+    C = ctx->cfg.cluster_size;
+  } else {
+    while (C < kMaxC && S.ngroups > (int64_t)C * kThreads * 8) C *= 2;
+    while (C < kMaxC && (int64_t)S.B * C < 148 * 8 && S.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  }
+  S.C = C;
+  S.cg = (S.ngroups + C - 1) / C;
+  S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
+  S.spr = (int)((S.nseg + kSegTilesPerCta - 1) / kSegTilesPerCta);
+  S.parts = ctx->parts;
+  S.pdec = ctx->pdec;
+  S.segsum = ctx->segsum;
+  S.counters = ctx->counters;
+  S.b_off = 0;
+  S.nb = S.B;
+  S.lz = ctx->lz;
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaError_t e = cudaSuccess;
+  int launches = 0;
+  for (int r = 0; r <= S.k && e == cudaSuccess; ++r) {
+    S.lazy = r + 1;
+    lc.gridDim = dim3((unsigned)((int64_t)S.B * C), 1, 1);
+    lc.attrs = nullptr;  // stream order: the round reads the previous round's lz
+    lc.numAttrs = 0;
+    e = cudaLaunchKernelEx(&lc, fn[0], S);
+    if (e == cudaSuccess) {
+      lc.gridDim = dim3((unsigned)((S.B + kWarps - 1) / kWarps), 1, 1);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, fd, S);
+    }
+    launches += 2;
+  }
+  S.lazy = 0;
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, fn[2], S);
+    launches += 1;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("lazy verify kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = launches;
+  ctx->last_cluster = C;
+  return COSINE_OK;
+}
+
 void fill_common(Params& P, const cosine_ctx_t ctx, int B, int k, int N, float T) {
   memset(&P, 0, sizeof(P));
   P.B = B;
@@ -1584,6 +1665,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   // counters: [B] kernel-B CTAs per request | [B] decided units per request | [B][k+1] chunks per unit
   const size_t ncnt = 2 * nb + nb * (size_t)(cfg->max_draft_len + 1);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, ncnt * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->lz, nb * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, ncnt * sizeof(int32_t));
   ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
@@ -1625,6 +1707,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     cudaFree(ctx->zall);
     cudaFree(ctx->ysend);
     cudaFree(ctx->yall);
+    cudaFree(ctx->lz);
     cudaGetLastError();
     cudaFree(ctx->recs);
     cudaFree(ctx->done);
@@ -1660,6 +1743,7 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->cpq);
   cudaFree(ctx->segsum);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  cudaFree(ctx->lz);
   cudaFree(ctx->rec_send);
   cudaFree(ctx->rec_all);
   cudaFree(ctx->zsend);
@@ -1835,6 +1919,45 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   }
   return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
                 ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+}
+
+cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                         int32_t N, const void* target_logits, int64_t ld_t,
+                                         float temperature, const void* draft, int64_t ld_q,
+                                         const int32_t* draft_tokens, const int32_t* draft_len,
+                                         const uint64_t* request_ids, uint32_t step,
+                                         cosine_weight_mode_t weight_mode, int32_t* accept_len,
+                                         int32_t* out_tokens, int32_t* status,
+                                         const cosine_debug_t* debug) {
+  cosine_status_t s = check_common(ctx, B, k, N);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_verify_batch_lazy runs on unsharded contexts (nranks == 1)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, target_logits, ld_t, ctx->cfg.target_dtype, "target_logits")) != COSINE_OK) return s;
+  if ((s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
+  if (!draft_tokens || !request_ids || !accept_len || !out_tokens || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature >= 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "temperature must be finite and >= 0");
+  if ((int)weight_mode < 0 || (int)weight_mode > 3)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad weight mode");
+  if (temperature == 0.f && ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "greedy (T = 0) needs PROBS drafts");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P;
+  fill_common(P, ctx, B, k, N, temperature);
+  SplitParams S;
+  memset(&S, 0, sizeof(S));
+  S.B = B; S.k = k; S.N = N;
+  S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+  S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+  S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+  S.rids = request_ids; S.seed = P.seed; S.step = step;
+  S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status;
+  if (debug) S.dbg = *debug;
+  return launch_lazy(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                     ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
 }
 
 cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
