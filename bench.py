@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lazy", action="store_true",
+                    help="early-exit verification (cosine_verify_batch_lazy, SURVEY 8(f) NEXT-1)")
     ap.add_argument("--seed", type=int, default=1234)
     return ap.parse_args()
 
@@ -215,7 +217,7 @@ def run_ours(args):
 
     def step():
         ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"],
-                   temperature=1.0)
+                   temperature=1.0, lazy=args.lazy)
         return cv.cosine_last_launch_count(ver.ctx)
 
     for _ in range(max(args.warmup, 3)):
@@ -257,6 +259,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     stats_ms, stats_n = cv.cosine_profile_read(ver.ctx)
     cv.cosine_profile_enable(ver.ctx, False)
+    if args.lazy:  # no single dominant launch: the whole call against its realised bytes
+        # rows read per request: target 0..L, drafters at positions 0..min(L, k-1), and the
+        # final draw's rows (1 + N at a rejection, the bonus row otherwise)
+        Ls = ver.accept_len[:B].long().clamp_min(0)
+        rows = (Ls + 1) + torch.clamp(Ls + 1, max=k) * N + torch.where(Ls < k, 1 + N, 1)
+        realised = int(rows.sum()) * V * esz
+        stats_ms, stats_n = statistics.mean(kern_ms) * max(stats_n, 1), max(stats_n, 1)
     elapsed_ms = sharding.max_over_ranks(elapsed_ms, device=dev)  # the slowest rank's device time
     acc = ver.accept_len[:B].float().mean().item()
     status_nonzero = int((ver.status[:B] & 0xff).ne(0).sum().item())
@@ -264,6 +273,8 @@ def run_ours(args):
     tokens_per_step = B * k * world
     value = tokens_per_step * args.steps / (elapsed_ms / 1e3)
     alg_bytes = synth.algorithmic_bytes(B, k, N, V, esz, esz)
+    if args.lazy:
+        alg_bytes = realised
     step_avg_s = statistics.mean(kern_ms) / 1e3
     kern_avg_s = (stats_ms / max(stats_n, 1)) / 1e3  # stats_kernel: reads every input byte once
     achieved = alg_bytes / kern_avg_s / 1e9
@@ -314,7 +325,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if dt == torch.bfloat16 else "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "batch_per_gpu": B, "global_batch": B * world,
+            "config": {"workload": WORKLOADS[args.config] + (" — LAZY early-exit verification (NEXT-1): rows after "
+                                                              "the first rejection are not read; bytes = realised"
+                                                              if args.lazy else ""),
+                       "batch_per_gpu": B, "global_batch": B * world,
                        "k": k, "drafters": N, "vocab": V, "parallelism": f"batch-sharded x{world}",
                        "l2": f"inputs {alg_bytes / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
                        "mean_accept_len": acc, "request_errors": status_nonzero},
@@ -471,6 +485,13 @@ def run_vocab(args, c, dev, world, rank, local):
     torch.cuda.synchronize()
     stats_ms, stats_n = cv.cosine_profile_read(ver.ctx)
     cv.cosine_profile_enable(ver.ctx, False)
+    if args.lazy:  # no single dominant launch: the whole call against its realised bytes
+        # rows read per request: target 0..L, drafters at positions 0..min(L, k-1), and the
+        # final draw's rows (1 + N at a rejection, the bonus row otherwise)
+        Ls = ver.accept_len[:B].long().clamp_min(0)
+        rows = (Ls + 1) + torch.clamp(Ls + 1, max=k) * N + torch.where(Ls < k, 1 + N, 1)
+        realised = int(rows.sum()) * V * esz
+        stats_ms, stats_n = statistics.mean(kern_ms) * max(stats_n, 1), max(stats_n, 1)
     kern_s = max(sharding.max_over_ranks(stats_ms / max(stats_n, 1), device=dev) / 1e3, 1e-9)
     acc = ver.accept_len[:B].float().mean().item()
     errs = int((ver.status[:B] & 0xff).ne(0).sum().item())

@@ -181,6 +181,28 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
                                     const cosine_debug_t* debug);
 
 /*
+ * cosine_verify_batch_lazy — the same verification with early exit: rows
+ * are streamed position by position, i = 0, 1, ..., and a request stops reading at its first
+ * rejection (the rows after it are discarded anyway), at an error, or at its bonus row.
+ * Rounds r = 0..k each launch the statistics of position r of the requests still verifying and
+ * their decisions; then the final draws.  2 (k + 1) + 1 kernel launches; rows after L_b are
+ * never read, so the realised bytes are sum_b (L_b + 1) rows (+ the resample pass).
+ * Arguments and outputs as cosine_verify_batch (ARGMAX selection; unsharded contexts only).
+ * Outputs are identical to cosine_verify_batch (counter-based Philox, reading #8) for every
+ * request whose rows 0..L_b are valid; a data error in a row after L_b is NOT detected (that
+ * request gets its normal result instead of an error status).  debug: per-position arrays are
+ * written for positions <= L_b only.
+ */
+cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                         int32_t N, const void* target_logits, int64_t ld_t,
+                                         float temperature, const void* draft, int64_t ld_q,
+                                         const int32_t* draft_tokens, const int32_t* draft_len,
+                                         const uint64_t* request_ids, uint32_t step,
+                                         cosine_weight_mode_t weight_mode, int32_t* accept_len,
+                                         int32_t* out_tokens, int32_t* status,
+                                         const cosine_debug_t* debug);
+
+/*
  * cosine_sample_residual — the final-token sample of one row group per request,
  * for callers that verify elsewhere.
  *   target_rows [B][ld_t] logits of the row at L_b;  temperature (0 = argmax)

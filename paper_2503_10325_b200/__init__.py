@@ -14,14 +14,15 @@ from ._lib import (  # noqa: F401
     BF16, F32, DRAFT_LOGITS, DRAFT_PROBS, INFO_DEGENERATE, INFO_NEAR_TIE, SEL_ARGMAX, SEL_SAMPLE,
     W_CONF, W_POINT, W_UNIFORM, W_WINNER, Context, CosineError, cosine_fuse_drafts,
     cosine_last_launch_count, cosine_profile_enable, cosine_profile_read, cosine_sample_residual,
-    cosine_nccl_unique_id, cosine_verify_batch, cosine_verify_destroy, cosine_verify_init,
+    cosine_nccl_unique_id, cosine_verify_batch, cosine_verify_batch_lazy, cosine_verify_destroy,
+    cosine_verify_init,
     cosine_verify_tree,
 )
 
 __all__ = [
     "Verifier", "cosine_verify_init", "cosine_verify_destroy", "cosine_fuse_drafts",
     "cosine_verify_batch", "cosine_sample_residual", "cosine_verify_tree", "cosine_last_launch_count",
-    "cosine_nccl_unique_id",
+    "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
     "CosineError",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE", "DRAFT_PROBS",
     "DRAFT_LOGITS",
@@ -57,14 +58,24 @@ class Verifier:
                 residual_mass=torch.empty(max_batch, **f), tie_margin=torch.empty(max_batch, **f))
 
     def verify(self, target, draft, draft_tokens, request_ids, *, temperature=1.0, draft_len=None,
-               step=0, weight_mode=W_CONF, select_mode=SEL_ARGMAX, stream=None):
-        """Device-resident inputs -> (accept_len, out_tokens, status) views (device)."""
+               step=0, weight_mode=W_CONF, select_mode=SEL_ARGMAX, stream=None, lazy=False):
+        """Device-resident inputs -> (accept_len, out_tokens, status) views (device).
+        lazy=True: early-exit verification (cosine_verify_batch_lazy, ARGMAX only)."""
         B = target.shape[0]
         dbg = None if self.debug is None else {n: t[:B] for n, t in self.debug.items()}
-        cosine_verify_batch(self.ctx, target, draft, draft_tokens, request_ids,
-                            self.accept_len[:B], self.out_tokens[:B], self.status[:B],
-                            temperature=temperature, draft_len=draft_len, step=step,
-                            weight_mode=weight_mode, select_mode=select_mode, debug=dbg, stream=stream)
+        if lazy:
+            if select_mode != SEL_ARGMAX:
+                raise ValueError("lazy verification takes ARGMAX selection")
+            cosine_verify_batch_lazy(self.ctx, target, draft, draft_tokens, request_ids,
+                                     self.accept_len[:B], self.out_tokens[:B], self.status[:B],
+                                     temperature=temperature, draft_len=draft_len, step=step,
+                                     weight_mode=weight_mode, debug=dbg, stream=stream)
+        else:
+            cosine_verify_batch(self.ctx, target, draft, draft_tokens, request_ids,
+                                self.accept_len[:B], self.out_tokens[:B], self.status[:B],
+                                temperature=temperature, draft_len=draft_len, step=step,
+                                weight_mode=weight_mode, select_mode=select_mode, debug=dbg,
+                                stream=stream)
         return self.accept_len[:B], self.out_tokens[:B], self.status[:B]
 
     def verify_host(self, host_inputs: dict, dev_buffers: dict, *, temperature=1.0, step=0,

@@ -65,6 +65,10 @@ _lib.cosine_verify_batch.argtypes = [_P, _P, _i32, _i32, _i32, _P, _i64, _f32, _
                                      _P, _u32, ctypes.c_int, ctypes.c_int, _P, _P, _P,
                                      ctypes.POINTER(cosine_debug_t)]
 _lib.cosine_verify_batch.restype = ctypes.c_int
+_lib.cosine_verify_batch_lazy.argtypes = [_P, _P, _i32, _i32, _i32, _P, _i64, _f32, _P, _i64, _P, _P,
+                                          _P, _u32, ctypes.c_int, _P, _P, _P,
+                                          ctypes.POINTER(cosine_debug_t)]
+_lib.cosine_verify_batch_lazy.restype = ctypes.c_int
 _lib.cosine_sample_residual.argtypes = [_P, _P, _i32, _P, _i64, _f32, _P, _P, _P, _i64, _P, _P,
                                         _i32, _P, _P, _u32, _P, _P]
 _lib.cosine_sample_residual.restype = ctypes.c_int
@@ -82,7 +86,7 @@ _lib.cosine_profile_read.restype = ctypes.c_int
 EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_error",
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
-                    "cosine_verify_tree", "cosine_nccl_unique_id")
+                    "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -203,6 +207,23 @@ def cosine_verify_batch(ctx, target_logits, draft, draft_tokens, request_ids, ac
                                   _ptr(draft_tokens), _ptr(draft_len), _ptr(request_ids), step,
                                   weight_mode, select_mode, _ptr(accept_len), _ptr(out_tokens),
                                   _ptr(status), ctypes.byref(dbg) if dbg is not None else None)
+    _check(rc, ctx)
+
+
+def cosine_verify_batch_lazy(ctx, target_logits, draft, draft_tokens, request_ids, accept_len, out_tokens,
+                             status, *, temperature=1.0, draft_len=None, step=0, weight_mode=W_CONF,
+                             debug=None, stream=None):
+    """Early-exit verification (NEXT-1): same arguments / outputs as cosine_verify_batch."""
+    B, kp1, ld_t = target_logits.shape
+    N, ld_q = draft.shape[2], draft.shape[3]
+    dbg = None
+    if debug is not None:
+        dbg = cosine_debug_t(**{f: _ptr(debug.get(f)) for f, _ in cosine_debug_t._fields_})
+    rc = _lib.cosine_verify_batch_lazy(ctx, _stream(stream, target_logits.device), B, kp1 - 1, N,
+                                       _ptr(target_logits), ld_t, temperature, _ptr(draft), ld_q,
+                                       _ptr(draft_tokens), _ptr(draft_len), _ptr(request_ids), step,
+                                       weight_mode, _ptr(accept_len), _ptr(out_tokens), _ptr(status),
+                                       ctypes.byref(dbg) if dbg is not None else None)
     _check(rc, ctx)
 
 

@@ -12,7 +12,7 @@ PROB_RTOL = 1e-5  # north_star: probabilities within 1e-5 relative (fp32)
 
 
 def gpu_verify(inp, *, T=1.0, seed=7, step=0, wm=0, sm=0, draft_kind="probs", cluster_size=0,
-               device=0, subset=None):
+               device=0, subset=None, lazy=False):
     import paper_2503_10325_b200 as cv
     tgt, drf = inp["target"], inp["draft"]
     B, kp1, _ = tgt.shape
@@ -23,7 +23,7 @@ def gpu_verify(inp, *, T=1.0, seed=7, step=0, wm=0, sm=0, draft_kind="probs", cl
                       draft_kind=cv.DRAFT_LOGITS if draft_kind == "logits" else cv.DRAFT_PROBS)
     d = {n: (t.to(dev) if torch.is_tensor(t) else t) for n, t in inp.items()}
     a, o, s = ver.verify(d["target"], d["draft"], d["draft_tokens"], d["request_ids"], temperature=T,
-                         draft_len=d["draft_len"], step=step, weight_mode=wm, select_mode=sm)
+                         draft_len=d["draft_len"], step=step, weight_mode=wm, select_mode=sm, lazy=lazy)
     torch.cuda.synchronize()
     out = dict(accept_len=a.cpu().numpy().copy(), out_tokens=o.cpu().numpy().copy(),
                status=s.cpu().numpy().copy(), launches=cv.cosine_last_launch_count(ver.ctx))
