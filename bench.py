@@ -263,7 +263,9 @@ def run_ours(args):
         # rows read per request: target 0..L, drafters at positions 0..min(L, k-1), and the
         # final draw's rows (1 + N at a rejection, the bonus row otherwise)
         Ls = ver.accept_len[:B].long().clamp_min(0)
-        rows = (Ls + 1) + torch.clamp(Ls + 1, max=k) * N + torch.where(Ls < k, 1 + N, 1)
+        # (2 positions per round: the round holding L also streamed position L + 1 if it exists)
+        span_end = torch.clamp((Ls // 2) * 2 + 2, max=k + 1)  # positions 0 .. span_end - 1 read
+        rows = span_end + torch.clamp(span_end, max=k) * N + torch.where(Ls < k, 1 + N, 1)
         realised = int(rows.sum()) * V * esz
         stats_ms, stats_n = statistics.mean(kern_ms) * max(stats_n, 1), max(stats_n, 1)
     elapsed_ms = sharding.max_over_ranks(elapsed_ms, device=dev)  # the slowest rank's device time
@@ -489,7 +491,9 @@ def run_vocab(args, c, dev, world, rank, local):
         # rows read per request: target 0..L, drafters at positions 0..min(L, k-1), and the
         # final draw's rows (1 + N at a rejection, the bonus row otherwise)
         Ls = ver.accept_len[:B].long().clamp_min(0)
-        rows = (Ls + 1) + torch.clamp(Ls + 1, max=k) * N + torch.where(Ls < k, 1 + N, 1)
+        # (2 positions per round: the round holding L also streamed position L + 1 if it exists)
+        span_end = torch.clamp((Ls // 2) * 2 + 2, max=k + 1)  # positions 0 .. span_end - 1 read
+        rows = span_end + torch.clamp(span_end, max=k) * N + torch.where(Ls < k, 1 + N, 1)
         realised = int(rows.sum()) * V * esz
         stats_ms, stats_n = statistics.mean(kern_ms) * max(stats_n, 1), max(stats_n, 1)
     kern_s = max(sharding.max_over_ranks(stats_ms / max(stats_n, 1), device=dev) / 1e3, 1e-9)

@@ -184,9 +184,10 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
  * cosine_verify_batch_lazy — the same verification with early exit: rows
  * are streamed position by position, i = 0, 1, ..., and a request stops reading at its first
  * rejection (the rows after it are discarded anyway), at an error, or at its bonus row.
- * Rounds r = 0..k each launch the statistics of position r of the requests still verifying and
- * their decisions; then the final draws.  2 (k + 1) + 1 kernel launches; rows after L_b are
- * never read, so the realised bytes are sum_b (L_b + 1) rows (+ the resample pass).
+ * Each round streams the next 2 positions of the requests still verifying and decides them in
+ * order; then the final draws: 2 ceil((k + 1) / 2) + 1 kernel launches.  Rows after the round
+ * holding L_b are never read (at most one speculative position per request), so the realised
+ * bytes are ~ sum_b (L_b + 2) rows (+ the resample pass).
  * Arguments and outputs as cosine_verify_batch (ARGMAX selection; unsharded contexts only).
  * Outputs are identical to cosine_verify_batch (counter-based Philox, reading #8) for every
  * request whose rows 0..L_b are valid; a data error in a row after L_b is NOT detected (that

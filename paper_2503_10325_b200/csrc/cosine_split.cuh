@@ -62,6 +62,7 @@ struct SplitParams {
   // streams position r of the requests still verifying (0 = off); lz[b] = 0 while request b
   // verifies, -1 once it stopped
   int lazy;
+  int lazy_span;  // positions per lazy round
   int32_t* lz;
   double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
   int64_t nseg;
@@ -176,10 +177,10 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
     gu = unit;
   } else {
     int b, i;
-    if (P.lazy) {  // lazy round r (NEXT-1): position r of the requests still verifying
-      b = (int)unit;
-      i = P.lazy - 1;
-      if (i > 0 && P.lz[b] != 0) return;
+    if (P.lazy) {  // lazy round (NEXT-1): positions r0 .. r0+span-1 of the requests still verifying
+      b = (int)(unit / P.lazy_span);
+      i = P.lazy - 1 + (int)(unit % P.lazy_span);
+      if (P.lazy > 1 && P.lz[b] != 0) return;
     } else {
       b = P.b_off + (int)(unit / (P.k + 1));
       i = (int)(unit % (P.k + 1));
@@ -613,22 +614,29 @@ __global__ void __launch_bounds__(kThreads) lazy_decide_kernel(const SplitParams
   asm volatile("griddepcontrol.wait;" ::: "memory");  // this round's partial records (PDL)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (b >= P.B) return;
-  const int r = P.lazy - 1;
+  const int r0 = P.lazy - 1;
   const int g = P.draft_len ? P.draft_len[b] : P.k;
-  if (g < 1 || g > P.k || r > g) return;
-  if (r > 0 && P.lz[b] != 0) return;
+  if (g < 1 || g > P.k || r0 > g) return;
+  if (r0 > 0 && P.lz[b] != 0) return;
   PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
-  warp_decide<TT, TQ, kLogits>(P, b, r, g, s_gx[warp], s_tok[warp], &pds[r], true);
-  __syncwarp();
-  if (lane != 0) return;
-  const PosDec& pd = pds[r];
-  const bool stop = pd.status != 0 || r == g || !pd.accept;
-  P.lz[b] = stop ? -1 : 0;
-  if (stop) {
-    PosDec ok;
-    init_posdec(ok);
-    for (int j = r + 1; j <= g; ++j) pds[j] = ok;
+  const int r1 = min(g, r0 + P.lazy_span - 1);
+  bool stop = false;
+  for (int r = r0; r <= r1 && !stop; ++r) {  // the round's positions in order
+    warp_decide<TT, TQ, kLogits>(P, b, r, g, s_gx[warp], s_tok[warp], &pds[r], true);
+    __syncwarp();
+    int st = 0;
+    if (lane == 0) {
+      const PosDec& pd = pds[r];
+      st = (pd.status != 0 || r == g || !pd.accept) ? 1 : 0;
+      if (st) {
+        PosDec ok;
+        init_posdec(ok);
+        for (int j = r + 1; j <= g; ++j) pds[j] = ok;
+      }
+    }
+    stop = __shfl_sync(0xffffffffu, st, 0) != 0;
   }
+  if (lane == 0) P.lz[b] = stop ? -1 : 0;
 }
 
 // The request-level view of the position decisions (first error, first rejection L, margins).
