@@ -371,7 +371,8 @@ def run_tree(args, c, dev, world, rank, local):
 
     def step():
         cv.cosine_verify_tree(ctx, t["parent"], t["node_token"], t["internal_row"], t["target"], t["draft"],
-                              t["node_draft_tokens"], t["request_ids"], al, an, ot, st, temperature=1.0)
+                              t["node_draft_tokens"], t["request_ids"], al, an, ot, st, temperature=1.0,
+                              lazy=args.lazy)
         return cv.cosine_last_launch_count(ctx)
 
     for _ in range(max(args.warmup, 3)):
@@ -395,6 +396,24 @@ def run_tree(args, c, dev, world, rank, local):
     ms = sharding.max_over_ranks(e0.elapsed_time(e1), device=dev) / args.steps
     tokens = B * t["J"] * world
     alg = synth.tree_algorithmic_bytes(B, nn, I, N, V, esz, esz)
+    accounting = "all nodes read once (whole call)"
+    if args.lazy:  # realised path bytes: the visited nodes' rows + one pass per rejection / bonus
+        par = t["parent"][0].tolist()
+        irow = t["internal_row"][0].tolist()
+        kids = {j: [c for c in range(1, nn) if par[c] == j] for j in range(nn)}
+        rows = 0
+        for b in range(B):
+            path = [0] + [int(x) for x in an[b].tolist() if x >= 0]
+            for d, j in enumerate(path):
+                node_rows = 1 + (N if irow[j] >= 0 else 0)
+                passes = 1  # the node's statistics
+                if d + 1 < len(path):
+                    passes += kids[j].index(path[d + 1])  # children rejected before the accepted one
+                else:
+                    passes += len(kids[j]) if kids[j] else 1  # all children rejected, or the bonus pass
+                rows += passes * node_rows
+        alg = rows * V * esz
+        accounting = "LAZY (NEXT-1): realised path bytes (visited nodes' statistics + rejection / bonus passes)"
     peak, peak_src = peaks()
     acc = al.float().mean().item()
     if rank == 0:
@@ -402,13 +421,15 @@ def run_tree(args, c, dev, world, rank, local):
             "metric": METRIC, "value": tokens / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOADS["c4"], "batch_per_gpu": B, "global_batch": B * world,
+            "config": {"workload": WORKLOADS["c4"] + (" — LAZY walk (NEXT-1): only the visited nodes' rows are read"
+                                                      if args.lazy else ""),
+                       "batch_per_gpu": B, "global_batch": B * world,
                        "tree_nodes": t["J"], "internal_nodes": I, "drafters": N, "vocab": V,
                        "parallelism": f"batch-sharded x{world}", "mean_accept_len": acc,
                        "l2": f"inputs {alg / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg, "accounting": "all nodes read once (whole call)",
+                         "algorithmic_bytes_per_launch": alg, "accounting": accounting,
                          "frac_of_8tbs": alg / (ms / 1e3) / 1e9 / 8000.0},
             "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": sampler.result(),
         }

@@ -249,6 +249,25 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
                                    int32_t* accept_len, int32_t* accepted_nodes,
                                    int32_t* out_tokens, int32_t* status);
 
+/*
+ * cosine_verify_tree_lazy — the tree walk with early exit: instead of
+ * reading every node's rows up front, the walk kernel computes the statistics of each node it
+ * visits (one pass over that node's rows, then the node's Eq. 4 fusion and its children's
+ * o / q) — path-only bytes, one kernel launch.  Arguments and outputs as cosine_verify_tree.
+ * Outputs are identical to cosine_verify_tree for every request whose visited nodes are valid;
+ * a data error in a node the walk does not visit is not detected (reading #23);
+ * structure errors (parent order, siblings, internal rows) are checked for the whole tree.
+ */
+cosine_status_t cosine_verify_tree_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                   int32_t I, int32_t N, const int32_t* parent,
+                                   const int32_t* node_token, const int32_t* internal_row,
+                                   const void* target, int64_t ld_t, float temperature,
+                                   const void* draft, int64_t ld_q,
+                                   const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, cosine_weight_mode_t weight_mode,
+                                   int32_t* accept_len, int32_t* accepted_nodes,
+                                   int32_t* out_tokens, int32_t* status);
+
 /* Number of kernels the last successful call on ctx enqueued (for launch accounting). */
 int32_t cosine_last_launch_count(cosine_ctx_t ctx);
 

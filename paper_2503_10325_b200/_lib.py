@@ -76,6 +76,8 @@ _lib.cosine_sample_residual.restype = ctypes.c_int
 _lib.cosine_verify_tree.argtypes = [_P, _P, _i32, _i32, _i32, _i32, _P, _P, _P, _P, _i64, _f32, _P, _i64,
                                     _P, _P, _u32, ctypes.c_int, _P, _P, _P, _P]
 _lib.cosine_verify_tree.restype = ctypes.c_int
+_lib.cosine_verify_tree_lazy.argtypes = _lib.cosine_verify_tree.argtypes
+_lib.cosine_verify_tree_lazy.restype = ctypes.c_int
 _lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
 _lib.cosine_nccl_unique_id.restype = ctypes.c_int
 _lib.cosine_profile_enable.argtypes = [_P, _i32]
@@ -86,7 +88,8 @@ _lib.cosine_profile_read.restype = ctypes.c_int
 EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_error",
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
-                    "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy")
+                    "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
+                    "cosine_verify_tree_lazy")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -229,11 +232,13 @@ def cosine_verify_batch_lazy(ctx, target_logits, draft, draft_tokens, request_id
 
 def cosine_verify_tree(ctx, parent, node_token, internal_row, target, draft, node_draft_tokens,
                        request_ids, accept_len, accepted_nodes, out_tokens, status, *, temperature=1.0,
-                       step=0, weight_mode=W_CONF, stream=None):
-    """parent / node_token / internal_row [B][J+1], target [B][J+1][ld_t], draft [B][I][N][ld_q]."""
+                       step=0, weight_mode=W_CONF, stream=None, lazy=False):
+    """parent / node_token / internal_row [B][J+1], target [B][J+1][ld_t], draft [B][I][N][ld_q].
+    lazy=True: cosine_verify_tree_lazy (path-only reads, NEXT-1)."""
     B, nn, ld_t = target.shape
     I, N, ld_q = draft.shape[1], draft.shape[2], draft.shape[3]
-    rc = _lib.cosine_verify_tree(ctx, _stream(stream, target.device), B, nn - 1, I, N, _ptr(parent),
+    fn = _lib.cosine_verify_tree_lazy if lazy else _lib.cosine_verify_tree
+    rc = fn(ctx, _stream(stream, target.device), B, nn - 1, I, N, _ptr(parent),
                                  _ptr(node_token), _ptr(internal_row), _ptr(target), ld_t, temperature,
                                  _ptr(draft), ld_q, _ptr(node_draft_tokens), _ptr(request_ids), step,
                                  weight_mode, _ptr(accept_len), _ptr(accepted_nodes), _ptr(out_tokens),

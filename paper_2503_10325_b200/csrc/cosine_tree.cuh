@@ -32,7 +32,129 @@ struct TreeParams {
   NodeDec* ndec;               // [B][nn]
   ChildPQ* cpq;                // [B][nn]
   int32_t* accepted_nodes;     // [B][nn]
+  int lazy;                    // NEXT-1: the walk computes the statistics of the nodes it visits
 };
+
+// ---------------- node decisions (one warp) ----------------
+// The statistics of node j's rows, combined over the whole vocabulary (valid in every lane).
+struct NodeStats {
+  float M;
+  double S;
+  double sig[kMaxN];
+  float dmax[kMaxN];
+  bool t_nf, t_empty, d_nf, d_empty;
+};
+
+// One warp decides node j of request b from its row statistics: Eq. 4 fusion at the node
+// (reading #2) and o_j(x_c), q_j(x_c) of every child c (lane-parallel).  Lane 0 writes
+// the node record *nd_out; the child values go to gcpq[c] (global) or scp[c] / scq[c] (shared).
+// s_*: per-warp shared scratch.  Shared by tree_decide_kernel and the lazy walk.
+template <typename TT, typename TQ, bool kLogits>
+__device__ __forceinline__ void node_decide_warp(const TreeParams& T, int b, int j, int ir, bool has_d,
+                                                 const TT* trow, const TQ* drow, const NodeStats& ns,
+                                                 float* s_gx, int32_t* s_tok, double* s_w, double* s_sig,
+                                                 float* s_dmax, int* s_zero, NodeDec* nd_out, ChildPQ* gcpq,
+                                                 double* scp, double* scq) {
+  const SplitParams& P = T.S;
+  const int lane = threadIdx.x & 31;
+  const int nn = P.nn, N = P.N;
+  const double k2 = (double)P.k2f;
+  if (lane == 0) *s_zero = 0;
+  if (has_d && lane < N * N) {  // d_m(X_n) for the confidences at this node
+    const int n = lane % N, m = lane / N;
+    const int32_t tk = T.node_draft_tokens[((int64_t)b * P.I + ir) * N + n];
+    float v = 0.f;
+    if (tk >= 0 && (int64_t)tk < P.V) v = load_one(drow + (int64_t)m * P.ld_q, tk);
+    s_gx[m * kMaxN + n] = v;
+    if (m == 0) s_tok[n] = tk;
+  }
+  __syncwarp();
+  NodeDec nd;
+  nd.M = ns.M;
+  nd.S = ns.S;
+  nd.gap = INFINITY;
+  for (int n = 0; n < kMaxN; ++n) { nd.a[n] = 0.f; nd.dm[n] = 0.f; }
+  int stc = 0;
+  bool ok_for_children = false;
+  if (lane == 0) {
+    bool tok_bad = false, zero = false;
+    if (has_d)
+      for (int n = 0; n < N; ++n)
+        if (s_tok[n] < 0 || (int64_t)s_tok[n] >= P.V) tok_bad = true;
+    if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
+    else if (ns.t_nf || ns.d_nf) stc = COSINE_REQ_NONFINITE_INPUT;
+    else if (ns.t_empty || ns.d_empty) stc = COSINE_REQ_EMPTY_ROW;
+    auto qval = [&](int m, double dv) {
+      return kLogits ? exp2(dv * k2 - (double)ns.dmax[m] * k2) / ns.sig[m] : dv / ns.sig[m];
+    };
+    double c[kMaxN], w[kMaxN];
+    if (!stc && has_d) {
+      for (int n = 0; n < N; ++n) {
+        c[n] = qval(n, (double)s_gx[n * kMaxN + n]);  // c_n = q_n(X_n) at this node
+        if (c[n] == 0.0) zero = true;
+      }
+      if (zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+    }
+    if (!stc && has_d) {  // Eq. 4 fusion weights at the node (reading #2)
+      int nsel = 0;
+      for (int n = 1; n < N; ++n)
+        if (c[n] > c[nsel]) nsel = n;
+      double second = -1.0;
+      for (int n = 0; n < N; ++n)
+        if (n != nsel && c[n] > second) second = c[n];
+      nd.gap = (N > 1) ? (float)((c[nsel] - second) / c[nsel]) : INFINITY;
+      if (P.weight_mode == COSINE_W_CONF) {
+        double sc = 0.0;
+        for (int n = 0; n < N; ++n) sc += c[n];
+        for (int n = 0; n < N; ++n) w[n] = c[n] / sc;
+      } else if (P.weight_mode == COSINE_W_UNIFORM) {
+        for (int n = 0; n < N; ++n) w[n] = 1.0 / (double)N;
+      } else {
+        for (int n = 0; n < N; ++n) w[n] = (n == nsel) ? 1.0 : 0.0;
+      }
+      for (int n = 0; n < N; ++n) {
+        nd.a[n] = (float)(w[n] / ns.sig[n]);
+        nd.dm[n] = ns.dmax[n];
+        s_w[n] = w[n];
+        s_sig[n] = ns.sig[n];
+        s_dmax[n] = ns.dmax[n];
+      }
+      ok_for_children = true;
+    }
+  }
+  ok_for_children = __shfl_sync(0xffffffffu, ok_for_children, 0);
+  __syncwarp();
+  // o_j(x_c), q_j(x_c) of every child c of j (lane-parallel over candidate node ids)
+  for (int c = j + 1 + lane; c < nn; c += 32) {
+    if (T.parent[(int64_t)b * nn + c] != j) continue;
+    const int32_t x = T.node_token[(int64_t)b * nn + c];
+    double pp = 0.0, qq = 0.0;
+    if (x >= 0 && (int64_t)x < P.V && ok_for_children) {
+      pp = exp2((double)load_one(trow, x) * k2 - (double)ns.M * k2) / ns.S;
+      for (int m = 0; m < N; ++m) {
+        const double dv = (double)load_one(drow + (int64_t)m * P.ld_q, x);
+        const double qm = kLogits ? exp2(dv * k2 - (double)s_dmax[m] * k2) / s_sig[m] : dv / s_sig[m];
+        qq += s_w[m] * qm;
+      }
+      if (qq == 0.0) atomicOr(s_zero, 1);  // a child the fused q cannot draw
+    }
+    if (gcpq) {
+      ChildPQ pq;
+      pq.p = pp;
+      pq.q = qq;
+      gcpq[c] = pq;
+    } else {
+      scp[c] = pp;
+      scq[c] = qq;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (!stc && *s_zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+    nd.status = stc;
+    *nd_out = nd;
+  }
+}
 
 // ---------------- kernel T1: one warp per node ----------------
 template <typename TT, typename TQ, bool kLogits>
@@ -54,29 +176,21 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
   const double k2 = (double)P.k2f;
   const TT* trow = (const TT*)P.target + unit * P.ld_t;
   const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (has_d ? ir : 0)) * N * P.ld_q;
-  if (lane == 0) s_zero[warp] = 0;
-  if (has_d && lane < N * N) {  // d_m(X_n) for the confidences at this node
-    const int n = lane % N, m = lane / N;
-    const int32_t tk = T.node_draft_tokens[((int64_t)b * P.I + ir) * N + n];
-    float v = 0.f;
-    if (tk >= 0 && (int64_t)tk < P.V) v = load_one(drow + (int64_t)m * P.ld_q, tk);
-    s_gx[warp][m * kMaxN + n] = v;
-    if (m == 0) s_tok[warp][n] = tk;
-  }
   // combine the partial records (chunk r in lane r)
   const PartRec* parts = P.parts + unit * C;
   const bool own = lane < C;
   const float tmax = own ? parts[lane].tmax : kNegBig;
   const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
-  const float M = warp_max(tmax);
+  NodeStats ns;
+  ns.M = warp_max(tmax);
   const double tsum = own ? parts[lane].tsum : 0.0;
-  const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
-  bool t_nf = !isfinite(S) || !isfinite(M), t_empty = false, d_nf = false, d_empty = false;
-  t_empty = !t_nf && !(S > 0.0);
-  double sig[kMaxN];
-  float dmax[kMaxN];
+  ns.S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)ns.M * k2) : 0.0);
+  ns.t_nf = !isfinite(ns.S) || !isfinite(ns.M);
+  ns.t_empty = !ns.t_nf && !(ns.S > 0.0);
+  ns.d_nf = false;
+  ns.d_empty = false;
   if (has_d) {
-    if (bad & 2) d_nf = true;
+    if (bad & 2) ns.d_nf = true;
     for (int n = 0; n < N; ++n) {
       double sv;
       float mx = kNegBig;
@@ -85,99 +199,19 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
         const float dmr = own ? parts[lane].dmax[n] : kNegBig;
         mx = warp_max(dmr);
         sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
-        if (!isfinite(mx)) d_nf = true;
+        if (!isfinite(mx)) ns.d_nf = true;
       } else {
         sv = warp_sum(ds);
       }
-      sig[n] = sv;
-      dmax[n] = mx;
-      if (!isfinite(sv)) d_nf = true;
-      else if (!(sv > 0.0)) d_empty = true;
+      ns.sig[n] = sv;
+      ns.dmax[n] = mx;
+      if (!isfinite(sv)) ns.d_nf = true;
+      else if (!(sv > 0.0)) ns.d_empty = true;
     }
   }
-  __syncwarp();
-  NodeDec nd;
-  nd.M = M;
-  nd.S = S;
-  nd.gap = INFINITY;
-  for (int n = 0; n < kMaxN; ++n) { nd.a[n] = 0.f; nd.dm[n] = 0.f; }
-  int stc = 0;
-  bool ok_for_children = false;
-  if (lane == 0) {
-    bool tok_bad = false, zero = false;
-    if (has_d)
-      for (int n = 0; n < N; ++n)
-        if (s_tok[warp][n] < 0 || (int64_t)s_tok[warp][n] >= P.V) tok_bad = true;
-    if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
-    else if (t_nf || d_nf) stc = COSINE_REQ_NONFINITE_INPUT;
-    else if (t_empty || d_empty) stc = COSINE_REQ_EMPTY_ROW;
-    auto qval = [&](int m, double dv) {
-      return kLogits ? exp2(dv * k2 - (double)dmax[m] * k2) / sig[m] : dv / sig[m];
-    };
-    double c[kMaxN], w[kMaxN];
-    if (!stc && has_d) {
-      for (int n = 0; n < N; ++n) {
-        c[n] = qval(n, (double)s_gx[warp][n * kMaxN + n]);  // c_n = q_n(X_n) at this node
-        if (c[n] == 0.0) zero = true;
-      }
-      if (zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
-    }
-    if (!stc && has_d) {  // Eq. 4 fusion weights at the node (reading #2)
-      int ns = 0;
-      for (int n = 1; n < N; ++n)
-        if (c[n] > c[ns]) ns = n;
-      double second = -1.0;
-      for (int n = 0; n < N; ++n)
-        if (n != ns && c[n] > second) second = c[n];
-      nd.gap = (N > 1) ? (float)((c[ns] - second) / c[ns]) : INFINITY;
-      if (P.weight_mode == COSINE_W_CONF) {
-        double sc = 0.0;
-        for (int n = 0; n < N; ++n) sc += c[n];
-        for (int n = 0; n < N; ++n) w[n] = c[n] / sc;
-      } else if (P.weight_mode == COSINE_W_UNIFORM) {
-        for (int n = 0; n < N; ++n) w[n] = 1.0 / (double)N;
-      } else {
-        for (int n = 0; n < N; ++n) w[n] = (n == ns) ? 1.0 : 0.0;
-      }
-      for (int n = 0; n < N; ++n) {
-        nd.a[n] = (float)(w[n] / sig[n]);
-        nd.dm[n] = dmax[n];
-        s_w[warp][n] = w[n];
-        s_sig[warp][n] = sig[n];
-        s_dmax[warp][n] = dmax[n];
-      }
-      ok_for_children = true;
-    }
-  }
-  ok_for_children = __shfl_sync(0xffffffffu, ok_for_children, 0);
-  __syncwarp();
-  // o_j(x_c), q_j(x_c) of every child c of j (lane-parallel over candidate node ids)
-  for (int c = j + 1 + lane; c < nn; c += 32) {
-    if (T.parent[(int64_t)b * nn + c] != j) continue;
-    const int32_t x = T.node_token[(int64_t)b * nn + c];
-    ChildPQ pq;
-    pq.p = 0.0;
-    pq.q = 0.0;
-    if (x >= 0 && (int64_t)x < P.V && ok_for_children) {
-      pq.p = exp2((double)load_one(trow, x) * k2 - (double)M * k2) / S;
-      double q = 0.0;
-      for (int m = 0; m < N; ++m) {
-        const double dv = (double)load_one(drow + (int64_t)m * P.ld_q, x);
-        const double qm = kLogits ? exp2(dv * k2 - (double)s_dmax[warp][m] * k2) / s_sig[warp][m]
-                                  : dv / s_sig[warp][m];
-        q += s_w[warp][m] * qm;
-      }
-      pq.q = q;
-      if (q == 0.0) atomicOr(&s_zero[warp], 1);  // a child the fused q cannot draw
-    }
-    T.cpq[(int64_t)b * nn + c] = pq;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    if (!stc && s_zero[warp]) stc = COSINE_REQ_ZERO_PROB_DRAFT;
-    nd.status = stc;
-    T.ndec[unit] = nd;
-  }
+  node_decide_warp<TT, TQ, kLogits>(T, b, j, ir, has_d, trow, drow, ns, s_gx[warp], s_tok[warp], s_w[warp],
+                                    s_sig[warp], s_dmax[warp], &s_zero[warp], &T.ndec[unit],
+                                    T.cpq + (int64_t)b * nn, nullptr, nullptr);
 }
 
 // ---------------- the walk ----------------
@@ -300,6 +334,164 @@ struct TreeRing {  // the shared-memory tile ring of one CTA
   }
 };
 
+// Lazy walk (NEXT-1): the statistics of node j's rows, computed by the walk CTA itself when it
+// arrives at j — one pass through the TMA ring (online max / sum-exp of the target row as in
+// stats_kernel, drafter sums or online softmax statistics), a fixed-order block reduction, then
+// warp 0 decides the node (node_decide_warp).  `it` (the ring position) advances by ntile.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__device__ __forceinline__ void tree_node_stats(
+    const TreeParams& T, int b, int j, int Nd, const TT* trow, const TQ* drow,
+    const TreeRing<TT, TQ, NMAX>& ring, uint64_t* s_full, uint64_t* s_empty, uint32_t& it, int64_t ntile,
+    bool producer, float (*s_rf)[1 + kMaxN], double (*s_rd)[1 + kMaxN], int* s_rbad, float* s_ngx,
+    int32_t* s_ntok, double* s_nw, double* s_nsig, float* s_ndmax, int* s_nzero, NodeDec* s_nd, double* s_cp,
+    double* s_cq, int ir) {
+  using Ring = TreeRing<TT, TQ, NMAX>;
+  constexpr int kTG = Ring::kTG;
+  const SplitParams& P = T.S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float k2 = P.k2f;
+  float tmx = kNegBig, tmk = kNegBig, ts = 0.f;
+  float dm[NMAX], dmk[NMAX], ds[NMAX];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) { dm[n] = kNegBig; dmk[n] = kNegBig; ds[n] = 0.f; }
+  bool dneg = false;
+  if (producer) {
+    if (lane == 0)
+      for (int64_t t = 0; t < ntile; ++t) ring.fill(it + (uint32_t)t, t, P, trow, drow, Nd);
+  } else {
+    for (int64_t t = 0; t < ntile; ++t) {
+      const uint32_t pos = it + (uint32_t)t;
+      const int stg = (int)(pos % kTreeStages);
+      mbar_wait_parity(&s_full[stg], (pos / kTreeStages) & 1u);
+      const unsigned char* sb = ring.base + stg * Ring::kStageB;
+      const int64_t g0 = t * kTG;
+      const int tg = (int)min((int64_t)kTG, P.ngroups - g0);
+      for (int g = tid; g < tg; g += kTreeThreads) {
+        const int vb = (int)((g0 + g) * kGroup);
+        float f[8];
+        Group<TT> tv;
+        tv.load_s(reinterpret_cast<const TT*>(sb), g);
+        tv.unpack(f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (vb + e >= P.V) f[e] = -INFINITY;
+        const float gm = max8(f);
+        if (gm > tmx) {  // rescale by 2^(old fl(m k2) - new fl(m k2)); exact in fp64 below
+          const float nmk = gm * k2;
+          ts *= ex2(tmk - nmk);
+          tmx = gm;
+          tmk = nmk;
+        }
+        float e8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) e8[e] = ex2(fmaf(f[e], k2, -tmk));
+        ts += sum8(e8);
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) {
+          if (n < Nd) {
+            Group<TQ> dv;
+            dv.load_s(reinterpret_cast<const TQ*>(sb + (1 + n) * Ring::kRowB), g);
+            dv.unpack(f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (vb + e >= P.V) f[e] = kLogits ? -INFINITY : 0.f;
+            if (kLogits) {
+              const float dg = max8(f);
+              if (dg > dm[n]) {
+                const float nmk = dg * k2;
+                ds[n] *= ex2(dmk[n] - nmk);
+                dm[n] = dg;
+                dmk[n] = nmk;
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) e8[e] = ex2(fmaf(f[e], k2, -dmk[n]));
+              ds[n] += sum8(e8);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dneg |= (f[e] < 0.f);
+              ds[n] += sum8(f);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[stg]);
+    }
+  }
+  it += (uint32_t)ntile;
+  // fixed-order block reduction (consumer warps): maxima, then the sums rescaled in fp64
+  if (!producer) {
+    const float wm = warp_max(tmx);
+    if (lane == 0) s_rf[warp][0] = wm;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      const float w = (kLogits && n < Nd) ? warp_max(dm[n]) : kNegBig;
+      if (lane == 0) s_rf[warp][1 + n] = w;
+    }
+  }
+  __syncthreads();
+  if (!producer) {
+    float Mc = kNegBig;
+    for (int w2 = 0; w2 < kTreeWarps; ++w2) Mc = fmaxf(Mc, s_rf[w2][0]);
+    double tsd = (ts != 0.f) ? (double)ts * exp2((double)tmk - (double)Mc * (double)k2) : 0.0;
+    tsd = warp_sum(tsd);
+    if (lane == 0) s_rd[warp][0] = tsd;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+      if (n < Nd) {
+        double dsd;
+        if (kLogits) {
+          float dMc = kNegBig;
+          for (int w2 = 0; w2 < kTreeWarps; ++w2) dMc = fmaxf(dMc, s_rf[w2][1 + n]);
+          dsd = (ds[n] != 0.f) ? (double)ds[n] * exp2((double)dmk[n] - (double)dMc * (double)k2) : 0.0;
+        } else {
+          dsd = (double)ds[n];
+        }
+        dsd = warp_sum(dsd);
+        if (lane == 0) s_rd[warp][1 + n] = dsd;
+      }
+    }
+    const int bad = __any_sync(0xffffffffu, dneg) ? 2 : 0;
+    if (lane == 0) s_rbad[warp] = bad;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    NodeStats ns;
+    float M = kNegBig;
+    double S = 0.0;
+    int bad = 0;
+    for (int w2 = 0; w2 < kTreeWarps; ++w2) {
+      M = fmaxf(M, s_rf[w2][0]);
+      S += s_rd[w2][0];
+      bad |= s_rbad[w2];
+    }
+    ns.M = M;
+    ns.S = S;
+    ns.t_nf = !isfinite(S) || !isfinite(M);
+    ns.t_empty = !ns.t_nf && !(S > 0.0);
+    ns.d_nf = (bad & 2) != 0;
+    ns.d_empty = false;
+    for (int n = 0; n < P.N; ++n) {
+      double sv = 0.0;
+      float mx = kNegBig;
+      if (n < Nd) {
+        for (int w2 = 0; w2 < kTreeWarps; ++w2) {
+          sv += s_rd[w2][1 + n];
+          if (kLogits) mx = fmaxf(mx, s_rf[w2][1 + n]);
+        }
+        if (kLogits && !isfinite(mx)) ns.d_nf = true;
+        if (!isfinite(sv)) ns.d_nf = true;
+        else if (!(sv > 0.0)) ns.d_empty = true;
+      }
+      ns.sig[n] = sv;
+      ns.dmax[n] = mx;
+    }
+    node_decide_warp<TT, TQ, kLogits>(T, b, j, ir, Nd > 0, trow, drow, ns, s_ngx, s_ntok, s_nw, s_nsig, s_ndmax,
+                                      s_nzero, s_nd, nullptr, s_cp, s_cq);
+  }
+  __syncthreads();
+}
+
 template <typename TT, typename TQ, bool kLogits, int NMAX>
 __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreeParams T) {
   using Ring = TreeRing<TT, TQ, NMAX>;
@@ -317,8 +509,18 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
   __shared__ int64_t s_y;
   __shared__ float s_margin;
   __shared__ int32_t par[kTreeMaxNodes], tok[kTreeMaxNodes], irw[kTreeMaxNodes];
-  __shared__ int32_t s_e1[kTreeMaxNodes], s_e2[kTreeMaxNodes], s_e3[kTreeMaxNodes];
+  __shared__ int32_t s_e12[kTreeMaxNodes], s_e3[kTreeMaxNodes];  // structure (e1 | e2 << 8), data
   __shared__ double s_cp[kTreeMaxNodes], s_cq[kTreeMaxNodes];
+  // lazy mode: the visited node's record and its statistics-pass scratch
+  __shared__ NodeDec s_nd;
+  __shared__ float s_rf[kTreeWarps][1 + kMaxN];
+  __shared__ double s_rd[kTreeWarps][1 + kMaxN];
+  __shared__ int s_rbad[kTreeWarps];
+  __shared__ float s_ngx[kMaxN * kMaxN];
+  __shared__ int32_t s_ntok[kMaxN];
+  __shared__ double s_nw[kMaxN], s_nsig[kMaxN];
+  __shared__ float s_ndmax[kMaxN];
+  __shared__ int s_nzero, s_have, s_err;
   const Ring ring{tree_smem, s_full, s_empty};
   double* s_parts = reinterpret_cast<double*>(tree_smem + kTreeStages * Ring::kStageB);  // [ntile][warps]
   const bool producer = warp == kTreeWarps;
@@ -336,9 +538,13 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
     par[c] = T.parent[(int64_t)b * nn + c];
     tok[c] = T.node_token[(int64_t)b * nn + c];
     irw[c] = P.irow[(int64_t)b * nn + c];
-    s_e3[c] = nds[c].status;
-    s_cp[c] = cpq[c].p;
-    s_cq[c] = cpq[c].q;
+    if (!T.lazy) {
+      s_e3[c] = nds[c].status;
+      s_cp[c] = cpq[c].p;
+      s_cq[c] = cpq[c].q;
+    } else {
+      s_e3[c] = 0;  // lazy: a node's data errors are found when the walk visits it
+    }
   }
   __syncthreads();
   int32_t* out = P.out_tokens + (int64_t)b * nn;
@@ -363,8 +569,7 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
     for (int c2 = c + 1; c2 < nn; ++c2)
       if (par[c2] == c) { has_child = true; break; }
     if (has_child != (irw[c] >= 0) || irw[c] >= P.I) e2 = COSINE_REQ_BAD_TREE;
-    s_e1[c] = e1;
-    s_e2[c] = e2;
+    s_e12[c] = e1 | (e2 << 8);
   }
   __syncthreads();
   // thread-0 walk state
@@ -372,8 +577,9 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
   float tm = INFINITY;
   bool need_init = true;
   if (tid == 0) {
-    for (int c = 0; c < nn && !err; ++c) err = s_e1[c];
-    for (int c = 0; c < nn && !err; ++c) err = s_e2[c];
+    s_have = -1;
+    for (int c = 0; c < nn && !err; ++c) err = s_e12[c] & 0xff;
+    for (int c = 0; c < nn && !err; ++c) err = s_e12[c] >> 8;
     for (int c = 0; c < nn && !err; ++c) err = s_e3[c];
     s_act = err ? 0 : -1;
   }
@@ -390,8 +596,17 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
       // advance the walk until the block is needed for a pass (act 1) or the final draw (act 2)
       int act = -1;
       while (act < 0) {
+        if (need_init && T.lazy && s_have != j) {  // lazy: node j's statistics first (act 3)
+          act = 3;
+          break;
+        }
         if (need_init) {  // arriving at node j: o_0, q_0 of the node
-          const NodeDec& nd = nds[j];
+          const NodeDec& nd = T.lazy ? s_nd : nds[j];
+          if (nd.status) {  // lazy: a data error of a visited node stops the request
+            err = nd.status;
+            act = 4;
+            break;
+          }
           st.M = nd.M;
           st.invS = (float)(1.0 / nd.S);
           st.k2 = P.k2f;
@@ -432,6 +647,7 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
       }
       s_act = act;
       s_node = j;
+      s_err = err;
       s_Nd = (irw[j] >= 0) ? N : 0;
       if (act == 2) s_u = philox_u24(P.seed, rid, (uint32_t)j, P.step, kTagSample);
     }
@@ -439,6 +655,19 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
     const int act = s_act, jn = s_node, Nd = s_Nd;
     const TT* trow = (const TT*)P.target + ((int64_t)b * nn + jn) * P.ld_t;
     const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? irw[jn] : 0)) * N * P.ld_q;
+    if (act == 4) {  // lazy: a visited node's data error (reading #23)
+      for (int c = tid; c < nn; c += kTreeBlock) { out[c] = -1; acc[c] = -1; }
+      if (tid == 0) { P.accept_len[b] = -1; P.status[b] = s_err; }
+      return;
+    }
+    if (act == 3) {  // lazy: node jn's row statistics (one pass) and its decisions (warp 0)
+      tree_node_stats<TT, TQ, kLogits, NMAX>(T, b, jn, Nd, trow, drow, ring, s_full, s_empty, it, ntile,
+                                             producer, s_rf, s_rd, s_rbad, s_ngx, s_ntok, s_nw, s_nsig,
+                                             s_ndmax, &s_nzero, &s_nd, s_cp, s_cq, irw[jn]);
+      if (tid == 0) s_have = jn;
+      __syncthreads();
+      continue;
+    }
     // A pass: per-tile masses of the weights (mode, rr) into s_tile[0 .. ntile).  The producer
     // lane fills ring slots it .. it + ntile - 1; consumer warp w writes its partial of tile t to
     // s_parts[t][w]; the tile sums (fixed order) follow one block barrier.

@@ -1969,7 +1969,7 @@ cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t strea
                      ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
 }
 
-cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+static cosine_status_t verify_tree_impl(bool lazy, cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
                                    int32_t I, int32_t N, const int32_t* parent,
                                    const int32_t* node_token, const int32_t* internal_row,
                                    const void* target, int64_t ld_t, float temperature,
@@ -2016,6 +2016,7 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
   S.parts = ctx->parts;
   T.parent = parent; T.node_token = node_token; T.node_draft_tokens = node_draft_tokens;
   T.ndec = ctx->ndec; T.cpq = ctx->cpq; T.accepted_nodes = accepted_nodes;
+  T.lazy = lazy ? 1 : 0;
   const int64_t units = (int64_t)B * (J + 1);
   int C = 1;
   if (ctx->cfg.cluster_size > 0) {
@@ -2037,13 +2038,16 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
-  cudaError_t e = cudaLaunchKernelEx(&lc, sf[0], S);  // every node's rows, once
-  if (e == cudaSuccess) {
-    lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&lc, tf[0], T);
+  cudaError_t e = cudaSuccess;
+  if (!lazy) {
+    lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+    e = cudaLaunchKernelEx(&lc, sf[0], S);  // every node's rows, once
+    if (e == cudaSuccess) {
+      lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, tf[0], T);
+    }
   }
   if (e == cudaSuccess) {
     lc.gridDim = dim3((unsigned)B, 1, 1);
@@ -2066,8 +2070,36 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
     ctx->last_launches = 0;
     return fail(ctx, COSINE_ERR_CUDA, std::string("tree kernels: ") + cudaGetErrorString(e));
   }
-  ctx->last_launches = 3;
+  ctx->last_launches = lazy ? 1 : 3;
   return COSINE_OK;
+}
+
+cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                   int32_t I, int32_t N, const int32_t* parent,
+                                   const int32_t* node_token, const int32_t* internal_row,
+                                   const void* target, int64_t ld_t, float temperature,
+                                   const void* draft, int64_t ld_q,
+                                   const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, cosine_weight_mode_t weight_mode,
+                                   int32_t* accept_len, int32_t* accepted_nodes,
+                                   int32_t* out_tokens, int32_t* status) {
+  return verify_tree_impl(false, ctx, stream, B, J, I, N, parent, node_token, internal_row, target, ld_t,
+                          temperature, draft, ld_q, node_draft_tokens, request_ids, step, weight_mode,
+                          accept_len, accepted_nodes, out_tokens, status);
+}
+
+cosine_status_t cosine_verify_tree_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                        int32_t I, int32_t N, const int32_t* parent,
+                                        const int32_t* node_token, const int32_t* internal_row,
+                                        const void* target, int64_t ld_t, float temperature,
+                                        const void* draft, int64_t ld_q,
+                                        const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                        uint32_t step, cosine_weight_mode_t weight_mode,
+                                        int32_t* accept_len, int32_t* accepted_nodes,
+                                        int32_t* out_tokens, int32_t* status) {
+  return verify_tree_impl(true, ctx, stream, B, J, I, N, parent, node_token, internal_row, target, ld_t,
+                          temperature, draft, ld_q, node_draft_tokens, request_ids, step, weight_mode,
+                          accept_len, accepted_nodes, out_tokens, status);
 }
 
 cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B,

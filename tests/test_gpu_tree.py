@@ -9,7 +9,7 @@ from paper_2503_10325_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def _gpu_tree(t, *, seed=3, step=0, wm=0, T=1.0, dtype=torch.float32):
+def _gpu_tree(t, *, seed=3, step=0, wm=0, T=1.0, dtype=torch.float32, lazy=False):
     import paper_2503_10325_b200 as cv
     dev = torch.device("cuda", 0)
     B, nn, _ = t["target"].shape
@@ -24,7 +24,7 @@ def _gpu_tree(t, *, seed=3, step=0, wm=0, T=1.0, dtype=torch.float32):
     d = {k: (v.to(dev) if torch.is_tensor(v) else v) for k, v in t.items()}
     cv.cosine_verify_tree(ctx, d["parent"], d["node_token"], d["internal_row"], d["target"], d["draft"],
                           d["node_draft_tokens"], d["request_ids"], al, an, ot, st, temperature=T, step=step,
-                          weight_mode=wm)
+                          weight_mode=wm, lazy=lazy)
     torch.cuda.synchronize()
     launches = cv.cosine_last_launch_count(ctx)
     cv.cosine_verify_destroy(ctx)
@@ -50,14 +50,15 @@ def _compare(g, r, subset=None):
     return int(mism.sum()), int(flagged.sum())
 
 
+@pytest.mark.parametrize("lazy", [False, True])
 @pytest.mark.parametrize("schedule,cap,V,wm", [((2, 2, 1), 12, 1003, 0), ((3, 1, 1, 1), 20, 777, 1),
                                                ((4, 2, 2, 1, 1, 1, 1, 1), 64, 2049, 2)])
-def test_tree_small(cuda_ok, schedule, cap, V, wm):
+def test_tree_small(cuda_ok, schedule, cap, V, wm, lazy):
     t = synth.tree_inputs(24, 3, V, schedule=schedule, cap=cap, dtype=torch.float32, seed=V, sigma=2.0)
-    g = _gpu_tree(t, wm=wm, step=1)
+    g = _gpu_tree(t, wm=wm, step=1, lazy=lazy)
     r = _oracle_tree(t, wm=wm, step=1)
     _compare(g, r)
-    assert g["launches"] == 3
+    assert g["launches"] == (1 if lazy else 3)
 
 
 def test_chain_tree_equals_linear_on_gpu(cuda_ok):
@@ -72,9 +73,10 @@ def test_chain_tree_equals_linear_on_gpu(cuda_ok):
              internal_row=torch.tensor(list(range(k)) + [-1], dtype=torch.int32).expand(B, k + 1).contiguous(),
              target=inp["target"], draft=inp["draft"], node_draft_tokens=inp["draft_tokens"],
              request_ids=inp["request_ids"], V=inp["V"])
-    g_tree = _gpu_tree(t, seed=21)
-    np.testing.assert_array_equal(g_tree["accept_len"], g_lin["accept_len"])
-    np.testing.assert_array_equal(g_tree["out_tokens"], g_lin["out_tokens"])
+    for lazy in (False, True):
+        g_tree = _gpu_tree(t, seed=21, lazy=lazy)
+        np.testing.assert_array_equal(g_tree["accept_len"], g_lin["accept_len"])
+        np.testing.assert_array_equal(g_tree["out_tokens"], g_lin["out_tokens"])
 
 
 def test_bad_tree_and_errors(cuda_ok):
@@ -97,3 +99,37 @@ def test_c4_full_size_sampled_requests(cuda_ok):
     subset = np.arange(0, c["B"], 25)
     r = _oracle_tree(t, seed=5, subset=torch.as_tensor(subset))
     _compare(g, r, subset=subset)
+
+
+def test_lazy_tree_c4_full_size_equals_full(cuda_ok):
+    # NEXT-1: the lazy walk reads only the visited nodes and must reproduce the all-nodes result
+    c = synth.CONFIGS["c4"]
+    t = synth.tree_inputs(c["B"], c["N"], c["V"], dtype=c["dtype"], seed=45, device="cuda")
+    full = _gpu_tree(t, seed=6)
+    lazy = _gpu_tree(t, seed=6, lazy=True)
+    tie = ((full["status"] | lazy["status"]) & 0x200) != 0
+    diff = (full["accept_len"] != lazy["accept_len"]) | (full["out_tokens"] != lazy["out_tokens"]).any(1) | \
+           (full["accepted_nodes"] != lazy["accepted_nodes"]).any(1) | \
+           ((full["status"] & 0xff) != (lazy["status"] & 0xff))
+    assert not (diff & ~tie).any(), np.nonzero(diff & ~tie)[0][:5]
+    assert lazy["launches"] == 1
+    subset = np.arange(3, c["B"], 41)
+    r = _oracle_tree(t, seed=6, subset=torch.as_tensor(subset))
+    _compare(lazy, r, subset=subset)
+
+
+def test_lazy_tree_errors(cuda_ok):
+    t = synth.tree_inputs(6, 2, 500, schedule=(2, 1), cap=6, dtype=torch.float32, seed=9, sigma=2.0)
+    clean = _gpu_tree(t)
+    t["parent"][1, 3] = 5                      # structure errors: checked for the whole tree
+    t["node_token"][2, 2] = t["node_token"][2, 1]
+    t["target"][4, 0, 7] = float("nan")        # the root is always visited
+    # request 5: poison a leaf the walk does not visit (reading #23: not detected)
+    path5 = set(int(x) for x in clean["accepted_nodes"][5] if x >= 0) | {0}
+    leaves = [j for j in range(1, t["parent"].shape[1]) if int(t["internal_row"][5, j]) < 0 and j not in path5]
+    t["target"][5, leaves[0], 3] = float("nan")
+    lazy = _gpu_tree(t, lazy=True)
+    assert list(lazy["status"][:5] & 0xff) == [0, 6, 6, 0, 3]
+    assert lazy["status"][5] & 0xff == 0
+    assert lazy["accept_len"][5] == clean["accept_len"][5]
+    np.testing.assert_array_equal(lazy["out_tokens"][5], clean["out_tokens"][5])
