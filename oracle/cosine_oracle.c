@@ -689,3 +689,52 @@ int orc_verify_tree(int32_t B, int32_t J, int32_t I, int32_t N, int64_t V,
   free(p); free(q); free(r); free(qn);
   return 0;
 }
+
+/* Drafter-side Fuse of one iteration (NEXT-2): Alg. 1 Fuse and Eq. 4's first line
+ * over the drafters' greedy tokens, written out step by step. */
+int orc_fuse_step(int32_t B, int32_t N, int64_t V, const double* logits, double temperature,
+                  int32_t* own_tokens, double* conf, int32_t* fused_token, int32_t* winner,
+                  int32_t* status, double* conf_gap) {
+  if (B < 0 || N < 1 || V < 1 || !(temperature > 0.0) || !logits) return 1;
+  for (int32_t b = 0; b < B; ++b) {
+    int st = 0;
+    double c[64];
+    int64_t X[64];
+    if (N > 64) return 1;
+    for (int32_t n = 0; n < N && !st; ++n) {
+      const double* l = logits + ((int64_t)b * N + n) * V;
+      int64_t am = -1;
+      st = orc_argmax(l, V, &am); /* X_n: the drafter's own (greedy) token */
+      if (st) break;
+      double M = 0.0, S = 0.0;
+      double* p = (double*)malloc(sizeof(double) * (size_t)V);
+      if (!p) return 1;
+      st = orc_softmax(l, V, temperature, p, &M, &S);
+      if (!st) c[n] = p[am]; /* c_n = P(X_n) */
+      free(p);
+      X[n] = am;
+    }
+    status[b] = st;
+    if (st) {
+      for (int32_t n = 0; n < N; ++n) { own_tokens[(int64_t)b * N + n] = -1; conf[(int64_t)b * N + n] = NAN; }
+      fused_token[b] = -1;
+      winner[b] = -1;
+      if (conf_gap) conf_gap[b] = NAN;
+      continue;
+    }
+    int nstar = 0; /* Eq. 4: the most confident drafter, lowest n on ties */
+    for (int32_t n = 1; n < N; ++n)
+      if (c[n] > c[nstar]) nstar = n;
+    double second = -1.0;
+    for (int32_t n = 0; n < N; ++n)
+      if (n != nstar && c[n] > second) second = c[n];
+    for (int32_t n = 0; n < N; ++n) {
+      own_tokens[(int64_t)b * N + n] = (int32_t)X[n];
+      conf[(int64_t)b * N + n] = c[n];
+    }
+    fused_token[b] = (int32_t)X[nstar];
+    winner[b] = nstar;
+    if (conf_gap) conf_gap[b] = (N > 1) ? (c[nstar] - second) / c[nstar] : INFINITY;
+  }
+  return 0;
+}

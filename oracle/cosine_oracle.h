@@ -103,6 +103,18 @@ int orc_verify_tree(int32_t B, int32_t J, int32_t I, int32_t N, int64_t V,
                     int32_t* accept_len, int32_t* accepted_nodes, int32_t* out_tokens,
                     int32_t* status, double* tie_margin);
 
+/* Drafter-side token fusion of one drafting iteration (Alg. 1 Fuse,
+ * P:376-381, Eq. 4 first line P:406-408, greedy drafting P:681): logits[B][N][V] are the N
+ * drafters' LM-head outputs for request b at iteration i.  Per drafter: its own token
+ * X_n = argmax_v l_n(v) (lowest index on ties) and its probability c_n = softmax(l_n / T)(X_n)
+ * = 1 / sum_v exp(l_n(v)/T - max/T); then x* = X_{n*}, n* = argmax_n c_n (lowest n on ties).
+ * Outputs own_tokens[B][N], conf[B][N], fused_token[B], winner[B], status[B] (per request: the
+ * first drafter row with an error decides it; -1 tokens), conf_gap[B] = (c_(1) - c_(2)) / c_(1)
+ * (the tie margin, reading #18; +inf for N = 1).  Returns 0, or 1 on a bad argument. */
+int orc_fuse_step(int32_t B, int32_t N, int64_t V, const double* logits, double temperature,
+                  int32_t* own_tokens, double* conf, int32_t* fused_token, int32_t* winner,
+                  int32_t* status, double* conf_gap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,7 @@ INFO_DEGENERATE = 0x100
 
 __all__ = [
     "build", "lib", "philox4x32_10", "uniform", "invcdf", "softmax", "residual",
-    "verify_batch", "fuse_drafts", "sample_residual", "verify_tree",
+    "verify_batch", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step",
     "TAG_ACCEPT", "TAG_SAMPLE", "TAG_FUSE", "TAG_TREE_GEN",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE",
     "DRAFT_PROBS", "DRAFT_LOGITS", "ST_OK", "ST_ZERO_PROB", "ST_TOKEN_RANGE",
@@ -72,6 +72,7 @@ def lib():
                                           _u64, _u32, _P, _P, _P, _P]
         L.orc_verify_tree.argtypes = [_i32, _i32, _i32, _i32, _i64, _P, _P, _P, _P, _f64, _P, _i32,
                                       _P, _P, _u64, _u32, _i32, _P, _P, _P, _P, _P]
+        L.orc_fuse_step.argtypes = [_i32, _i32, _i64, _P, _f64, _P, _P, _P, _P, _P, _P]
         _lib = L
     return _lib
 
@@ -238,4 +239,21 @@ def verify_tree(parent, node_token, internal_row, target, draft, node_draft_toke
                                _ptr(out["status"]), _ptr(out["tie_margin"]))
     if rc != 0:
         raise ValueError("oracle verify_tree: invalid argument")
+    return out
+
+
+def fuse_step(logits, *, temperature=1.0, vocab=None):
+    """Drafter-side Fuse of one iteration (NEXT-2): logits [B][N][V] -> dict(own_tokens, conf,
+    fused_token, winner, status, conf_gap)."""
+    l = _f64arr(logits)
+    if vocab is not None:
+        l = np.ascontiguousarray(l[..., :vocab])
+    B, N, V = l.shape
+    out = dict(own_tokens=np.zeros((B, N), np.int32), conf=np.zeros((B, N)), fused_token=np.zeros(B, np.int32),
+               winner=np.zeros(B, np.int32), status=np.zeros(B, np.int32), conf_gap=np.zeros(B))
+    rc = lib().orc_fuse_step(B, N, V, _ptr(l), float(temperature), _ptr(out["own_tokens"]), _ptr(out["conf"]),
+                             _ptr(out["fused_token"]), _ptr(out["winner"]), _ptr(out["status"]),
+                             _ptr(out["conf_gap"]))
+    if rc != 0:
+        raise ValueError("oracle fuse_step: invalid argument")
     return out

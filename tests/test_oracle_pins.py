@@ -486,3 +486,41 @@ def test_tree_enumeration_exact_and_realised():
         seq = tuple(int(x) for x in rt["out_tokens"][b, : rt["accept_len"][b] + 1])
         counts[seq] = counts.get(seq, 0) + 1
     assert _chi2_law(counts, law, n) > 1e-4
+
+
+# ---------------- drafter-side Fuse of one iteration (NEXT-2) ----------------
+def test_fuse_step_pins_against_library_routines():
+    # X_n = numpy argmax (lowest index), c_n = scipy softmax at X_n, n* = first max
+    import scipy.special
+    rng = np.random.default_rng(3)
+    B, N, V = 7, 4, 301
+    l = rng.normal(size=(B, N, V)) * 3.0
+    l[2, 1, 17] = l[2, 1].max() + 1.0   # a clear winner token
+    l[3, 2] = l[3, 0]                   # identical drafters -> tie -> lowest n
+    r = oracle.fuse_step(l, temperature=0.8)
+    X = l.argmax(-1)
+    p = scipy.special.softmax(l / 0.8, axis=-1)
+    c = np.take_along_axis(p, X[..., None], -1)[..., 0]
+    np.testing.assert_array_equal(r["own_tokens"], X)
+    np.testing.assert_allclose(r["conf"], c, rtol=1e-12)
+    np.testing.assert_array_equal(r["winner"], c.argmax(-1))
+    np.testing.assert_array_equal(r["fused_token"], X[np.arange(B), c.argmax(-1)])
+    assert (r["status"] == 0).all()
+    # the closed form c = 1 / sum exp((l - max) / T)
+    S = np.exp((l - l.max(-1, keepdims=True)) / 0.8).sum(-1)
+    np.testing.assert_allclose(r["conf"], 1.0 / S, rtol=1e-12)
+
+
+def test_fuse_step_ties_and_errors():
+    l = np.zeros((3, 3, 5))
+    l[0, :, 2] = 1.0                     # every drafter picks token 2 with the same confidence
+    l[1, 1, 4] = 5.0                     # drafter 1 is the most confident
+    l[2, 2, 0] = np.nan                  # a non-finite logit in the last drafter
+    r = oracle.fuse_step(l, temperature=1.0)
+    assert r["winner"][0] == 0 and r["fused_token"][0] == 2 and r["conf_gap"][0] == 0.0
+    assert r["winner"][1] == 1 and r["fused_token"][1] == 4
+    assert r["status"][2] == 3 and r["fused_token"][2] == -1
+    # ties in a row: the lowest index is the drafter's token
+    l2 = np.zeros((1, 1, 6))
+    l2[0, 0, [1, 4]] = 2.0
+    assert oracle.fuse_step(l2)["own_tokens"][0, 0] == 1
