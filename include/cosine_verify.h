@@ -204,6 +204,22 @@ cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t strea
                                          const cosine_debug_t* debug);
 
 /*
+ * cosine_fuse_step — drafter-side token fusion of ONE drafting iteration (
+ * Alg. 1 Fuse P:376-381, Eq. 4 first line P:406-408, greedy drafting P:681): the central node's
+ * step between the drafters' LM heads and the next iteration.
+ *   logits [B][N][ld] the N drafters' LM-head outputs for request b (config draft_dtype;
+ *          ld >= V, 16-byte aligned rows);  temperature > 0 (softmax of l / T)
+ * Outputs: own_tokens [B][N] X_n = argmax_v l_n(v) (lowest index on ties); conf [B][N]
+ *   c_n = softmax(l_n / T)(X_n); fused_token [B] x* = X_{n*}; winner [B] n* = argmax_n c_n
+ *   (lowest n on ties); status [B] (NaN / +inf logit -> NONFINITE_INPUT, all -inf -> EMPTY_ROW;
+ *   the first erroring drafter decides; tokens -1).  Needs B * N <= max_batch * (max_draft_len + 1)
+ *   (context scratch).  Two launches (one streaming pass over the rows, one combine).
+ */
+cosine_status_t cosine_fuse_step(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t N,
+                                 const void* logits, int64_t ld, float temperature, int32_t* own_tokens,
+                                 float* conf, int32_t* fused_token, int32_t* winner, int32_t* status);
+
+/*
  * cosine_sample_residual — the final-token sample of one row group per request,
  * for callers that verify elsewhere.
  *   target_rows [B][ld_t] logits of the row at L_b;  temperature (0 = argmax)

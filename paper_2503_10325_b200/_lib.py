@@ -77,6 +77,8 @@ _lib.cosine_verify_tree.argtypes = [_P, _P, _i32, _i32, _i32, _i32, _P, _P, _P, 
                                     _P, _P, _u32, ctypes.c_int, _P, _P, _P, _P]
 _lib.cosine_verify_tree.restype = ctypes.c_int
 _lib.cosine_verify_tree_lazy.argtypes = _lib.cosine_verify_tree.argtypes
+_lib.cosine_fuse_step.argtypes = [_P, _P, _i32, _i32, _P, _i64, _f32, _P, _P, _P, _P, _P]
+_lib.cosine_fuse_step.restype = ctypes.c_int
 _lib.cosine_verify_tree_lazy.restype = ctypes.c_int
 _lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
 _lib.cosine_nccl_unique_id.restype = ctypes.c_int
@@ -89,7 +91,7 @@ EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
                     "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
-                    "cosine_verify_tree_lazy")
+                    "cosine_verify_tree_lazy", "cosine_fuse_step")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -257,4 +259,14 @@ def cosine_sample_residual(ctx, target_rows, node_ids, request_ids, out_token, s
                                      _ptr(draft_rows), ld_q, _ptr(weights), _ptr(draft_norm), N,
                                      _ptr(node_ids), _ptr(request_ids), step, _ptr(out_token),
                                      _ptr(status))
+    _check(rc, ctx)
+
+
+def cosine_fuse_step(ctx, logits, own_tokens, conf, fused_token, winner, status, *, temperature=1.0,
+                     stream=None):
+    """Drafter-side Fuse of one iteration (NEXT-2): logits [B][N][ld] -> own_tokens [B][N],
+    conf [B][N], fused_token [B], winner [B], status [B]."""
+    B, N, ld = logits.shape
+    rc = _lib.cosine_fuse_step(ctx, _stream(stream, logits.device), B, N, _ptr(logits), ld, temperature,
+                               _ptr(own_tokens), _ptr(conf), _ptr(fused_token), _ptr(winner), _ptr(status))
     _check(rc, ctx)

@@ -1072,6 +1072,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
 #include "cosine_split.cuh"
 #include "cosine_tree.cuh"
 #include "cosine_shard.cuh"
+#include "cosine_fuse_step.cuh"
 namespace cosine {
 
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
@@ -1179,6 +1180,7 @@ struct cosine_ctx_s {
   int32_t last_launches = 0;
   int32_t last_cluster = 0, last_ncl = 0;
   int32_t* lz = nullptr;  // lazy verification: per-request state
+  size_t parts_cap = 0;    // PartRec entries in `parts`
   // vocabulary-sharded mode (nranks > 1)
   ncclComm_t comm = nullptr;
   uint32_t* rec_send = nullptr;
@@ -1670,6 +1672,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ndec, nt * sizeof(NodeDec));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->cpq, nt * sizeof(ChildPQ));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->parts, nu * kMaxC * sizeof(PartRec));
+  ctx->parts_cap = nu * kMaxC;
   if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
   // counters: [B] kernel-B CTAs per request | [B] decided units per request | [B][k+1] chunks per unit
   const size_t ncnt = 2 * nb + nb * (size_t)(cfg->max_draft_len + 1);
@@ -2086,6 +2089,64 @@ cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int
   return verify_tree_impl(false, ctx, stream, B, J, I, N, parent, node_token, internal_row, target, ld_t,
                           temperature, draft, ld_q, node_draft_tokens, request_ids, step, weight_mode,
                           accept_len, accepted_nodes, out_tokens, status);
+}
+
+cosine_status_t cosine_fuse_step(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t N,
+                                 const void* logits, int64_t ld, float temperature, int32_t* own_tokens,
+                                 float* conf, int32_t* fused_token, int32_t* winner, int32_t* status) {
+  cosine_status_t s = check_common(ctx, B, 1, N);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_fuse_step runs on unsharded contexts (nranks == 1)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, logits, ld, ctx->cfg.draft_dtype, "logits")) != COSINE_OK) return s;
+  if (!own_tokens || !conf || !fused_token || !winner || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature > 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "fuse_step needs a finite temperature > 0");
+  DeviceGuard dg(ctx->cfg.device);
+  FuseStepParams F;
+  memset(&F, 0, sizeof(F));
+  F.B = B; F.N = N; F.V = ctx->V; F.ld = ld;
+  F.ngroups = (ctx->V + kGroup - 1) / kGroup;
+  F.gfull = ctx->V / kGroup;
+  F.k2f = (float)(1.4426950408889634 / (double)temperature);
+  const int64_t rows = (int64_t)B * N;
+  int C = 1;
+  while (C < kMaxC && F.ngroups > (int64_t)C * kThreads * 8) C *= 2;
+  while (C < kMaxC && rows * C < 148 * 8 && F.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  while (C > 1 && (size_t)(rows * C) > ctx->parts_cap) C /= 2;
+  if ((size_t)(rows * C) > ctx->parts_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "B * N exceeds the context's scratch (raise max_batch / max_draft_len)");
+  F.C = C;
+  F.cg = (F.ngroups + C - 1) / C;
+  F.logits = logits;
+  F.parts = ctx->parts;
+  F.own_tokens = own_tokens; F.conf = conf; F.fused_token = fused_token; F.winner = winner; F.status = status;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  lc.gridDim = dim3((unsigned)(rows * C), 1, 1);
+  cudaError_t e = (ctx->cfg.draft_dtype == COSINE_BF16)
+                      ? cudaLaunchKernelEx(&lc, fuse_step_stats_kernel<__nv_bfloat16>, F)
+                      : cudaLaunchKernelEx(&lc, fuse_step_stats_kernel<float>, F);
+  if (e == cudaSuccess) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    lc.gridDim = dim3((unsigned)((B + kWarps - 1) / kWarps), 1, 1);
+    e = cudaLaunchKernelEx(&lc, fuse_step_combine_kernel, F);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("fuse_step kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 2;
+  return COSINE_OK;
 }
 
 cosine_status_t cosine_verify_tree_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
