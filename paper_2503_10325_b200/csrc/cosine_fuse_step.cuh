@@ -35,22 +35,23 @@ __global__ void __launch_bounds__(kThreads) fuse_step_stats_kernel(const FuseSte
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const T* r = (const T*)P.logits + row * P.ld;
   const float k2 = P.k2f;
-  float bv = -INFINITY;
+  float bv = -INFINITY;  // running max (also the argmax value); sums are relative to fl(bv k2)
   int64_t bi = -1;
-  float tmx = kNegBig, tmk = kNegBig, ts = 0.f;
-  bool bad = false;
+  float tmk = kNegBig, ts = 0.f;
   const int64_t gb = (int64_t)rank * P.cg, ge = min(P.ngroups, gb + P.cg), gfe = min(ge, P.gfull);
+  // ~40 instructions per 8 elements: the index search and the rescale run only when the group
+  // max improves; a NaN / +inf logit poisons the sum (detected at the combine)
   auto step = [&](const float (&f)[8], int64_t gi) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      if (f[e] > bv) { bv = f[e]; bi = gi * kGroup + e; }  // ascending order: first index wins ties
-      bad |= !(f[e] <= 3.402823466e+38f);                  // NaN or +inf
-    }
     const float gm = max8(f);
-    if (gm > tmx) {
+    if (gm > bv) {  // ascending order: the first index of the new max wins ties
+      int e0 = 0;
+#pragma unroll
+      for (int e = 7; e >= 0; --e)
+        if (f[e] == gm) e0 = e;
+      bi = gi * kGroup + e0;
+      bv = gm;
       const float nmk = gm * k2;
       ts *= ex2(tmk - nmk);
-      tmx = gm;
       tmk = nmk;
     }
     float e8[8];
@@ -58,51 +59,54 @@ __global__ void __launch_bounds__(kThreads) fuse_step_stats_kernel(const FuseSte
     for (int e = 0; e < 8; ++e) e8[e] = ex2(fmaf(f[e], k2, -tmk));
     ts += sum8(e8);
   };
-  for (int64_t gi = gb + tid; gi < gfe; gi += kThreads) {
-    Group<T> g;
-    g.load(r, gi);
-    float f[8];
-    g.unpack(f);
-    step(f, gi);
+  // four groups of loads in flight per thread (one row per CTA: 16 B per load), processed in
+  // ascending index order (the argmax keeps the first index on ties)
+  constexpr int kU = 4;
+  for (int64_t g0 = gb + tid; g0 < gfe; g0 += kU * kThreads) {
+    Group<T> g[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (g0 + u * kThreads < gfe) g[u].load(r, g0 + u * kThreads);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (g0 + u * kThreads < gfe) {
+        float f[8];
+        g[u].unpack(f);
+        step(f, g0 + u * kThreads);
+      }
+    }
   }
   if (gfe < ge && tid == (int)((gfe - gb) % kThreads)) {  // the row's partial last group
     float f[8];
     load_partial(r, gfe, P.V, -INFINITY, f);
     step(f, gfe);
   }
-  __shared__ float s_v[kWarps], s_m[kWarps];
+  __shared__ float s_v[kWarps];
   __shared__ int64_t s_i[kWarps];
   __shared__ double s_s[kWarps];
-  __shared__ int s_bad[kWarps];
   float wv = bv;
   int64_t wi = bi;
   warp_argmax(wv, wi);
-  const float wm = warp_max(tmx);
-  if (lane == 0) { s_v[warp] = wv; s_i[warp] = wi; s_m[warp] = wm; }
+  if (lane == 0) { s_v[warp] = wv; s_i[warp] = wi; }
   __syncthreads();
-  float Mc = kNegBig;
-  for (int w = 0; w < kWarps; ++w) Mc = fmaxf(Mc, s_m[w]);
-  double tsd = (ts != 0.f) ? (double)ts * exp2((double)tmk - (double)Mc * (double)k2) : 0.0;
+  float Mc = -INFINITY;
+  int64_t ix = -1;
+  for (int w = 0; w < kWarps; ++w)
+    if (s_i[w] >= 0 && (ix < 0 || s_v[w] > Mc || (s_v[w] == Mc && s_i[w] < ix))) { Mc = s_v[w]; ix = s_i[w]; }
+  const float Mk = (ix >= 0) ? Mc : kNegBig;
+  double tsd = (ts != 0.f) ? (double)ts * exp2((double)tmk - (double)Mk * (double)k2) : 0.0;
   tsd = warp_sum(tsd);
-  const int wb = __any_sync(0xffffffffu, bad) ? 1 : 0;
-  if (lane == 0) { s_s[warp] = tsd; s_bad[warp] = wb; }
+  if (lane == 0) s_s[warp] = tsd;
   __syncthreads();
   if (tid == 0) {
-    float v = -INFINITY;
-    int64_t ix = -1;
     double t = 0.0;
-    int bd = 0;
-    for (int w = 0; w < kWarps; ++w) {
-      if (s_i[w] >= 0 && (ix < 0 || s_v[w] > v || (s_v[w] == v && s_i[w] < ix))) { v = s_v[w]; ix = s_i[w]; }
-      t += s_s[w];
-      bd |= s_bad[w];
-    }
+    for (int w = 0; w < kWarps; ++w) t += s_s[w];
     PartRec* rec = P.parts + row * C + rank;
-    rec->tmax = Mc;   // chunk max (the sums are relative to it)
+    rec->tmax = Mk;   // chunk max (the sums are relative to it)
     rec->targ = ix;   // chunk argmax (global index), -1 if the chunk is all -inf
-    rec->dmax[0] = v; // its value
-    rec->tsum = t;
-    rec->bad = bd;
+    rec->dmax[0] = Mc;
+    rec->tsum = t;    // NaN / inf if the chunk has a NaN or +inf logit
+    rec->bad = 0;
   }
 }
 
@@ -125,10 +129,9 @@ __global__ void __launch_bounds__(kThreads) fuse_step_combine_kernel(const FuseS
     const float M = warp_max(tmax);
     const double ts = own ? pr[lane].tsum : 0.0;
     const double S = warp_sum(ts != 0.0 ? ts * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
-    const int bad = __reduce_or_sync(0xffffffffu, own ? pr[lane].bad : 0);
     int sn = 0;
-    if (bad) sn = COSINE_REQ_NONFINITE_INPUT;
-    else if (ix < 0 || !(S > 0.0) || !isfinite(S)) sn = COSINE_REQ_EMPTY_ROW;
+    if (!isfinite(S) || (ix >= 0 && !isfinite(v))) sn = COSINE_REQ_NONFINITE_INPUT;  // NaN / +inf logit
+    else if (ix < 0 || !(S > 0.0)) sn = COSINE_REQ_EMPTY_ROW;                        // all -inf
     if (!st && sn) st = sn;  // the first drafter row with an error decides the request
     const double c = sn ? NAN : 1.0 / S;  // P(X_n) = 2^0 / S
     if (lane == 0) {

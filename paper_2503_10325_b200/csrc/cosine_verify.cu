@@ -2112,9 +2112,11 @@ cosine_status_t cosine_fuse_step(cosine_ctx_t ctx, cosine_stream_t stream, int32
   F.gfull = ctx->V / kGroup;
   F.k2f = (float)(1.4426950408889634 / (double)temperature);
   const int64_t rows = (int64_t)B * N;
+  // one row per CTA (16 B per load): ~32 groups per thread keep the per-CTA reduction cheap
   int C = 1;
-  while (C < kMaxC && F.ngroups > (int64_t)C * kThreads * 8) C *= 2;
-  while (C < kMaxC && rows * C < 148 * 8 && F.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  while (C < kMaxC && F.ngroups > (int64_t)C * kThreads * 32) C *= 2;
+  while (C < kMaxC && rows * C < 148 * 6 && F.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  if (const char* v = getenv("COSINE_FUSE_STEP_C")) C = std::max(1, std::min(kMaxC, atoi(v)));
   while (C > 1 && (size_t)(rows * C) > ctx->parts_cap) C /= 2;
   if ((size_t)(rows * C) > ctx->parts_cap)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "B * N exceeds the context's scratch (raise max_batch / max_draft_len)");
