@@ -738,3 +738,57 @@ int orc_fuse_step(int32_t B, int32_t N, int64_t V, const double* logits, double 
   }
   return 0;
 }
+
+/* Routing feedback (NEXT-3): Eq. 1 then Eq. 2, written out. */
+static double orc_cos(const double* a, const double* b, int64_t H) {
+  double ab = 0.0, aa = 0.0, bb = 0.0;
+  for (int64_t h = 0; h < H; ++h) { ab += a[h] * b[h]; aa += a[h] * a[h]; bb += b[h] * b[h]; }
+  if (aa == 0.0 || bb == 0.0) return 0.0;
+  return ab / (sqrt(aa) * sqrt(bb));
+}
+
+int orc_route_update(int32_t B, int32_t N, int32_t K, int64_t V, int64_t Hd, const int32_t* draft_tokens,
+                     const double* conf, const int32_t* accepted, int64_t acc_stride, const int32_t* accept_len,
+                     const double* emb, const uint8_t* participating, double decay, double eps, double* M,
+                     double* d_out, int32_t* status) {
+  if (B < 0 || N < 1 || K < 1 || V < 1 || Hd < 1 || acc_stride < K || !(eps > 0.0 && eps < 0.5)) return 1;
+  for (int32_t b = 0; b < B; ++b) {
+    status[b] = 0;
+    const int32_t L = accept_len[b];
+    if (L < 0) continue; /* a request whose verification failed: no feedback */
+    int bad = 0;
+    for (int32_t n = 0; n < N; ++n)
+      for (int32_t i = 0; i < K; ++i) {
+        const int32_t x = draft_tokens[((int64_t)b * N + n) * K + i];
+        if (x < 0 || x >= V) bad = 1;
+      }
+    for (int32_t i = 0; i < K && i < L; ++i) {
+      const int32_t a = accepted[(int64_t)b * acc_stride + i];
+      if (a < 0 || a >= V) bad = 1;
+    }
+    if (bad) { status[b] = 2; continue; }
+    for (int32_t n = 0; n < N; ++n) {
+      const int64_t bn = (int64_t)b * N + n;
+      if (participating && !participating[bn]) {
+        M[bn] = 0.5 + decay * (M[bn] - 0.5); /* non-participating entries decay to 0.5 */
+        continue;
+      }
+      double m = 0.0;
+      for (int32_t i = 0; i < K; ++i) {
+        double d = 0.0;
+        if (i < L) { /* Eq. 1 */
+          const int32_t a = accepted[(int64_t)b * acc_stride + i];
+          const int32_t x = draft_tokens[bn * K + i];
+          d = orc_cos(emb + (int64_t)a * Hd, emb + (int64_t)x * Hd, Hd);
+        }
+        if (d_out) d_out[bn * K + i] = d;
+        double c = conf[bn * K + i];
+        c = c < eps ? eps : (c > 1.0 - eps ? 1.0 - eps : c);
+        d = d < eps ? eps : (d > 1.0 - eps ? 1.0 - eps : d);
+        m += c * d / (c * d + (1.0 - c) * (1.0 - d)); /* Eq. 2 */
+      }
+      M[bn] = m / K;
+    }
+  }
+  return 0;
+}

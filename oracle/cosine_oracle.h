@@ -115,6 +115,20 @@ int orc_fuse_step(int32_t B, int32_t N, int64_t V, const double* logits, double 
                   int32_t* own_tokens, double* conf, int32_t* fused_token, int32_t* winner,
                   int32_t* status, double* conf_gap);
 
+/* Routing feedback after verification (Alg. 1 "Update routing matrix",
+ * Eq. 1 P:318-327 and Eq. 2).  Per request b and node n:
+ *   d_{n,i} = cos(H(x_i), H(X_{n,i})) for i < L_b (x_i = accepted token i, H = embedding rows
+ *             emb[V][Hd]), else 0                                              (Eq. 1)
+ *   m_n = (1/K) sum_i c d / (c d + (1 - c)(1 - d)), c and d clamped to [eps, 1 - eps]  (Eq. 2)
+ * participating[b][n] != 0: M[b][n] = m_n; else M[b][n] = 0.5 + decay (M[b][n] - 0.5)
+ * (S:315).  draft_tokens [B][N][K], conf [B][N][K], accepted [B][K] (or longer rows, stride
+ * acc_stride), accept_len [B] (< 0: request skipped), M [B][N] in/out, d_out [B][N][K] or NULL.
+ * A token outside [0, V) makes that request's status 2 (M unchanged).  Returns 0 / 1 (bad arg). */
+int orc_route_update(int32_t B, int32_t N, int32_t K, int64_t V, int64_t Hd, const int32_t* draft_tokens,
+                     const double* conf, const int32_t* accepted, int64_t acc_stride, const int32_t* accept_len,
+                     const double* emb, const uint8_t* participating, double decay, double eps, double* M,
+                     double* d_out, int32_t* status);
+
 #ifdef __cplusplus
 }
 #endif

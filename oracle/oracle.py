@@ -24,7 +24,7 @@ INFO_DEGENERATE = 0x100
 
 __all__ = [
     "build", "lib", "philox4x32_10", "uniform", "invcdf", "softmax", "residual",
-    "verify_batch", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step",
+    "verify_batch", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step", "route_update",
     "TAG_ACCEPT", "TAG_SAMPLE", "TAG_FUSE", "TAG_TREE_GEN",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE",
     "DRAFT_PROBS", "DRAFT_LOGITS", "ST_OK", "ST_ZERO_PROB", "ST_TOKEN_RANGE",
@@ -73,6 +73,8 @@ def lib():
         L.orc_verify_tree.argtypes = [_i32, _i32, _i32, _i32, _i64, _P, _P, _P, _P, _f64, _P, _i32,
                                       _P, _P, _u64, _u32, _i32, _P, _P, _P, _P, _P]
         L.orc_fuse_step.argtypes = [_i32, _i32, _i64, _P, _f64, _P, _P, _P, _P, _P, _P]
+        L.orc_route_update.argtypes = [_i32, _i32, _i32, _i64, _i64, _P, _P, _P, _i64, _P, _P, _P, _f64, _f64,
+                                       _P, _P, _P]
         _lib = L
     return _lib
 
@@ -257,3 +259,24 @@ def fuse_step(logits, *, temperature=1.0, vocab=None):
     if rc != 0:
         raise ValueError("oracle fuse_step: invalid argument")
     return out
+
+
+def route_update(draft_tokens, conf, accepted, accept_len, emb, M, *, participating=None, decay=0.9,
+                 eps=1e-6):
+    """Routing feedback (NEXT-3, Eqs. 1-2): returns dict(M (updated copy), d, status)."""
+    X = _arr(draft_tokens, np.int32)
+    B, N, K = X.shape
+    c = _f64arr(conf)
+    acc = _arr(accepted, np.int32)
+    L = _arr(accept_len, np.int32)
+    E = _f64arr(emb)
+    V, Hd = E.shape
+    Mo = _f64arr(M).copy()
+    part = None if participating is None else _arr(participating, np.uint8)
+    d = np.zeros((B, N, K))
+    st = np.zeros(B, np.int32)
+    rc = lib().orc_route_update(B, N, K, V, Hd, _ptr(X), _ptr(c), _ptr(acc), acc.shape[1], _ptr(L), _ptr(E),
+                                _ptr(part), float(decay), float(eps), _ptr(Mo), _ptr(d), _ptr(st))
+    if rc != 0:
+        raise ValueError("oracle route_update: invalid argument")
+    return dict(M=Mo, d=d, status=st)

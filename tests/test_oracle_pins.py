@@ -524,3 +524,55 @@ def test_fuse_step_ties_and_errors():
     l2 = np.zeros((1, 1, 6))
     l2[0, 0, [1, 4]] = 2.0
     assert oracle.fuse_step(l2)["own_tokens"][0, 0] == 1
+
+
+# ---------------- routing feedback (NEXT-3): Eqs. 1-2 ----------------
+def _one_hot_emb(V, H):
+    E = np.zeros((V, H))
+    for v in range(V):
+        E[v, v % H] = 1.0
+    return E
+
+
+def test_route_update_spec_examples():
+    # S:273-275 (Eq. 2 evaluated by hand): c = d = 0.5 -> 0.5; K=1, c = d = 0.9 -> 0.81 / 0.82;
+    # K=2 terms (0.9, 0.9) and (0.5, 0.5) -> (0.9878... + 0.5) / 2.  d is set through cosines of
+    # crafted embeddings (cos = 0.9 / 0.5 between tokens 1 and 2 / 3) so that Eq. 1 feeds Eq. 2.
+    H = 2
+    E = np.array([[1.0, 0.0], [1.0, 0.0], [0.9, np.sqrt(1 - 0.81)], [0.5, np.sqrt(0.75)]])
+    M = np.zeros((1, 1))
+    r = oracle.route_update([[[2]]], [[[0.9]]], [[1]], [1], E, M)
+    assert abs(r["M"][0, 0] - 0.81 / 0.82) < 1e-12 and abs(r["M"][0, 0] - 0.9878048780487805) < 1e-12
+    r = oracle.route_update([[[2, 3]]], [[[0.9, 0.5]]], [[1, 1]], [2], E, M)
+    assert abs(r["M"][0, 0] - 0.7439024390243902) < 1e-12
+    r = oracle.route_update([[[3]]], [[[0.5]]], [[1]], [1], E, M)
+    assert abs(r["M"][0, 0] - 0.5) < 1e-12
+
+
+def test_route_update_eq1_cases_and_decay():
+    V, H, K = 8, 8, 4
+    E = _one_hot_emb(V, H)
+    X = np.array([[[1, 2, 3, 4], [5, 6, 7, 0]]], np.int32)
+    acc = np.array([[1, 2, 3, 4]], np.int32)
+    c = np.full((1, 2, K), 0.7)
+    M = np.array([[0.9, 0.9]])
+    # self-similarity: the draft is the accepted prefix -> d = 1; orthogonal -> 0
+    r = oracle.route_update(X, c, acc, [4], E, M)
+    np.testing.assert_allclose(r["d"][0, 0], 1.0)
+    np.testing.assert_allclose(r["d"][0, 1], 0.0)
+    # accept_len = 0: all d = 0
+    r0 = oracle.route_update(X, c, acc, [0], E, M)
+    assert (r0["d"] == 0).all()
+    # d beyond L is 0 (Eq. 1 "otherwise")
+    r2 = oracle.route_update(X, c, acc, [2], E, M)
+    np.testing.assert_allclose(r2["d"][0, 0], [1, 1, 0, 0])
+    # non-participating decay: 0.5 + 0.9 (0.9 - 0.5) = 0.86
+    r3 = oracle.route_update(X, c, acc, [4], E, M, participating=[[1, 0]], decay=0.9)
+    assert abs(r3["M"][0, 1] - 0.86) < 1e-12
+    # scores stay in (0, 1) and are monotone in c
+    lo = oracle.route_update(X, np.full((1, 2, K), 0.3), acc, [3], E, M)["M"]
+    hi = oracle.route_update(X, np.full((1, 2, K), 0.8), acc, [3], E, M)["M"]
+    assert ((lo > 0) & (lo < 1) & (hi >= lo)).all()
+    # a token outside [0, V): status 2, M unchanged
+    bad = oracle.route_update(np.array([[[1, 2, 3, 99], [5, 6, 7, 0]]], np.int32), c, acc, [4], E, M)
+    assert bad["status"][0] == 2 and (bad["M"] == M).all()
