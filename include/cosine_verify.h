@@ -220,6 +220,27 @@ cosine_status_t cosine_fuse_step(cosine_ctx_t ctx, cosine_stream_t stream, int32
                                  float* conf, int32_t* fused_token, int32_t* winner, int32_t* status);
 
 /*
+ * cosine_route_update — routing feedback after verification (Alg. 1 "Update
+ * routing matrix"; Eq. 1, Eq. 2; decay of non-participating nodes S:315).
+ *   draft_tokens [B][N][K] int32 X_{n,i} (node n's own draft);  conf [B][N][K] fp32 c_{n,i}
+ *   accepted [B][acc_stride] int32 (e.g. out_tokens, acc_stride = k + 1);  accept_len [B] L_b
+ *     (< 0: the request failed verification -> no update)
+ *   emb [V][ld_e] embedding rows H(.) (bf16 / fp32, hidden % 8 == 0, 16-byte aligned rows)
+ *   participating [B][N] uint8 or NULL (= all);  decay in [0, 1]
+ *   M [B][N] fp32 routing scores, updated in place:  m_n = (1/K) sum_i c d / (c d + (1-c)(1-d))
+ *     with d_{n,i} = cos(H(x_i), H(X_{n,i})) for i < L_b else 0, c and d clamped to
+ *     [1e-6, 1 - 1e-6] (reading #24); non-participating: M = 0.5 + decay (M - 0.5)
+ *   d_out [B][N][K] fp32 or NULL;  status [B]: 2 if a token is outside [0, vocab_size) (M kept).
+ * One launch (CTA per request, warp per node).  V = the context's vocab_size.
+ */
+cosine_status_t cosine_route_update(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t N, int32_t K,
+                                    const int32_t* draft_tokens, const float* conf, const int32_t* accepted,
+                                    int64_t acc_stride, const int32_t* accept_len, const void* emb,
+                                    int64_t hidden, int64_t ld_e, cosine_dtype_t emb_dtype,
+                                    const uint8_t* participating, float decay, float* M, float* d_out,
+                                    int32_t* status);
+
+/*
  * cosine_sample_residual — the final-token sample of one row group per request,
  * for callers that verify elsewhere.
  *   target_rows [B][ld_t] logits of the row at L_b;  temperature (0 = argmax)

@@ -79,6 +79,9 @@ _lib.cosine_verify_tree.restype = ctypes.c_int
 _lib.cosine_verify_tree_lazy.argtypes = _lib.cosine_verify_tree.argtypes
 _lib.cosine_fuse_step.argtypes = [_P, _P, _i32, _i32, _P, _i64, _f32, _P, _P, _P, _P, _P]
 _lib.cosine_fuse_step.restype = ctypes.c_int
+_lib.cosine_route_update.argtypes = [_P, _P, _i32, _i32, _i32, _P, _P, _P, _i64, _P, _P, _i64, _i64, ctypes.c_int,
+                                     _P, _f32, _P, _P, _P]
+_lib.cosine_route_update.restype = ctypes.c_int
 _lib.cosine_verify_tree_lazy.restype = ctypes.c_int
 _lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
 _lib.cosine_nccl_unique_id.restype = ctypes.c_int
@@ -91,7 +94,8 @@ EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_
                     "cosine_fuse_drafts", "cosine_verify_batch", "cosine_sample_residual",
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
                     "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
-                    "cosine_verify_tree_lazy", "cosine_fuse_step")
+                    "cosine_verify_tree_lazy", "cosine_fuse_step",
+                    "cosine_route_update")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -269,4 +273,17 @@ def cosine_fuse_step(ctx, logits, own_tokens, conf, fused_token, winner, status,
     B, N, ld = logits.shape
     rc = _lib.cosine_fuse_step(ctx, _stream(stream, logits.device), B, N, _ptr(logits), ld, temperature,
                                _ptr(own_tokens), _ptr(conf), _ptr(fused_token), _ptr(winner), _ptr(status))
+    _check(rc, ctx)
+
+
+def cosine_route_update(ctx, draft_tokens, conf, accepted, accept_len, emb, M, status, *, participating=None,
+                        decay=0.9, d_out=None, stream=None):
+    """Routing feedback (NEXT-3): draft_tokens / conf [B][N][K], accepted [B][>=K], accept_len [B],
+    emb [V][H] (bf16 / fp32), M [B][N] fp32 updated in place, status [B]."""
+    B, N, K = draft_tokens.shape
+    H = emb.shape[1]
+    rc = _lib.cosine_route_update(ctx, _stream(stream, M.device), B, N, K, _ptr(draft_tokens), _ptr(conf),
+                                  _ptr(accepted), accepted.shape[1], _ptr(accept_len), _ptr(emb), H,
+                                  emb.stride(0), _DT[emb.dtype], _ptr(participating), decay, _ptr(M),
+                                  _ptr(d_out), _ptr(status))
     _check(rc, ctx)

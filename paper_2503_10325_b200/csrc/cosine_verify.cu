@@ -1073,6 +1073,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
 #include "cosine_tree.cuh"
 #include "cosine_shard.cuh"
 #include "cosine_fuse_step.cuh"
+#include "cosine_route.cuh"
 namespace cosine {
 
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
@@ -2148,6 +2149,46 @@ cosine_status_t cosine_fuse_step(cosine_ctx_t ctx, cosine_stream_t stream, int32
     return fail(ctx, COSINE_ERR_CUDA, std::string("fuse_step kernels: ") + cudaGetErrorString(e));
   }
   ctx->last_launches = 2;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_route_update(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t N, int32_t K,
+                                    const int32_t* draft_tokens, const float* conf, const int32_t* accepted,
+                                    int64_t acc_stride, const int32_t* accept_len, const void* emb,
+                                    int64_t hidden, int64_t ld_e, cosine_dtype_t emb_dtype,
+                                    const uint8_t* participating, float decay, float* M, float* d_out,
+                                    int32_t* status) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  if (B < 0 || B > ctx->cfg.max_batch) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "B outside [0, max_batch]");
+  if (N < 1 || N > kWarps * 4 || K < 1 || acc_stride < K)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad N / K / acc_stride");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if (!draft_tokens || !conf || !accepted || !accept_len || !emb || !M || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (emb_dtype != COSINE_BF16 && emb_dtype != COSINE_F32)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "embedding dtype must be COSINE_BF16 or COSINE_F32");
+  if (hidden < 8 || hidden % 8 != 0 || ld_e < hidden || !aligned16(emb) || ((uint64_t)ld_e * esize(emb_dtype)) % 16 != 0)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "embedding rows: hidden % 8 == 0, 16-byte aligned rows");
+  if (!(decay >= 0.f && decay <= 1.f)) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "decay outside [0, 1]");
+  DeviceGuard dg(ctx->cfg.device);
+  RouteParams R;
+  memset(&R, 0, sizeof(R));
+  R.B = B; R.N = N; R.K = K; R.V = ctx->cfg.vocab_size; R.Hd = hidden; R.ld_e = ld_e; R.acc_stride = acc_stride;
+  R.draft_tokens = draft_tokens; R.conf = conf; R.accepted = accepted; R.accept_len = accept_len; R.emb = emb;
+  R.participating = participating; R.decay = decay; R.eps = 1e-6f; R.M = M; R.d_out = d_out; R.status = status;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.gridDim = dim3((unsigned)B, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  cudaError_t e = (emb_dtype == COSINE_BF16) ? cudaLaunchKernelEx(&lc, route_update_kernel<__nv_bfloat16>, R)
+                                             : cudaLaunchKernelEx(&lc, route_update_kernel<float>, R);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("route_update: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 1;
   return COSINE_OK;
 }
 
