@@ -792,3 +792,82 @@ int orc_route_update(int32_t B, int32_t N, int32_t K, int64_t V, int64_t Hd, con
   }
   return 0;
 }
+
+/* TreeSelection (NEXT-4, reading #25), step by step: trie insertion, node scores, top-budget
+ * pruning, breadth-first renumbering. */
+int orc_tree_select(int32_t B, int32_t S, int32_t K, const int32_t* tokens, const double* conf, int32_t budget,
+                    int32_t* n_nodes, int32_t* parent, int32_t* token, double* score, int32_t* depth) {
+  if (B < 0 || S < 1 || K < 1 || budget < 0 || S * K > 4096) return 1;
+  const int cap = S * K + 1;
+  int32_t* tp = (int32_t*)malloc(sizeof(int32_t) * cap); /* trie: parent, token, depth, score */
+  int32_t* tt = (int32_t*)malloc(sizeof(int32_t) * cap);
+  int32_t* td = (int32_t*)malloc(sizeof(int32_t) * cap);
+  double* ts = (double*)malloc(sizeof(double) * cap);
+  int32_t* keep = (int32_t*)malloc(sizeof(int32_t) * cap);
+  int32_t* newid = (int32_t*)malloc(sizeof(int32_t) * cap);
+  if (!tp || !tt || !td || !ts || !keep || !newid) return 1;
+  for (int32_t b = 0; b < B; ++b) {
+    int n = 1;
+    tp[0] = -1; tt[0] = -1; td[0] = 0; ts[0] = 1.0;
+    for (int32_t s2 = 0; s2 < S; ++s2) { /* 1. merge the branches into a prefix tree */
+      int cur = 0;
+      double prod = 1.0;
+      for (int32_t i = 0; i < K; ++i) {
+        const int32_t x = tokens[((int64_t)b * S + s2) * K + i];
+        if (x < 0) break;
+        prod *= conf[((int64_t)b * S + s2) * K + i];
+        int child = -1;
+        for (int c = 1; c < n; ++c)
+          if (tp[c] == cur && tt[c] == x) { child = c; break; }
+        if (child < 0) { child = n++; tp[child] = cur; tt[child] = x; td[child] = td[cur] + 1; ts[child] = prod; }
+        else if (prod > ts[child]) ts[child] = prod; /* 2. the best branch product reaching it */
+        cur = child;
+      }
+    }
+    /* 3. keep the budget best non-root nodes: score desc, depth asc, creation order */
+    for (int c = 0; c < n; ++c) keep[c] = (c == 0);
+    const int nk = (n - 1 < budget) ? n - 1 : budget;
+    for (int r = 0; r < nk; ++r) {
+      int best = -1;
+      for (int c = 1; c < n; ++c) {
+        if (keep[c]) continue;
+        if (best < 0 || ts[c] > ts[best] || (ts[c] == ts[best] && (td[c] < td[best] || (td[c] == td[best] && c < best))))
+          best = c;
+      }
+      keep[best] = 1;
+    }
+    /* 4. breadth-first renumbering; siblings by (score desc, creation) */
+    for (int c = 0; c < n; ++c) newid[c] = -1;
+    newid[0] = 0;
+    int next = 1;
+    for (int d = 1; d <= K; ++d) {
+      for (int p = 0; p < next; ++p) { /* parents in their new order */
+        int old_p = -1;
+        for (int c = 0; c < n; ++c)
+          if (newid[c] == p) { old_p = c; break; }
+        for (;;) { /* the best remaining kept child of old_p at depth d */
+          int best = -1;
+          for (int c = 1; c < n; ++c) {
+            if (!keep[c] || newid[c] >= 0 || tp[c] != old_p || td[c] != d) continue;
+            if (best < 0 || ts[c] > ts[best] || (ts[c] == ts[best] && c < best)) best = c;
+          }
+          if (best < 0) break;
+          newid[best] = next++;
+        }
+      }
+    }
+    const int64_t o = (int64_t)b * (budget + 1);
+    for (int j = 0; j <= budget; ++j) { parent[o + j] = -1; token[o + j] = -1; score[o + j] = 0.0; depth[o + j] = -1; }
+    for (int c = 0; c < n; ++c) {
+      if (!keep[c]) continue;
+      const int j = newid[c];
+      parent[o + j] = (c == 0) ? -1 : newid[tp[c]];
+      token[o + j] = tt[c];
+      score[o + j] = ts[c];
+      depth[o + j] = td[c];
+    }
+    n_nodes[b] = next;
+  }
+  free(tp); free(tt); free(td); free(ts); free(keep); free(newid);
+  return 0;
+}

@@ -129,6 +129,18 @@ int orc_route_update(int32_t B, int32_t N, int32_t K, int64_t V, int64_t Hd, con
                      const double* emb, const uint8_t* participating, double decay, double eps, double* M,
                      double* d_out, int32_t* status);
 
+/* TreeSelection (Alg. 1 "TreeSelection" P:372, not defined by the paper —
+ * SPEC S:303-311's construction, reading #25).  Per request: S branches (each node's own
+ * and fused branch) of K tokens with confidences are merged into a prefix tree rooted at the last
+ * verified token (node 0); a node's score is the largest product of confidences along any branch
+ * reaching it; the `budget` best non-root nodes are kept (score desc, then depth asc, then creation
+ * order), which is prefix-closed; the kept nodes are renumbered breadth-first with siblings in
+ * (score desc, creation) order, so parent[j] < j and children are in slot order.
+ * Outputs [B][budget + 1]: parent (-1 root / padding), token (-1 root / padding), score, depth;
+ * n_nodes[B] = kept + 1.  tokens < 0 end a branch.  Returns 0 / 1 (bad argument). */
+int orc_tree_select(int32_t B, int32_t S, int32_t K, const int32_t* tokens, const double* conf, int32_t budget,
+                    int32_t* n_nodes, int32_t* parent, int32_t* token, double* score, int32_t* depth);
+
 #ifdef __cplusplus
 }
 #endif

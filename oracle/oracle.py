@@ -24,7 +24,7 @@ INFO_DEGENERATE = 0x100
 
 __all__ = [
     "build", "lib", "philox4x32_10", "uniform", "invcdf", "softmax", "residual",
-    "verify_batch", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step", "route_update",
+    "verify_batch", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step", "route_update", "tree_select",
     "TAG_ACCEPT", "TAG_SAMPLE", "TAG_FUSE", "TAG_TREE_GEN",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE",
     "DRAFT_PROBS", "DRAFT_LOGITS", "ST_OK", "ST_ZERO_PROB", "ST_TOKEN_RANGE",
@@ -73,6 +73,7 @@ def lib():
         L.orc_verify_tree.argtypes = [_i32, _i32, _i32, _i32, _i64, _P, _P, _P, _P, _f64, _P, _i32,
                                       _P, _P, _u64, _u32, _i32, _P, _P, _P, _P, _P]
         L.orc_fuse_step.argtypes = [_i32, _i32, _i64, _P, _f64, _P, _P, _P, _P, _P, _P]
+        L.orc_tree_select.argtypes = [_i32, _i32, _i32, _P, _P, _i32, _P, _P, _P, _P, _P]
         L.orc_route_update.argtypes = [_i32, _i32, _i32, _i64, _i64, _P, _P, _P, _i64, _P, _P, _P, _f64, _f64,
                                        _P, _P, _P]
         _lib = L
@@ -280,3 +281,18 @@ def route_update(draft_tokens, conf, accepted, accept_len, emb, M, *, participat
     if rc != 0:
         raise ValueError("oracle route_update: invalid argument")
     return dict(M=Mo, d=d, status=st)
+
+
+def tree_select(tokens, conf, budget):
+    """TreeSelection (NEXT-4): tokens / conf [B][S][K] -> dict(n_nodes, parent, token, score, depth)."""
+    X = _arr(tokens, np.int32)
+    C = _f64arr(conf)
+    B, S, K = X.shape
+    out = dict(n_nodes=np.zeros(B, np.int32), parent=np.zeros((B, budget + 1), np.int32),
+               token=np.zeros((B, budget + 1), np.int32), score=np.zeros((B, budget + 1)),
+               depth=np.zeros((B, budget + 1), np.int32))
+    rc = lib().orc_tree_select(B, S, K, _ptr(X), _ptr(C), int(budget), _ptr(out["n_nodes"]), _ptr(out["parent"]),
+                               _ptr(out["token"]), _ptr(out["score"]), _ptr(out["depth"]))
+    if rc != 0:
+        raise ValueError("oracle tree_select: invalid argument")
+    return out

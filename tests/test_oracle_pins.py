@@ -576,3 +576,46 @@ def test_route_update_eq1_cases_and_decay():
     # a token outside [0, V): status 2, M unchanged
     bad = oracle.route_update(np.array([[[1, 2, 3, 99], [5, 6, 7, 0]]], np.int32), c, acc, [4], E, M)
     assert bad["status"][0] == 2 and (bad["M"] == M).all()
+
+
+# ---------------- TreeSelection (NEXT-4) ----------------
+def test_tree_select_spec_examples():
+    # one branch, budget >= K -> a single chain; two branches diverging at step 1 ->
+    # branching factor 2 under the root; budget = 1 -> the single most confident first token
+    r = oracle.tree_select([[[5, 6, 7]]], [[[0.9, 0.8, 0.7]]], budget=5)
+    assert r["n_nodes"][0] == 4 and list(r["parent"][0, :4]) == [-1, 0, 1, 2] and list(r["token"][0, 1:4]) == [5, 6, 7]
+    r = oracle.tree_select([[[5, 6], [9, 6]]], [[[0.6, 0.9], [0.8, 0.9]]], budget=4)
+    assert list(r["parent"][0, :5]) == [-1, 0, 0, 1, 2] and list(r["token"][0, 1:3]) == [9, 5]  # siblings by score
+    r = oracle.tree_select([[[5, 6], [9, 6]]], [[[0.6, 0.9], [0.8, 0.9]]], budget=1)
+    assert r["n_nodes"][0] == 2 and r["token"][0, 1] == 9
+
+
+def _closed_best(par, sc, budget):
+    # brute force: the largest total score of a prefix-closed set of `budget` non-root nodes
+    import itertools
+    n = len(par)
+    best = -1.0
+    for sub in itertools.combinations(range(1, n), min(budget, n - 1)):
+        s = set(sub) | {0}
+        if all(par[c] in s for c in sub):
+            best = max(best, sum(sc[c] for c in sub))
+    return best
+
+
+def test_tree_select_is_the_best_prefix_closed_set():
+    rng = np.random.default_rng(8)
+    for trial in range(40):
+        S, K = 3, 3
+        X = rng.integers(0, 3, size=(1, S, K)).astype(np.int32)
+        C = rng.uniform(0.05, 1.0, size=(1, S, K))
+        full = oracle.tree_select(X, C, budget=S * K)
+        n = int(full["n_nodes"][0])
+        par, sc = full["parent"][0, :n], full["score"][0, :n]
+        assert all(par[j] < j for j in range(1, n))                  # BFS numbering, parent first
+        assert all(sc[j] <= sc[par[j]] + 1e-15 for j in range(1, n))  # scores fall along paths
+        for budget in (1, 2, 4):
+            r = oracle.tree_select(X, C, budget=budget)
+            m = int(r["n_nodes"][0])
+            assert m - 1 == min(budget, n - 1)
+            assert all(r["parent"][0, j] < j for j in range(1, m))
+            assert abs(r["score"][0, 1:m].sum() - _closed_best(par, sc, budget)) < 1e-12
