@@ -241,6 +241,22 @@ cosine_status_t cosine_route_update(cosine_ctx_t ctx, cosine_stream_t stream, in
                                     int32_t* status);
 
 /*
+ * cosine_tree_select — TreeSelection (Alg. 1 "TreeSelection" P:372; the paper
+ * does not define it: SPEC S:303-311's construction, reading #25).  Per request, S branch
+ * sequences (each drafter's own and fused branch) of K tokens with their confidences:
+ *   tokens [B][S][K] int32 (< 0 ends a branch), conf [B][S][K] fp32, budget = non-root nodes kept.
+ * The branches are merged into a prefix tree rooted at the last verified token (node 0); a node's
+ * score is the largest product of confidences along a branch reaching it; the `budget` best nodes
+ * (score desc, depth asc, creation order) are kept — a prefix-closed set — and renumbered
+ * breadth-first with siblings by (score desc, creation), ready for cosine_verify_tree.
+ * Outputs [B][budget + 1]: parent (-1 root / padding), token (-1 root / padding), score, depth;
+ * n_nodes [B] = kept + 1.  S * K + 1 <= 1024.  One launch (CTA per request).
+ */
+cosine_status_t cosine_tree_select(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t S, int32_t K,
+                                   const int32_t* tokens, const float* conf, int32_t budget, int32_t* n_nodes,
+                                   int32_t* parent, int32_t* token, float* score, int32_t* depth);
+
+/*
  * cosine_sample_residual — the final-token sample of one row group per request,
  * for callers that verify elsewhere.
  *   target_rows [B][ld_t] logits of the row at L_b;  temperature (0 = argmax)

@@ -14,7 +14,7 @@ from ._lib import (  # noqa: F401
     BF16, F32, DRAFT_LOGITS, DRAFT_PROBS, INFO_DEGENERATE, INFO_NEAR_TIE, SEL_ARGMAX, SEL_SAMPLE,
     W_CONF, W_POINT, W_UNIFORM, W_WINNER, Context, CosineError, cosine_fuse_drafts,
     cosine_last_launch_count, cosine_profile_enable, cosine_profile_read, cosine_sample_residual,
-    cosine_fuse_step, cosine_nccl_unique_id, cosine_route_update, cosine_verify_batch, cosine_verify_batch_lazy,
+    cosine_fuse_step, cosine_nccl_unique_id, cosine_route_update, cosine_tree_select, cosine_verify_batch, cosine_verify_batch_lazy,
     cosine_verify_destroy,
     cosine_verify_init,
     cosine_verify_tree,
@@ -24,7 +24,7 @@ __all__ = [
     "Verifier", "cosine_verify_init", "cosine_verify_destroy", "cosine_fuse_drafts",
     "cosine_verify_batch", "cosine_sample_residual", "cosine_verify_tree", "cosine_last_launch_count",
     "cosine_nccl_unique_id", "cosine_verify_batch_lazy", "cosine_fuse_step",
-    "cosine_route_update",
+    "cosine_route_update", "cosine_tree_select",
     "CosineError",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE", "DRAFT_PROBS",
     "DRAFT_LOGITS",

@@ -82,6 +82,8 @@ _lib.cosine_fuse_step.restype = ctypes.c_int
 _lib.cosine_route_update.argtypes = [_P, _P, _i32, _i32, _i32, _P, _P, _P, _i64, _P, _P, _i64, _i64, ctypes.c_int,
                                      _P, _f32, _P, _P, _P]
 _lib.cosine_route_update.restype = ctypes.c_int
+_lib.cosine_tree_select.argtypes = [_P, _P, _i32, _i32, _i32, _P, _P, _i32, _P, _P, _P, _P, _P]
+_lib.cosine_tree_select.restype = ctypes.c_int
 _lib.cosine_verify_tree_lazy.restype = ctypes.c_int
 _lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
 _lib.cosine_nccl_unique_id.restype = ctypes.c_int
@@ -95,7 +97,7 @@ EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
                     "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
                     "cosine_verify_tree_lazy", "cosine_fuse_step",
-                    "cosine_route_update")
+                    "cosine_route_update", "cosine_tree_select")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -286,4 +288,13 @@ def cosine_route_update(ctx, draft_tokens, conf, accepted, accept_len, emb, M, s
                                   _ptr(accepted), accepted.shape[1], _ptr(accept_len), _ptr(emb), H,
                                   emb.stride(0), _DT[emb.dtype], _ptr(participating), decay, _ptr(M),
                                   _ptr(d_out), _ptr(status))
+    _check(rc, ctx)
+
+
+def cosine_tree_select(ctx, tokens, conf, budget, n_nodes, parent, token, score, depth, *, stream=None):
+    """TreeSelection (NEXT-4): tokens / conf [B][S][K] -> n_nodes [B], parent / token / score / depth
+    [B][budget + 1] (breadth-first numbering, ready for cosine_verify_tree)."""
+    B, S, K = tokens.shape
+    rc = _lib.cosine_tree_select(ctx, _stream(stream, tokens.device), B, S, K, _ptr(tokens), _ptr(conf), budget,
+                                 _ptr(n_nodes), _ptr(parent), _ptr(token), _ptr(score), _ptr(depth))
     _check(rc, ctx)

@@ -1074,6 +1074,7 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 ? 4 : 2)) unit_kernel(con
 #include "cosine_shard.cuh"
 #include "cosine_fuse_step.cuh"
 #include "cosine_route.cuh"
+#include "cosine_tree_select.cuh"
 namespace cosine {
 
 __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
@@ -2187,6 +2188,35 @@ cosine_status_t cosine_route_update(cosine_ctx_t ctx, cosine_stream_t stream, in
     cudaGetLastError();
     ctx->last_launches = 0;
     return fail(ctx, COSINE_ERR_CUDA, std::string("route_update: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 1;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_tree_select(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t S, int32_t K,
+                                   const int32_t* tokens, const float* conf, int32_t budget, int32_t* n_nodes,
+                                   int32_t* parent, int32_t* token, float* score, int32_t* depth) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  if (B < 0 || S < 1 || K < 1 || budget < 0 || (int64_t)S * K + 1 > kSelMaxNodes)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad B / S / K / budget (S * K + 1 <= 1024)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if (!tokens || !conf || !n_nodes || !parent || !token || !score || !depth)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  DeviceGuard dg(ctx->cfg.device);
+  TreeSelParams T;
+  memset(&T, 0, sizeof(T));
+  T.B = B; T.S = S; T.K = K; T.budget = budget; T.tokens = tokens; T.conf = conf;
+  T.n_nodes = n_nodes; T.parent = parent; T.token = token; T.score = score; T.depth = depth;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.gridDim = dim3((unsigned)B, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  const cudaError_t e = cudaLaunchKernelEx(&lc, tree_select_kernel, T);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("tree_select: ") + cudaGetErrorString(e));
   }
   ctx->last_launches = 1;
   return COSINE_OK;
