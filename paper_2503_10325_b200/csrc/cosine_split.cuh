@@ -67,6 +67,7 @@ struct SplitParams {
   double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
   int64_t nseg;
   int spr;         // B2a CTAs per request
+  int tpc;         // tiles per B2 CTA (<= kSegTilesPerCta)
   int b_off, nb;   // this launch covers requests [b_off, b_off + nb) (batch pipelining)
   // tree mode (cosine_verify_tree): a unit is a node (b, j); rows via internal_row
   int tree, nn, I;           // nodes per request (J + 1), internal (drafter) rows per request
@@ -794,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
   const int part = blockIdx.x % P.spr;
-  const int64_t tile0 = (int64_t)part * kSegTilesPerCta;
+  const int64_t tile0 = (int64_t)part * P.tpc;
   __shared__ __align__(16) PosDec s_pd[kMaxPos];
   __shared__ ReqView s_v;
   __shared__ Decision s_d;
@@ -880,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   const bool need_q = (kind0 == kWResidual);
   const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
   const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
-  const int ntiles = (int)min((int64_t)kSegTilesPerCta, P.nseg - tile0);
+  const int ntiles = (int)min((int64_t)P.tpc, P.nseg - tile0);
 #pragma unroll 1
   for (int j = 0; j < ntiles; ++j) {  // one tile of (1+N) loads per thread in flight
     const int64_t g0 = (tile0 + j) * kTileGroups + tid;

@@ -1263,6 +1263,13 @@ cosine_status_t launch(cosine_ctx_t ctx, cudaStream_t stream, Params& P, int64_t
 
 // Kernel A (stats + decisions) then kernel B (first rejection + cooperative sample), the
 // latter launched with programmatic dependent launch so its launch overlaps A's tail.
+// Tiles (256 groups) per resample CTA: fewer -> more, shorter CTAs (less wave tail).
+int resample_tiles_per_cta() {
+  int t = 8;
+  if (const char* v = getenv("COSINE_TPC")) t = atoi(v);
+  return std::max(1, std::min(kSegTilesPerCta, t));
+}
+
 cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S,
                              cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
   SplitFn fn[3];
@@ -1279,7 +1286,8 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   S.C = C;
   S.cg = (S.ngroups + C - 1) / C;
   S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
-  S.spr = (int)((S.nseg + kSegTilesPerCta - 1) / kSegTilesPerCta);
+  S.tpc = resample_tiles_per_cta();
+  S.spr = (int)((S.nseg + S.tpc - 1) / S.tpc);
   S.parts = ctx->parts;
   S.pdec = ctx->pdec;
   S.segsum = ctx->segsum;
@@ -1422,7 +1430,8 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   S.C = C;
   S.cg = (S.ngroups + C - 1) / C;
   S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
-  S.spr = (int)((S.nseg + kSegTilesPerCta - 1) / kSegTilesPerCta);
+  S.tpc = resample_tiles_per_cta();
+  S.spr = (int)((S.nseg + S.tpc - 1) / S.tpc);
   S.parts = ctx->parts;
   S.pdec = ctx->pdec;
   S.segsum = ctx->segsum;
@@ -1534,7 +1543,8 @@ cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& 
   S.C = C;
   S.cg = (S.ngroups + C - 1) / C;
   S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
-  S.spr = (int)((S.nseg + kSegTilesPerCta - 1) / kSegTilesPerCta);
+  S.tpc = resample_tiles_per_cta();
+  S.spr = (int)((S.nseg + S.tpc - 1) / S.tpc);
   S.parts = ctx->parts;
   S.pdec = ctx->pdec;
   S.segsum = ctx->segsum;

@@ -1,0 +1,4 @@
+#!/bin/bash
+run() { timeout 300 env "$@" python bench.py --steps 30 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print('$*', round(d['value']), round(d['ms_per_step']*1000,1))"; }
+for t in 8 4 2; do run COSINE_TPC=$t; done
+for t in 8 4; do run COSINE_TPC=$t; done
