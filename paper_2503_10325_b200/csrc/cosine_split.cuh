@@ -612,8 +612,7 @@ __global__ void __launch_bounds__(kThreads) lazy_decide_kernel(const SplitParams
   const int b = blockIdx.x * kWarps + warp;
   __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
   __shared__ int32_t s_tok[kWarps][kMaxN];
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // this round's partial records (PDL)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!P.fused) asm volatile("griddepcontrol.wait;" ::: "memory");  // this round's records (PDL)
   if (b >= P.B) return;
   const int r0 = P.lazy - 1;
   const int g = P.draft_len ? P.draft_len[b] : P.k;
@@ -621,8 +620,24 @@ __global__ void __launch_bounds__(kThreads) lazy_decide_kernel(const SplitParams
   if (r0 > 0 && P.lz[b] != 0) return;
   PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
   const int r1 = min(g, r0 + P.lazy_span - 1);
+  // fused: wait for each position's C chunk records (device counters; every stats CTA of the
+  // round is resident or done once this CTA runs), consume and reset every counted position
+  auto wait_unit = [&](int r) {
+    if (!P.fused) return;
+    if (lane == 0) {
+      const int32_t* cnt = P.ucnt + (int64_t)b * (P.k + 1) + r;
+      uint32_t n;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(cnt) : "memory");
+        if ((int)n >= P.C) break;
+        __nanosleep(100);
+      }
+    }
+    __syncwarp();
+  };
   bool stop = false;
   for (int r = r0; r <= r1 && !stop; ++r) {  // the round's positions in order
+    wait_unit(r);
     warp_decide<TT, TQ, kLogits>(P, b, r, g, s_gx[warp], s_tok[warp], &pds[r], true);
     __syncwarp();
     int st = 0;
@@ -636,6 +651,11 @@ __global__ void __launch_bounds__(kThreads) lazy_decide_kernel(const SplitParams
       }
     }
     stop = __shfl_sync(0xffffffffu, st, 0) != 0;
+  }
+  if (P.fused) {  // the round's streamed positions: all counted -> reset for the next round / call
+    for (int r = r0; r <= r1; ++r) wait_unit(r);
+    if (lane == 0)
+      for (int r = r0; r <= r1; ++r) P.ucnt[(int64_t)b * (P.k + 1) + r] = 0;
   }
   if (lane == 0) P.lz[b] = stop ? -1 : 0;
 }

@@ -1570,6 +1570,12 @@ cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& 
   if (const char* v = getenv("COSINE_LAZY_C")) C1 = std::max(1, std::min(kMaxC, atoi(v)));
   if (const char* v = getenv("COSINE_LAZY_SPAN")) span = std::max(1, std::min(S.k + 1, atoi(v)));
   S.lazy_span = span;
+  // per-unit counters: each round's decide kernel is scheduled into the stats tail (PDL) and
+  // waits per position (COSINE_LAZY_FUSED=0: whole-grid waits)
+  S.fused = 1;
+  if (const char* v = getenv("COSINE_LAZY_FUSED")) S.fused = atoi(v) != 0;
+  S.dcnt = ctx->counters + std::max(ctx->cfg.max_batch, 1);
+  S.ucnt = ctx->counters + 2 * (size_t)std::max(ctx->cfg.max_batch, 1);
   for (int r = 0; r <= S.k && e == cudaSuccess; r += span) {
     S.lazy = r + 1;
     S.C = (r == 0) ? C : C1;
@@ -1587,6 +1593,7 @@ cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& 
     launches += 2;
   }
   S.lazy = 0;
+  S.fused = 0;  // the final draws wait for the last round's grid (griddepcontrol.wait)
   if (e == cudaSuccess) {
     lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
     lc.attrs = at;
