@@ -1576,11 +1576,14 @@ cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& 
   if (const char* v = getenv("COSINE_LAZY_FUSED")) S.fused = atoi(v) != 0;
   S.dcnt = ctx->counters + std::max(ctx->cfg.max_batch, 1);
   S.ucnt = ctx->counters + 2 * (size_t)std::max(ctx->cfg.max_batch, 1);
-  for (int r = 0; r <= S.k && e == cudaSuccess; r += span) {
+  int span0 = span;  // the first round's span (COSINE_LAZY_SPAN0)
+  if (const char* v = getenv("COSINE_LAZY_SPAN0")) span0 = std::max(1, std::min(S.k + 1, atoi(v)));
+  for (int r = 0; r <= S.k && e == cudaSuccess; r += S.lazy_span) {
+    S.lazy_span = (r == 0) ? span0 : span;
     S.lazy = r + 1;
     S.C = (r == 0) ? C : C1;
     S.cg = (S.ngroups + S.C - 1) / S.C;
-    lc.gridDim = dim3((unsigned)((int64_t)S.B * span * S.C), 1, 1);
+    lc.gridDim = dim3((unsigned)((int64_t)S.B * S.lazy_span * S.C), 1, 1);
     lc.attrs = nullptr;  // stream order: the round reads the previous round's lz
     lc.numAttrs = 0;
     e = cudaLaunchKernelEx(&lc, fn[0], S);
