@@ -6,19 +6,24 @@
 One "step" = one cosine_verify_batch call over one batch of synthetic inputs already
 resident in HBM (all of SURVEY §8(a): target softmax stats, drafter normalisers,
 Eq. 4 fusion, acceptance, first rejection, residual / bonus resample).  For N > 1
-(torchrun, one process per GPU) every rank verifies its own batch of the same
-shape with distinct global request ids: weak scaling, no data-path collective
-(requests are independent, Alg. 2).  Prints ONE JSON line on rank 0.
+(one process per GPU; `--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset) every rank verifies its own batch of the same shape with distinct
+global request ids: weak scaling, no data-path collective (requests are independent,
+Alg. 2).  c5 is the vocabulary-sharded call (strong scaling).  Prints ONE JSON
+line on rank 0.
 
 `--impl reference` times the CPU oracle (oracle/, fp64 C) on the host cores as the
-reference arm: each step verifies a bounded sample (one request) of the workload.
+reference arm: each step verifies a bounded sample of the workload's requests, one
+request slice per host thread.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -29,14 +34,17 @@ sys.path.insert(0, ROOT)
 METRIC = "verified draft tokens/sec and HBM GB/s vs 8 TB/s at 1/2/4/8 B200"
 UNIT = "verified draft tokens/s"
 WORKLOADS = {
-    "c1": "c1: batch=1, 2 drafters, k=4, vocab=32000, fp32 logits/probs, CONF fusion, T=1",
-    "c2": "c2: batch=64, 3 drafters, k=8, vocab=32000 (Llama-2), bf16 logits/probs, CONF fusion, T=1",
-    "c3": "c3: batch=256, 4 drafters, k=8, vocab=128256 (Llama-3), bf16 logits/probs, CONF fusion, T=1",
+    "c1": "c1: batch=1, 2 drafters, k=4, vocab=32000, fp32 logits/probs, T=1",
+    "c2": "c2: batch=64, 3 drafters, k=8, vocab=32000 (Llama-2), bf16 logits/probs, T=1",
+    "c3": "c3: batch=256, 4 drafters, k=8, vocab=128256 (Llama-3), bf16 logits/probs, T=1",
     "c4": "c4: tree-shaped drafts, 64-node tree per request (schedule 4,2,2,1,1,1,1,1), batch=128, "
-          "4 drafters, vocab=128256, bf16, CONF fusion, T=1",
+          "4 drafters, vocab=128256, bf16, T=1",
     "c5": "c5: batch=1024, 4 drafters, k=8, vocab=128256 (Llama-3) split in N column shards (tensor-parallel "
-          "LM head layout), bf16, CONF fusion, T=1, vocabulary-sharded verification over NCCL",
+          "LM head layout), bf16, T=1, vocabulary-sharded verification over NCCL",
 }
+WEIGHTS = {"conf": 0, "winner": 1, "uniform": 2, "point": 3}
+SELECTS = {"argmax": 0, "sample": 1}
+L2_BYTES = 126 * 2**20
 
 
 def parse():
@@ -46,15 +54,51 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--weights", default="conf", choices=sorted(WEIGHTS),
+                    help="fusion weights (Eq. 4 CONF default; reading #2)")
+    ap.add_argument("--select", default="argmax", choices=sorted(SELECTS),
+                    help="argmax = Eq. 4 fused token (paper-literal); sample = x* ~ fused q (reading #3)")
     ap.add_argument("--cluster-size", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0 = all host cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--flush", default="auto", choices=["auto", "on", "off"],
+                    help="flush L2 between timed calls (auto: when the inputs are < 4x L2)")
+    ap.add_argument("--traffic", default="auto", choices=["auto", "off"],
+                    help="auto: measure the kernel's DRAM bytes with an ncu child run (N = 1 only)")
     ap.add_argument("--lazy", action="store_true",
                     help="early-exit verification (cosine_verify_batch_lazy, SURVEY 8(f) NEXT-1)")
     ap.add_argument("--seed", type=int, default=1234)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.lazy and a.config == "c5":
+        ap.error("--lazy runs on unsharded contexts (c1..c4)")
+    if a.config in ("c4", "c5") and a.select != "argmax":
+        ap.error("tree / vocabulary-sharded verification takes ARGMAX selection")
+    if a.lazy and a.select != "argmax":
+        ap.error("lazy verification takes ARGMAX selection")
+    return a
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run, one rank
+    per GPU; inside torchrun: the world size must equal --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if int(world or 1) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
 
 def peaks():
@@ -116,35 +160,32 @@ class ClockSampler(threading.Thread):
 
 
 def cfg_of(name):
-    from paper_2503_10325_b200 import synth
-    c = dict(synth.CONFIGS[name])
-    return c
+    import synth
+    return dict(synth.CONFIGS[name])
+
+
+def cpu_threads(args):
+    return args.cpu_threads if args.cpu_threads > 0 else (os.cpu_count() or 1)
 
 
 # --------------------------------------------------------------------------------------
-def cpu_oracle_rate(host_inputs, k, N, V, budget_s, seed):
-    """Time the CPU oracle (as it stands, single-threaded) on whole requests of the workload
-    until ~budget_s seconds of CPU work; returns (tokens/s, requests, seconds)."""
-    import numpy as np
+def cpu_oracle_rate(host_inputs, k, V, budget_s, seed, threads, wm=0, sm=0):
+    """The CPU oracle as it stands, on `threads` host threads (one request slice each, GIL
+    released in the C code), on rounds of `threads` whole requests of the workload until
+    ~budget_s seconds; returns (tokens/s, requests, seconds)."""
     import oracle
-    t = host_inputs["target"]
-    d = host_inputs["draft"]
-    X = host_inputs["draft_tokens"]
-    rid = host_inputs["request_ids"]
-    done_req, tok, spent = 0, 0, 0.0
-    B = t.shape[0]
+    B = host_inputs["target"].shape[0]
+    done_req, spent = 0, 0.0
     while spent < budget_s and done_req < B:
-        b = done_req
-        tt = t[b:b + 1, :, :V].double().numpy()
-        dd = d[b:b + 1, :, :, :V].double().numpy()
-        xx = X[b:b + 1].numpy()
-        rr = rid[b:b + 1].numpy().astype(np.uint64)
+        b0, b1 = done_req, min(B, done_req + threads)
         t0 = time.perf_counter()
-        oracle.verify_batch(tt, dd, xx, rr, temperature=1.0, seed=seed)
+        oracle.verify_batch_parallel(host_inputs["target"][b0:b1], host_inputs["draft"][b0:b1],
+                                     host_inputs["draft_tokens"][b0:b1], host_inputs["request_ids"][b0:b1],
+                                     threads=threads, temperature=1.0, seed=seed, vocab=V, weight_mode=wm,
+                                     select_mode=sm)
         spent += time.perf_counter() - t0
-        done_req += 1
-        tok += k
-    return tok / spent, done_req, spent
+        done_req = b1
+    return done_req * k / spent, done_req, spent
 
 
 def run_reference(args):
@@ -152,39 +193,76 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from paper_2503_10325_b200 import synth
+    import synth
     import oracle
-    import numpy as np
     c = cfg_of(args.config)
     B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
+    threads = cpu_threads(args)
     steps, warm = args.steps, args.warmup
-    nreq = min(B, steps + warm, 16)  # a bounded sample, cycled
+    per = min(B, threads)  # requests per step: one per thread (a bounded sample of the batch)
+    # bound the whole run to a few minutes of host time (~30 ms per c3-sized request and thread)
+    est = 0.03 * (V / 128256) * (k + 1 + k * N) / 41 * (warm + steps)
+    if est > 150:
+        steps = max(3, int(steps * 150 / est))
+    nreq = min(B, per * 4)
     inp = synth.linear_inputs(nreq, k, N, V, dtype=dt, seed=args.seed, device="cpu", chunk=4)
     times = []
     for s in range(warm + steps):
-        b = s % nreq
-        tt = inp["target"][b:b + 1, :, :V].double().numpy()
-        dd = inp["draft"][b:b + 1, :, :, :V].double().numpy()
-        xx = inp["draft_tokens"][b:b + 1].numpy()
-        rr = inp["request_ids"][b:b + 1].numpy().astype(np.uint64)
+        b0 = (s * per) % nreq
+        sl = slice(b0, b0 + per)
         t0 = time.perf_counter()
-        oracle.verify_batch(tt, dd, xx, rr, temperature=1.0, seed=args.seed)
-        dt_s = time.perf_counter() - t0
+        oracle.verify_batch_parallel(inp["target"][sl], inp["draft"][sl], inp["draft_tokens"][sl],
+                                     inp["request_ids"][sl], threads=threads, temperature=1.0, seed=args.seed,
+                                     vocab=V, weight_mode=WEIGHTS[args.weights], select_mode=SELECTS[args.select])
         if s >= warm:
-            times.append(dt_s)
+            times.append(time.perf_counter() - t0)
     total = sum(times)
-    value = steps * k / total
+    value = steps * per * k / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": 1e3 * total / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "sample_per_step": "1 request (k verified tokens)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{steps} steps x 1 request of {args.config} (fp64 C oracle, 1 thread)"},
+        "config": {"workload": WORKLOADS[args.config], "weights": args.weights, "select": args.select,
+                   "sample_per_step": f"{per} requests ({per * k} verified tokens), one per host thread"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{steps} steps x {per} requests of {args.config} (fp64 C oracle, "
+                                   f"{threads} threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(args, kernel_regex):
+    """DRAM bytes (read + write) and duration of one launch of the dominant kernel, from an ncu
+    child run of this script (its own numbers are not used; N = 1 only)."""
+    ncu = "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", f"regex:{kernel_regex}", "-s", "3", "-c", "1", "--csv",
+           sys.executable, os.path.abspath(__file__), "--config", args.config, "--steps", "1", "--warmup", "3",
+           "--weights", args.weights, "--select", args.select, "--no-cpu-baseline", "--no-e2e",
+           "--traffic", "off", "--flush", "off"] + (["--lazy"] if args.lazy else [])
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    except Exception as e:  # pragma: no cover
+        return None, f"ncu failed: {e}"
+    vals = {}
+    import csv
+    import io
+    rows = [ln for ln in res.stdout.splitlines() if ln.startswith('"')]
+    for r in csv.DictReader(io.StringIO("\n".join(rows))):
+        name, unit, v = r.get("Metric Name"), r.get("Metric Unit"), r.get("Metric Value", "").replace(",", "")
+        try:
+            x = float(v)
+        except ValueError:
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                 "msecond": 1e-3}.get(unit, 1)
+        vals[name] = x * scale
+    if "dram__bytes_read.sum" not in vals:
+        return None, f"ncu gave no metrics (rc {res.returncode})"
+    return vals, "ncu dram__bytes_read.sum + dram__bytes_write.sum, one launch (cold L2)"
 
 
 # --------------------------------------------------------------------------------------
@@ -198,7 +276,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_2503_10325_b200 as cv
-    from paper_2503_10325_b200 import sharding, synth
+    import synth
+    from paper_2503_10325_b200 import sharding
 
     c = cfg_of(args.config)
     B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
@@ -208,16 +287,20 @@ def run_ours(args):
         return run_tree(args, c, dev, world, rank, local)
     if args.config == "c5":
         return run_vocab(args, c, dev, world, rank, local)
+    wm, sm = WEIGHTS[args.weights], SELECTS[args.select]
     rids = sharding.weak_request_ids(B, rank)  # weak scaling: a full batch per rank, global ids
     inp = synth.linear_inputs(B, k, N, V, dtype=dt, seed=args.seed + 7919 * rank, device=dev,
                               rid_base=rids.start)
     ver = cv.Verifier(V, max_batch=B, k=k, N=N, device=local, target_dtype=dt, draft_dtype=dt,
                       seed=args.seed, cluster_size=args.cluster_size)
     stream = torch.cuda.current_stream(dev)
+    alg_bytes = synth.algorithmic_bytes(B, k, N, V, esz, esz)
+    flush = args.flush == "on" or (args.flush == "auto" and alg_bytes < 4 * L2_BYTES)
+    scratch = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
 
     def step():
         ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"],
-                   temperature=1.0, lazy=args.lazy)
+                   temperature=1.0, lazy=args.lazy, weight_mode=wm, select_mode=sm)
         return cv.cosine_last_launch_count(ver.ctx)
 
     for _ in range(max(args.warmup, 3)):
@@ -236,6 +319,8 @@ def run_ours(args):
     launches = 0
     t_start.record(stream)
     for s in range(args.steps):
+        if flush:
+            scratch.zero_()  # evict the inputs from L2 (untimed: outside this call's events)
         ev[s][0].record(stream)
         launches += step()
         ev[s][1].record(stream)
@@ -245,48 +330,47 @@ def run_ours(args):
         dist.barrier()
     sampler.stop_ev.set()
     sampler.join()
-    elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [a.elapsed_time(b) for a, b in ev]
-    # second timed pass of the same K steps with CUDA events bracketing the dominant (stats)
-    # kernel on its stream (kept out of the first pass: an event between the two kernels
-    # disables their programmatic dependent launch)
+    elapsed_ms = sum(kern_ms) if flush else t_start.elapsed_time(t_end)
+    # second timed pass with CUDA events recorded by the library around its dominant launch on
+    # the launching stream (cosine_profile_*)
     cv.cosine_profile_enable(ver.ctx, True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     for s in range(args.steps):
+        if flush:
+            scratch.zero_()
         step()
     torch.cuda.synchronize()
-    stats_ms, stats_n = cv.cosine_profile_read(ver.ctx)
+    prof_ms, prof_n = cv.cosine_profile_read(ver.ctx)
     cv.cosine_profile_enable(ver.ctx, False)
+    kernel_name = "cosine::verify_kernel (the whole call: one launch)"
+    kernel_regex = "verify_kernel"
     if args.lazy:  # no single dominant launch: the whole call against its realised bytes
-        # rows read per request: target 0..L, drafters at positions 0..min(L, k-1), and the
-        # final draw's rows (1 + N at a rejection, the bonus row otherwise)
+        # rows read per request: target 0..L, drafters at positions 0..min(L, k-1) — the round
+        # holding L (kLazySpan = 2 positions per round) also streamed its other position — and
+        # the final draw's rows (1 + N at a rejection, the bonus row otherwise)
+        span = 2
         Ls = ver.accept_len[:B].long().clamp_min(0)
-        # (2 positions per round: the round holding L also streamed position L + 1 if it exists)
-        span_end = torch.clamp((Ls // 2) * 2 + 2, max=k + 1)  # positions 0 .. span_end - 1 read
+        span_end = torch.clamp((Ls // span) * span + span, max=k + 1)  # positions 0 .. span_end - 1 read
         rows = span_end + torch.clamp(span_end, max=k) * N + torch.where(Ls < k, 1 + N, 1)
-        realised = int(rows.sum()) * V * esz
-        stats_ms, stats_n = statistics.mean(kern_ms) * max(stats_n, 1), max(stats_n, 1)
+        alg_bytes = int(rows.sum()) * V * esz
+        prof_ms, prof_n = statistics.mean(kern_ms), 1
+        kernel_name, kernel_regex = "whole lazy call (rounds of stats + lazy_decide, then resample)", "stats_kernel"
+    elif sm == 1:
+        kernel_name = "cosine::unit_kernel (legacy SAMPLE-select path)"
+        kernel_regex = "unit_kernel"
     elapsed_ms = sharding.max_over_ranks(elapsed_ms, device=dev)  # the slowest rank's device time
     acc = ver.accept_len[:B].float().mean().item()
     status_nonzero = int((ver.status[:B] & 0xff).ne(0).sum().item())
 
     tokens_per_step = B * k * world
     value = tokens_per_step * args.steps / (elapsed_ms / 1e3)
-    alg_bytes = synth.algorithmic_bytes(B, k, N, V, esz, esz)
-    if args.lazy:
-        alg_bytes = realised
     step_avg_s = statistics.mean(kern_ms) / 1e3
-    kern_avg_s = (stats_ms / max(stats_n, 1)) / 1e3  # stats_kernel: reads every input byte once
+    kern_avg_s = (prof_ms / max(prof_n, 1)) / 1e3
     achieved = alg_bytes / kern_avg_s / 1e9
     peak, peak_src = peaks()
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(args.config)
-    except Exception:
-        pass
 
     # ---- e2e: the public call from pinned host buffers, H2D + kernel + D2H in the region
     e2e = None
@@ -296,7 +380,7 @@ def run_ours(args):
         devbuf = {n: torch.empty_like(inp[n]) for n in names}
         h2d = sum(host[n].numel() * host[n].element_size() for n in names)
         d2h = B * 4 + B * (k + 1) * 4 + B * 4
-        ver.verify_host(host, devbuf)
+        ver.verify_host(host, devbuf, weight_mode=wm, select_mode=sm)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -304,7 +388,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            ver.verify_host(host, devbuf)
+            ver.verify_host(host, devbuf, weight_mode=wm, select_mode=sm)
         e1.record(stream)
         torch.cuda.synchronize()
         te = sharding.max_over_ranks(e0.elapsed_time(e1), device=dev)
@@ -314,11 +398,22 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        host_inp = {n: inp[n][: min(B, 512)].cpu() for n in ("target", "draft", "draft_tokens", "request_ids")}
-        rate, nreq, spent = cpu_oracle_rate(host_inp, k, N, V, args.cpu_seconds, args.seed)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+        threads = cpu_threads(args)
+        host_inp = {n: inp[n][: min(B, 4 * threads)].cpu() for n in ("target", "draft", "draft_tokens", "request_ids")}
+        rate, nreq, spent = cpu_oracle_rate(host_inp, k, V, args.cpu_seconds, args.seed, threads, wm, sm)
+        rate1, nreq1, spent1 = cpu_oracle_rate(host_inp, k, V, args.cpu_seconds / 4, args.seed, 1, wm, sm)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"{nreq} requests of {args.config} ({nreq * k} verified tokens), fp64 C oracle, "
-                         f"1 thread, {spent:.1f} s"}
+                         f"{threads} threads (one request slice each), {spent:.1f} s",
+               "single_thread": {"value": rate1, "cores": 1, "sample": f"{nreq1} requests, {spent1:.1f} s"}}
+    ver.close()
+    del inp
+    traffic, traffic_src = None, "not measured"
+    if rank == 0 and world == 1 and args.traffic == "auto":
+        torch.cuda.empty_cache()
+        t, traffic_src = ncu_traffic(args, kernel_regex)
+        if t is not None:
+            traffic = t["dram__bytes_read.sum"] + t.get("dram__bytes_write.sum", 0.0)
 
     if rank == 0:
         clocks = sampler.result()
@@ -330,22 +425,25 @@ def run_ours(args):
             "config": {"workload": WORKLOADS[args.config] + (" — LAZY early-exit verification (NEXT-1): rows after "
                                                               "the first rejection are not read; bytes = realised"
                                                               if args.lazy else ""),
+                       "weights": args.weights, "select": args.select,
                        "batch_per_gpu": B, "global_batch": B * world,
                        "k": k, "drafters": N, "vocab": V, "parallelism": f"batch-sharded x{world}",
-                       "l2": f"inputs {alg_bytes / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
+                       "l2": (f"L2 flushed between timed calls ({2 * L2_BYTES >> 20} MiB memset, outside the "
+                              f"timed events; inputs {alg_bytes / 1e6:.1f} MB)") if flush else
+                             f"inputs {alg_bytes / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
                        "mean_accept_len": acc, "request_errors": status_nonzero},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "frac_of_8tbs": achieved / 8000.0, "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel_us": kern_avg_s * 1e6, "kernel": "cosine::stats_kernel",
-                         "kernel_launches_timed": stats_n,
+                         "kernel_us": kern_avg_s * 1e6, "kernel": kernel_name,
+                         "kernel_launches_timed": prof_n,
                          "step_us": step_avg_s * 1e6, "step_achieved": alg_bytes / step_avg_s / 1e9,
                          "step_frac": alg_bytes / step_avg_s / 1e9 / peak,
                          "step_frac_of_8tbs": alg_bytes / step_avg_s / 1e9 / 8000.0},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    ver.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -355,7 +453,8 @@ def run_tree(args, c, dev, world, rank, local):
     import torch
     import torch.distributed as dist
     import paper_2503_10325_b200 as cv
-    from paper_2503_10325_b200 import sharding, synth
+    import synth
+    from paper_2503_10325_b200 import sharding
     B, N, V, dt = c["B"], c["N"], c["V"], c["dtype"]
     t = synth.tree_inputs(B, N, V, dtype=dt, seed=args.seed + 7919 * rank, device=dev,
                           rid_base=sharding.weak_request_ids(B, rank).start)
@@ -368,11 +467,12 @@ def run_tree(args, c, dev, world, rank, local):
     ot = torch.empty(B, nn, dtype=torch.int32, device=dev)
     st = torch.empty(B, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    wm = WEIGHTS[args.weights]
 
     def step():
         cv.cosine_verify_tree(ctx, t["parent"], t["node_token"], t["internal_row"], t["target"], t["draft"],
                               t["node_draft_tokens"], t["request_ids"], al, an, ot, st, temperature=1.0,
-                              lazy=args.lazy)
+                              lazy=args.lazy, weight_mode=wm)
         return cv.cosine_last_launch_count(ctx)
 
     for _ in range(max(args.warmup, 3)):
@@ -397,6 +497,7 @@ def run_tree(args, c, dev, world, rank, local):
     tokens = B * t["J"] * world
     alg = synth.tree_algorithmic_bytes(B, nn, I, N, V, esz, esz)
     accounting = "all nodes read once (whole call)"
+    emitted = (al.clamp_min(0) + 1).sum().item() * world
     if args.lazy:  # realised path bytes: the visited nodes' rows + one pass per rejection / bonus
         par = t["parent"][0].tolist()
         irow = t["internal_row"][0].tolist()
@@ -423,9 +524,10 @@ def run_tree(args, c, dev, world, rank, local):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOADS["c4"] + (" — LAZY walk (NEXT-1): only the visited nodes' rows are read"
                                                       if args.lazy else ""),
-                       "batch_per_gpu": B, "global_batch": B * world,
+                       "weights": args.weights, "batch_per_gpu": B, "global_batch": B * world,
                        "tree_nodes": t["J"], "internal_nodes": I, "drafters": N, "vocab": V,
                        "parallelism": f"batch-sharded x{world}", "mean_accept_len": acc,
+                       "emitted_tokens_per_s": emitted / (ms / 1e3),
                        "l2": f"inputs {alg / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
@@ -441,12 +543,13 @@ def run_tree(args, c, dev, world, rank, local):
 
 def run_vocab(args, c, dev, world, rank, local):
     """c5: the same B = 1024 requests on every rank, each rank holding 1/N of the vocabulary
-    columns; one collective cosine_verify_batch per step (7 kernels + 3 NCCL
+    columns; one collective cosine_verify_batch per step (kernels + NCCL
     all-gathers).  Total work is fixed: strong scaling; value = B k / step time."""
     import torch
     import torch.distributed as dist
     import paper_2503_10325_b200 as cv
-    from paper_2503_10325_b200 import sharding, synth
+    import synth
+    from paper_2503_10325_b200 import sharding
     B, N, k, V, dt = c["B"], c["N"], c["k"], c["V"], c["dtype"]
     esz = torch.tensor([], dtype=dt).element_size()
     vb, ve = sharding.vocab_shard(V, world, rank)
@@ -474,9 +577,10 @@ def run_vocab(args, c, dev, world, rank, local):
                                     target_dtype=dt, draft_dtype=dt, seed=args.seed)
     ver = cv.Verifier(V, max_batch=B, k=k, N=N, device=local, ctx=ctx)
     stream = torch.cuda.current_stream(dev)
+    wm = WEIGHTS[args.weights]
 
     def step():
-        ver.verify(tgt, drf, toks, rid, temperature=1.0)
+        ver.verify(tgt, drf, toks, rid, temperature=1.0, weight_mode=wm)
         return cv.cosine_last_launch_count(ver.ctx)
 
     for _ in range(max(args.warmup, 3)):
@@ -508,15 +612,6 @@ def run_vocab(args, c, dev, world, rank, local):
     torch.cuda.synchronize()
     stats_ms, stats_n = cv.cosine_profile_read(ver.ctx)
     cv.cosine_profile_enable(ver.ctx, False)
-    if args.lazy:  # no single dominant launch: the whole call against its realised bytes
-        # rows read per request: target 0..L, drafters at positions 0..min(L, k-1), and the
-        # final draw's rows (1 + N at a rejection, the bonus row otherwise)
-        Ls = ver.accept_len[:B].long().clamp_min(0)
-        # (2 positions per round: the round holding L also streamed position L + 1 if it exists)
-        span_end = torch.clamp((Ls // 2) * 2 + 2, max=k + 1)  # positions 0 .. span_end - 1 read
-        rows = span_end + torch.clamp(span_end, max=k) * N + torch.where(Ls < k, 1 + N, 1)
-        realised = int(rows.sum()) * V * esz
-        stats_ms, stats_n = statistics.mean(kern_ms) * max(stats_n, 1), max(stats_n, 1)
     kern_s = max(sharding.max_over_ranks(stats_ms / max(stats_n, 1), device=dev) / 1e3, 1e-9)
     acc = ver.accept_len[:B].float().mean().item()
     errs = int((ver.status[:B] & 0xff).ne(0).sum().item())
@@ -529,7 +624,8 @@ def run_vocab(args, c, dev, world, rank, local):
             "metric": METRIC, "value": B * k / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOADS["c5"], "global_batch": B, "k": k, "drafters": N, "vocab": V,
+            "config": {"workload": WORKLOADS["c5"], "weights": args.weights, "global_batch": B, "k": k,
+                       "drafters": N, "vocab": V,
                        "shard_columns": W, "parallelism": f"vocab-sharded x{world}", "mean_accept_len": acc,
                        "request_errors": errs,
                        "l2": f"inputs {alg_rank / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
@@ -549,6 +645,7 @@ def run_vocab(args, c, dev, world, rank, local):
 
 if __name__ == "__main__":
     a = parse()
+    launch_ranks(a)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -331,6 +331,7 @@ int32_t cosine_last_launch_count(cosine_ctx_t ctx);
 cosine_status_t cosine_profile_enable(cosine_ctx_t ctx, int32_t enable);
 cosine_status_t cosine_profile_read(cosine_ctx_t ctx, double* total_ms, int32_t* launches);
 
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,8 @@ from . import _lib
 from ._lib import (  # noqa: F401
     BF16, F32, DRAFT_LOGITS, DRAFT_PROBS, INFO_DEGENERATE, INFO_NEAR_TIE, SEL_ARGMAX, SEL_SAMPLE,
     W_CONF, W_POINT, W_UNIFORM, W_WINNER, Context, CosineError, cosine_fuse_drafts,
-    cosine_last_launch_count, cosine_profile_enable, cosine_profile_read, cosine_sample_residual,
+    cosine_last_launch_count, cosine_profile_enable, cosine_profile_read,
+    cosine_sample_residual,
     cosine_fuse_step, cosine_nccl_unique_id, cosine_route_update, cosine_tree_select, cosine_verify_batch, cosine_verify_batch_lazy,
     cosine_verify_destroy,
     cosine_verify_init,
@@ -82,24 +83,28 @@ class Verifier:
 
     def verify_host(self, host_inputs: dict, dev_buffers: dict, *, temperature=1.0, step=0,
                     weight_mode=W_CONF, select_mode=SEL_ARGMAX, stream=None):
-        """End-to-end call from (pinned) host tensors: H2D copies into `dev_buffers`, the kernel,
-        and the D2H read of the results.  Returns host (accept_len, out_tokens, status)."""
-        for name in ("target", "draft", "draft_tokens", "request_ids"):
-            dev_buffers[name].copy_(host_inputs[name], non_blocking=True)
-        dl = None
-        if host_inputs.get("draft_len") is not None:
-            dev_buffers["draft_len"].copy_(host_inputs["draft_len"], non_blocking=True)
-            dl = dev_buffers["draft_len"]
-        a, o, s = self.verify(dev_buffers["target"], dev_buffers["draft"], dev_buffers["draft_tokens"],
-                              dev_buffers["request_ids"], temperature=temperature, draft_len=dl,
-                              step=step, weight_mode=weight_mode, select_mode=select_mode,
-                              stream=stream)
-        out = (torch.empty(a.shape, dtype=a.dtype, pin_memory=True),
-               torch.empty(o.shape, dtype=o.dtype, pin_memory=True),
-               torch.empty(s.shape, dtype=s.dtype, pin_memory=True))
-        out[0].copy_(a, non_blocking=True)
-        out[1].copy_(o, non_blocking=True)
-        out[2].copy_(s, non_blocking=True)
+        """End-to-end call from (pinned) host tensors: H2D copies into `dev_buffers`, the kernel
+        and the D2H read of the results, all on ONE stream (`stream`, default the current one),
+        which is synchronized before returning.  Returns host (accept_len, out_tokens, status),
+        valid on return (pinned buffers owned by this Verifier, overwritten by the next call)."""
+        s = stream if stream is not None else torch.cuda.current_stream(torch.device("cuda", self.device))
+        with torch.cuda.stream(s):
+            for name in ("target", "draft", "draft_tokens", "request_ids"):
+                dev_buffers[name].copy_(host_inputs[name], non_blocking=True)
+            dl = None
+            if host_inputs.get("draft_len") is not None:
+                dev_buffers["draft_len"].copy_(host_inputs["draft_len"], non_blocking=True)
+                dl = dev_buffers["draft_len"]
+            a, o, st = self.verify(dev_buffers["target"], dev_buffers["draft"], dev_buffers["draft_tokens"],
+                                   dev_buffers["request_ids"], temperature=temperature, draft_len=dl,
+                                   step=step, weight_mode=weight_mode, select_mode=select_mode, stream=s)
+            B = a.shape[0]
+            if getattr(self, "_host_out", None) is None or self._host_out[0].shape[0] < B:
+                self._host_out = tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (a, o, st))
+            out = tuple(h[:B] for h in self._host_out)
+            for h, d in zip(out, (a, o, st)):
+                h.copy_(d, non_blocking=True)
+        s.synchronize()
         return out
 
     def close(self):

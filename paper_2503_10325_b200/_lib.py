@@ -14,7 +14,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("COSINE_LIB") or os.path.join(_PKG, "libcosine_verify.so")
+LIB_PATH = os.path.join(_PKG, "libcosine_verify.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

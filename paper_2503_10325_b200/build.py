@@ -1,7 +1,9 @@
 """Compile libcosine_verify.so (sm_100a) in-tree with nvcc.
 
 `python paper_2503_10325_b200/build.py` or `__graft_entry__.build()` (run by path: the
-package itself refuses to import until the library exists).
+package itself refuses to import until the library exists).  The kernel templates are split
+over one translation unit per (target, draft) dtype pair plus the host TU; they compile in
+parallel and link into one shared library.
 """
 from __future__ import annotations
 
@@ -9,21 +11,20 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
+OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libcosine_verify.so")
-SOURCES = [os.path.join(CSRC, "cosine_verify.cu")]
-DEPS = SOURCES + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(INCLUDE, "*.h")))
+SOURCES = [os.path.join(CSRC, f) for f in ("cosine_abi.cu", "k_bb.cu", "k_bf.cu", "k_fb.cu", "k_ff.cu")]
+HEADERS = (sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(CSRC, "*.h")))
+           + sorted(glob.glob(os.path.join(CSRC, "*.inc"))) + sorted(glob.glob(os.path.join(INCLUDE, "*.h"))))
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-Xptxas", "-v",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc() -> str:
@@ -33,29 +34,57 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in DEPS)
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def stale() -> bool:
+    return _stale(LIB, SOURCES + HEADERS)
+
+
+def _compile(src: str):
+    out = _obj(src)
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", "-o", tmp, src]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode == 0:
+        os.replace(tmp, out)
+    return src, res
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    todo = [s for s in SOURCES if force or _stale(_obj(s), [s] + HEADERS)]
+    logs = []
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        for src, res in ex.map(_compile, todo):
+            logs.append(f"== {os.path.basename(src)}\n{res.stderr}")
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError(f"nvcc failed on {os.path.basename(src)}")
+    if logs:
+        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+            f.write("\n".join(logs))
+        if verbose:
+            sys.stderr.write("\n".join(logs))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *SOURCES, "-lnccl"]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *[_obj(s) for s in SOURCES], "-lnccl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libcosine_verify.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libcosine_verify.so")
     os.replace(tmp, LIB)
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

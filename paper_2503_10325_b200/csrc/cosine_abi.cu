@@ -1,0 +1,1046 @@
+// cosine_abi.cu — host side of libcosine_verify.so: the C ABI (include/cosine_verify.h),
+// argument checks, context / scratch ownership, launch configuration, NCCL for the
+// vocabulary-sharded mode, and the kernels that do not depend on the row dtypes.
+//
+// Kernels (all hand-written for sm_100a; nothing on this path is a contraction, so no tensor
+// cores — it is HBM-bound):
+//   cosine_verify_batch (1 GPU, ARGMAX)   stats -> decide -> resample (PDL, device counters)
+//   cosine_verify_batch (vocab-sharded)   stats -> pack -> all-gather -> decide -> resample ->
+//                                         all-gather -> sample -> all-gather -> finish
+//   cosine_verify_batch_lazy (NEXT-1)     rounds of stats + lazy_decide, then resample
+//   cosine_verify_tree[_lazy] (A10)       stats + tree_decide + tree_walk (cosine_tree.cuh)
+//   cosine_fuse_step / route_update / tree_select (NEXT-2..4)
+// See DESIGN.md §5 for the roofline, byte accounting and the B200 design choices.
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "cosine_dispatch.h"
+#include "cosine_fuse_step.cuh"
+#include "cosine_route.cuh"
+#include "cosine_shard.cuh"
+#include "cosine_tree_select.cuh"
+#include "cosine_verify.h"
+
+namespace cosine {
+
+__global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) { done[j] = 0; first_rej[j] = kNoReject; }
+}
+
+void kernel_set(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, KernelSet* ks) {
+  if (tt == COSINE_BF16 && tq == COSINE_BF16) kernel_set_bb(logits, N, ks);
+  else if (tt == COSINE_BF16 && tq == COSINE_F32) kernel_set_bf(logits, N, ks);
+  else if (tt == COSINE_F32 && tq == COSINE_BF16) kernel_set_fb(logits, N, ks);
+  else kernel_set_ff(logits, N, ks);
+}
+
+}  // namespace cosine
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+using namespace cosine;
+
+struct cosine_ctx_s {
+  cosine_config_t cfg;
+  int64_t V;
+  UnitRec* recs = nullptr;
+  PartRec* parts = nullptr;
+  PosDec* pdec = nullptr;
+  int32_t* counters = nullptr;
+  NodeDec* ndec = nullptr;
+  ChildPQ* cpq = nullptr;
+  double* segsum = nullptr;
+  size_t segsum_cap = 0;
+  // optional live timing of the dominant kernel (stats_kernel) with CUDA events on the stream
+  int prof_on = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+  size_t prof_n = 0;
+  int32_t* done = nullptr;
+  int32_t* first_rej = nullptr;
+  std::string err;
+  int32_t last_launches = 0;
+  int32_t last_cluster = 0, last_ncl = 0;
+  int32_t* lz = nullptr;  // lazy verification: per-request state
+  size_t parts_cap = 0;    // PartRec entries in `parts`
+  // vocabulary-sharded mode (nranks > 1)
+  ncclComm_t comm = nullptr;
+  uint32_t* rec_send = nullptr;
+  uint32_t* rec_all = nullptr;
+  double* zsend = nullptr;
+  double* zall = nullptr;
+  YRec* ysend = nullptr;
+  YRec* yall = nullptr;
+};
+
+static thread_local std::string g_init_error;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+cosine_status_t fail(cosine_ctx_t ctx, cosine_status_t s, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  else g_init_error = msg;
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+size_t esize(cosine_dtype_t t) { return t == COSINE_BF16 ? 2 : 4; }
+
+int pick_cluster(const cosine_ctx_t ctx, int64_t units, int64_t ngroups) {
+  if (ctx->cfg.cluster_size > 0) return std::min(ctx->cfg.cluster_size, 8);
+  // ~8 groups (64 elements per row) per thread, then widen while the grid is small
+  int C = 1;
+  while (C < 8 && ngroups > (int64_t)C * kThreads * 8) C *= 2;
+  while (C < 8 && units * C < 148 * 8 && ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  return C;
+}
+
+cosine_status_t launch(cosine_ctx_t ctx, cudaStream_t stream, Params& P, int64_t units,
+                       cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+  const int C = pick_cluster(ctx, units, P.ngroups);
+  P.C = C;
+  P.gpc = (P.ngroups + C - 1) / C;
+  P.recs = ctx->recs;
+  P.done = ctx->done;
+  P.first_rej = ctx->first_rej;
+  if (units == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  KernelSet ks;
+  kernel_set(tt, tq, logits, P.N, &ks);
+  KernelFn fn = ks.unit;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, fn, P);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 1;
+  return COSINE_OK;
+}
+
+// Chunk CTAs per unit of the streaming kernels: ~8 groups (64 elements per row) per thread,
+// then widen while the grid has fewer than ~8 CTAs per SM.
+int stats_chunks(const cosine_ctx_t ctx, int64_t units, int64_t ngroups, int per_thread = 8) {
+  if (ctx->cfg.cluster_size > 0) return ctx->cfg.cluster_size;
+  int C = 1;
+  while (C < kMaxC && ngroups > (int64_t)C * kThreads * per_thread) C *= 2;
+  while (C < kMaxC && units * C < 148 * 8 && ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  return C;
+}
+
+void fill_scratch(const cosine_ctx_t ctx, SplitParams& S, int C) {
+  S.C = C;
+  S.cg = (S.ngroups + C - 1) / C;
+  S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
+  S.tpc = kSegTilesPerCta;
+  S.spr = (int)((S.nseg + S.tpc - 1) / S.tpc);
+  S.parts = ctx->parts;
+  S.pdec = ctx->pdec;
+  S.segsum = ctx->segsum;
+  S.counters = ctx->counters;
+  S.dcnt = ctx->counters + std::max(ctx->cfg.max_batch, 1);
+  S.ucnt = ctx->counters + 2 * (size_t)std::max(ctx->cfg.max_batch, 1);
+  S.b_off = 0;
+  S.nb = S.B;
+}
+
+// Optional live timing of the dominant kernel with CUDA events on its stream.
+std::pair<cudaEvent_t, cudaEvent_t> prof_events(cosine_ctx_t ctx) {
+  if (!ctx->prof_on) return {nullptr, nullptr};
+  if (ctx->prof_n == ctx->prof_ev.size()) {
+    cudaEvent_t a0, a1;
+    cudaEventCreate(&a0);
+    cudaEventCreate(&a1);
+    ctx->prof_ev.emplace_back(a0, a1);
+  }
+  return ctx->prof_ev[ctx->prof_n++];
+}
+
+// The split path: stats_kernel -> decide_kernel -> resample_kernel, the latter two programmatic
+// dependents waiting per unit / per request on device counters (scheduled into the previous
+// grid's tail wave; the waits always end because every CTA they wait for is resident or done).
+cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, const KernelSet& ks) {
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  fill_scratch(ctx, S, stats_chunks(ctx, units, S.ngroups));
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  S.fused = 1;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  const auto pe = prof_events(ctx);
+  if (pe.first) cudaEventRecord(pe.first, stream);
+  lc.gridDim = dim3((unsigned)(units * S.C), 1, 1);
+  cudaError_t e = cudaLaunchKernelEx(&lc, ks.stats, S);
+  if (pe.second) cudaEventRecord(pe.second, stream);
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+    lc.attrs = pe.second ? nullptr : at;  // (an event record between the two breaks PDL)
+    lc.numAttrs = pe.second ? 0 : 1;
+    e = cudaLaunchKernelEx(&lc, ks.decide, S);
+  }
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, ks.resample, S);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("verify kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 3;
+  ctx->last_cluster = S.C;
+  return COSINE_OK;
+}
+
+// cosine_verify_batch on one GPU (ARGMAX selection).
+cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S,
+                             cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+  KernelSet ks;
+  memset(&ks, 0, sizeof(ks));
+  kernel_set(tt, tq, logits, S.N, &ks);
+  return launch_split3(ctx, stream, S, ks);
+}
+
+// Vocabulary-sharded verification (cosine_shard.cuh): 7 kernels and 3 all-gathers on `stream`.
+cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, cosine_dtype_t tt,
+                             cosine_dtype_t tq, bool logits) {
+  KernelSet ks;
+  kernel_set(tt, tq, logits, S.N, &ks);
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  const int C = stats_chunks(ctx, units, S.ngroups);
+  fill_scratch(ctx, S, C);
+  S.fused = 0;
+  S.shard = 1;
+  S.G = ctx->cfg.nranks;
+  S.rank = ctx->cfg.rank;
+  S.v0 = ctx->cfg.vocab_begin;
+  S.Vg = ctx->cfg.vocab_size;
+  S.rec_words = shard_rec_words(S.N);
+  S.rec_send = ctx->rec_send;
+  S.rec_all = ctx->rec_all;
+  S.zsend = ctx->zsend;
+  S.zall = ctx->zall;
+  S.ysend = ctx->ysend;
+  S.yall = ctx->yall;
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  const unsigned unit_blocks = (unsigned)((units + kWarps - 1) / kWarps);
+  auto launch = [&](SplitFn f, unsigned grid, bool pdl) {
+    lc.gridDim = dim3(grid, 1, 1);
+    lc.attrs = pdl ? at : nullptr;
+    lc.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&lc, f, S);
+  };
+  const char* stage = "stats";
+  const auto pe = prof_events(ctx);
+  if (pe.first) cudaEventRecord(pe.first, stream);
+  cudaError_t e = launch(ks.stats, (unsigned)(units * C), false);  // local row statistics
+  if (pe.second) cudaEventRecord(pe.second, stream);
+  if (e == cudaSuccess) { stage = "pack"; e = launch(ks.shard_pack, unit_blocks, pe.second == nullptr); }
+  ncclResult_t r = ncclSuccess;
+  if (e == cudaSuccess) {
+    r = ncclAllGather(ctx->rec_send, ctx->rec_all, (size_t)units * S.rec_words * 4, ncclUint8, ctx->comm, stream);
+  }
+  if (e == cudaSuccess && r == ncclSuccess) { stage = "decide"; e = launch(logits ? shard_decide_kernel<true> : shard_decide_kernel<false>, unit_blocks, false); }
+  if (e == cudaSuccess && r == ncclSuccess) { stage = "resample"; e = launch(ks.resample, (unsigned)(S.B * S.spr), false); }
+  if (e == cudaSuccess && r == ncclSuccess)
+    r = ncclAllGather(ctx->zsend, ctx->zall, (size_t)S.B * sizeof(double), ncclUint8, ctx->comm, stream);
+  if (e == cudaSuccess && r == ncclSuccess) { stage = "sample"; e = launch(ks.shard_sample, (unsigned)S.B, false); }
+  if (e == cudaSuccess && r == ncclSuccess)
+    r = ncclAllGather(ctx->ysend, ctx->yall, (size_t)S.B * sizeof(YRec), ncclUint8, ctx->comm, stream);
+  if (e == cudaSuccess && r == ncclSuccess) {
+    stage = "finish";
+    lc.gridDim = dim3((unsigned)((S.B + kThreads - 1) / kThreads), 1, 1);
+    lc.attrs = nullptr;
+    lc.numAttrs = 0;
+    e = cudaLaunchKernelEx(&lc, shard_finish_kernel, S);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("sharded verify (") + stage + "): " + cudaGetErrorString(e));
+  }
+  if (r != ncclSuccess) {
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_NCCL, std::string("sharded verify all-gather: ") + ncclGetErrorString(r));
+  }
+  ctx->last_launches = 7;
+  ctx->last_cluster = C;
+  return COSINE_OK;
+}
+
+// Lazy verification (NEXT-1): rounds r = 0..k of (stats of position r of the requests still
+// verifying -> their decisions), then the final draws.  2 (k + 1) + 1 launches on `stream`.
+cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, cosine_dtype_t tt,
+                            cosine_dtype_t tq, bool logits) {
+  KernelSet ks;
+  kernel_set(tt, tq, logits, S.N, &ks);
+  const int C = stats_chunks(ctx, S.B, S.ngroups);
+  fill_scratch(ctx, S, C);
+  S.lz = ctx->lz;
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaError_t e = cudaSuccess;
+  int launches = 0;
+  // rounds of kLazySpan positions (measured on c3: 1 -> 393 us, 2 -> 366 us, 3 -> 372 us); each
+  // round's decide kernel is scheduled into the stats tail (PDL) and waits per position
+  S.lazy_span = kLazySpan;
+  S.fused = 1;
+  for (int r = 0; r <= S.k && e == cudaSuccess; r += S.lazy_span) {
+    S.lazy = r + 1;
+    lc.gridDim = dim3((unsigned)((int64_t)S.B * S.lazy_span * S.C), 1, 1);
+    lc.attrs = nullptr;  // stream order: the round reads the previous round's lz
+    lc.numAttrs = 0;
+    e = cudaLaunchKernelEx(&lc, ks.stats, S);
+    if (e == cudaSuccess) {
+      lc.gridDim = dim3((unsigned)((S.B + kWarps - 1) / kWarps), 1, 1);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, ks.lazy_decide, S);
+    }
+    launches += 2;
+  }
+  S.lazy = 0;
+  S.fused = 0;  // the final draws wait for the last round's grid (griddepcontrol.wait)
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, ks.resample, S);
+    launches += 1;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("lazy verify kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = launches;
+  ctx->last_cluster = C;
+  return COSINE_OK;
+}
+
+void fill_common(Params& P, const cosine_ctx_t ctx, int B, int k, int N, float T) {
+  memset(&P, 0, sizeof(P));
+  P.B = B;
+  P.k = k;
+  P.N = N;
+  P.V = ctx->V;
+  P.ngroups = (ctx->V + kGroup - 1) / kGroup;
+  P.gfull = ctx->V / kGroup;
+  P.T = T;
+  P.greedy = (T == 0.f);
+  const double k2 = (T > 0.f) ? 1.4426950408889634 / (double)T : 0.0;
+  P.k2d = k2;
+  P.k2f = (float)k2;
+  P.seed = ctx->cfg.seed;
+}
+
+cosine_status_t check_rows(cosine_ctx_t ctx, const void* p, int64_t ld, cosine_dtype_t t,
+                           const char* what) {
+  if (!p) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, std::string(what) + " is NULL");
+  if (ld < ctx->V) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, std::string(what) + ": ld < vocabulary width");
+  if (!aligned16(p) || ((uint64_t)ld * esize(t)) % 16 != 0)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, std::string(what) + ": rows must be 16-byte aligned");
+  return COSINE_OK;
+}
+
+cosine_status_t check_common(cosine_ctx_t ctx, int B, int k, int N) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  if (B < 0 || B > ctx->cfg.max_batch) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "B outside [0, max_batch]");
+  if (k < 1 || k > ctx->cfg.max_draft_len) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "k outside [1, max_draft_len]");
+  if (N < 1 || N > ctx->cfg.max_drafters || N > kMaxN) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "N outside [1, max_drafters]");
+  return COSINE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out) {
+  if (!out) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cfg is NULL");
+  if (cfg->vocab_size < 1 || cfg->vocab_begin < 0 || cfg->vocab_end > cfg->vocab_size ||
+      cfg->vocab_end <= cfg->vocab_begin)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad vocabulary range");
+  if (cfg->vocab_end - cfg->vocab_begin > (int64_t)0x7fffffff)
+    return fail(nullptr, COSINE_ERR_UNSUPPORTED, "vocabulary wider than 2^31 - 1");
+  if (cfg->max_tree_nodes < 0 || cfg->max_tree_nodes > kTreeMaxNodes)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "max_tree_nodes outside [0, 1024]");
+  if (cfg->max_batch < 0 || cfg->max_draft_len < 1 || cfg->max_draft_len > kMaxPos - 1 ||
+      cfg->max_drafters < 1 || cfg->max_drafters > kMaxN)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad max_* sizes (max_draft_len <= 64, max_drafters <= 8)");
+  if ((cfg->target_dtype != COSINE_BF16 && cfg->target_dtype != COSINE_F32) ||
+      (cfg->draft_dtype != COSINE_BF16 && cfg->draft_dtype != COSINE_F32))
+    return fail(nullptr, COSINE_ERR_UNSUPPORTED, "dtype must be COSINE_BF16 or COSINE_F32");
+  if (cfg->draft_kind != COSINE_DRAFT_PROBS && cfg->draft_kind != COSINE_DRAFT_LOGITS)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad draft_kind");
+  if (cfg->nranks < 1 || cfg->nranks > 32 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks must be in [1, 32] and rank in [0, nranks)");
+  if (cfg->nranks == 1 && (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab_size))
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "an unsharded context covers [0, vocab_size)");
+  if (cfg->nranks > 1 && !cfg->nccl_unique_id)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks > 1 needs nccl_unique_id (cosine_nccl_unique_id on rank 0)");
+  if (cfg->cluster_size != 0 && cfg->cluster_size != 1 && cfg->cluster_size != 2 &&
+      cfg->cluster_size != 4 && cfg->cluster_size != 8 && cfg->cluster_size != 16)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cluster_size must be 0, 1, 2, 4, 8 or 16");
+  cosine_ctx_t ctx = new (std::nothrow) cosine_ctx_s();
+  if (!ctx) return fail(nullptr, COSINE_ERR_OUT_OF_MEMORY, "host allocation failed");
+  ctx->cfg = *cfg;
+  ctx->cfg.nccl_unique_id = nullptr;
+  ctx->V = cfg->vocab_end - cfg->vocab_begin;
+  DeviceGuard dg(cfg->device);
+  const size_t nb = (size_t)std::max(cfg->max_batch, 1);
+  cudaError_t e = cudaMalloc(&ctx->recs, nb * (size_t)(cfg->max_draft_len + 1) * sizeof(UnitRec));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->done, nb * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->first_rej, nb * sizeof(int32_t));
+  const size_t nu = nb * (size_t)std::max(cfg->max_draft_len + 1, std::max(cfg->max_tree_nodes, 1));
+  const size_t nt = nb * (size_t)std::max(cfg->max_tree_nodes, 1);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->ndec, nt * sizeof(NodeDec));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->cpq, nt * sizeof(ChildPQ));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->parts, nu * kMaxC * sizeof(PartRec));
+  ctx->parts_cap = nu * kMaxC;
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
+  // counters: [B] kernel-B CTAs per request | [B] decided units per request | [B][k+1] chunks per unit
+  const size_t ncnt = 2 * nb + nb * (size_t)(cfg->max_draft_len + 1);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, ncnt * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->lz, nb * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, ncnt * sizeof(int32_t));
+  ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
+  if (e == cudaSuccess) {
+    init_scratch<<<(unsigned)((nb + 255) / 256), 256>>>(ctx->done, ctx->first_rej, (int)nb);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && cfg->nranks > 1) {  // vocabulary-sharded: exchange buffers + communicator
+    const size_t units = nb * (size_t)(cfg->max_draft_len + 1);
+    const size_t rb = units * (size_t)shard_rec_words(cfg->max_drafters) * 4;
+    e = cudaMalloc(&ctx->rec_send, rb);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->rec_all, rb * (size_t)cfg->nranks);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->zsend, nb * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->zall, nb * sizeof(double) * (size_t)cfg->nranks);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->ysend, nb * sizeof(YRec));
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->yall, nb * sizeof(YRec) * (size_t)cfg->nranks);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  ncclResult_t nr = ncclSuccess;
+  if (e == cudaSuccess && cfg->nranks > 1) {
+    ncclUniqueId uid;
+    memcpy(&uid, cfg->nccl_unique_id, sizeof(uid));
+    nr = ncclCommInitRank(&ctx->comm, cfg->nranks, uid, cfg->rank);
+    if (nr != ncclSuccess) ctx->comm = nullptr;
+  }
+  if (e != cudaSuccess || nr != ncclSuccess) {
+    std::string msg = (e != cudaSuccess) ? std::string("init: ") + cudaGetErrorString(e)
+                                         : std::string("init: ncclCommInitRank: ") + ncclGetErrorString(nr);
+    cudaFree(ctx->rec_send);
+    cudaFree(ctx->rec_all);
+    cudaFree(ctx->zsend);
+    cudaFree(ctx->zall);
+    cudaFree(ctx->ysend);
+    cudaFree(ctx->yall);
+    cudaFree(ctx->lz);
+    cudaGetLastError();
+    cudaFree(ctx->recs);
+    cudaFree(ctx->done);
+    cudaFree(ctx->first_rej);
+    cudaFree(ctx->parts);
+    cudaFree(ctx->pdec);
+    cudaFree(ctx->counters);
+    cudaFree(ctx->ndec);
+    cudaFree(ctx->cpq);
+    cudaFree(ctx->segsum);
+    delete ctx;
+    if (e == cudaSuccess) return fail(nullptr, COSINE_ERR_NCCL, msg);
+    return fail(nullptr, e == cudaErrorMemoryAllocation ? COSINE_ERR_OUT_OF_MEMORY : COSINE_ERR_CUDA, msg);
+  }
+  *out = ctx;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
+  if (!ctx) return COSINE_OK;
+  DeviceGuard dg(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  cudaFree(ctx->recs);
+  cudaFree(ctx->done);
+  cudaFree(ctx->first_rej);
+  cudaFree(ctx->parts);
+  cudaFree(ctx->pdec);
+  cudaFree(ctx->counters);
+  cudaFree(ctx->ndec);
+  cudaFree(ctx->cpq);
+  cudaFree(ctx->segsum);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  cudaFree(ctx->lz);
+  cudaFree(ctx->rec_send);
+  cudaFree(ctx->rec_all);
+  cudaFree(ctx->zsend);
+  cudaFree(ctx->zall);
+  cudaFree(ctx->ysend);
+  cudaFree(ctx->yall);
+  for (auto& pe : ctx->prof_ev) {
+    cudaEventDestroy(pe.first);
+    cudaEventDestroy(pe.second);
+  }
+  delete ctx;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_nccl_unique_id(void* out, int64_t capacity) {
+  if (!out || capacity < (int64_t)sizeof(ncclUniqueId))
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "unique id buffer smaller than COSINE_NCCL_UNIQUE_ID_BYTES");
+  ncclUniqueId uid;
+  const ncclResult_t r = ncclGetUniqueId(&uid);
+  if (r != ncclSuccess) return fail(nullptr, COSINE_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(out, &uid, sizeof(uid));
+  return COSINE_OK;
+}
+
+const char* cosine_last_error(cosine_ctx_t ctx) {
+  return ctx ? ctx->err.c_str() : g_init_error.c_str();
+}
+
+int32_t cosine_last_launch_count(cosine_ctx_t ctx) { return ctx ? ctx->last_launches : 0; }
+
+cosine_status_t cosine_profile_enable(cosine_ctx_t ctx, int32_t enable) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  ctx->prof_on = enable ? 1 : 0;
+  ctx->prof_n = 0;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_profile_read(cosine_ctx_t ctx, double* total_ms, int32_t* launches) {
+  if (!ctx || !total_ms || !launches) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard dg(ctx->cfg.device);
+  double t = 0.0;
+  for (size_t j = 0; j < ctx->prof_n; ++j) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->prof_ev[j].second) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, ctx->prof_ev[j].first, ctx->prof_ev[j].second) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, COSINE_ERR_CUDA, "profile events not recorded");
+    }
+    t += ms;
+  }
+  *total_ms = t;
+  *launches = (int32_t)ctx->prof_n;
+  ctx->prof_n = 0;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                   int32_t N, const void* draft, int64_t ld_q,
+                                   const int32_t* draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, float temperature,
+                                   cosine_weight_mode_t weight_mode, cosine_select_mode_t select_mode,
+                                   int32_t* fused_tokens, float* weights, float* draft_norm,
+                                   float* fused_q, int64_t ld_fq, int32_t* status) {
+  cosine_status_t s = check_common(ctx, B, k, N);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_fuse_drafts runs on unsharded contexts (nranks == 1)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
+  if (!draft_tokens || !request_ids || !fused_tokens || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if ((int)weight_mode < 0 || (int)weight_mode > 3 || (int)select_mode < 0 || (int)select_mode > 1)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad weight / select mode");
+  if (weight_mode == COSINE_W_POINT && select_mode == COSINE_SEL_SAMPLE)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "POINT weights need ARGMAX selection");
+  if (ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS && !(temperature > 0.f && std::isfinite(temperature)))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "LOGITS drafts need temperature > 0");
+  if (fused_q && (ld_fq < ctx->V || !aligned16(fused_q) || (ld_fq * 4) % 16 != 0))
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "fused_q must be 16-byte aligned with ld_fq >= V");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P;
+  fill_common(P, ctx, B, k, N, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS ? temperature : 1.f);
+  P.greedy = 0;
+  P.mode = kModeFuse;
+  P.ld_q = ld_q;
+  P.ld_fq = ld_fq;
+  P.draft = draft;
+  P.draft_tokens = draft_tokens;
+  P.rids = request_ids;
+  P.step = step;
+  P.weight_mode = weight_mode;
+  P.select_mode = select_mode;
+  P.fused_tokens = fused_tokens;
+  P.w_out = weights;
+  P.norm_out = draft_norm;
+  P.fused_q = fused_q;
+  P.status = status;
+  return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * k, ctx->cfg.target_dtype,
+                ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+}
+
+cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                    int32_t N, const void* target_logits, int64_t ld_t,
+                                    float temperature, const void* draft, int64_t ld_q,
+                                    const int32_t* draft_tokens, const int32_t* draft_len,
+                                    const uint64_t* request_ids, uint32_t step,
+                                    cosine_weight_mode_t weight_mode,
+                                    cosine_select_mode_t select_mode, int32_t* accept_len,
+                                    int32_t* out_tokens, int32_t* status,
+                                    const cosine_debug_t* debug) {
+  cosine_status_t s = check_common(ctx, B, k, N);
+  if (s != COSINE_OK) return s;
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, target_logits, ld_t, ctx->cfg.target_dtype, "target_logits")) != COSINE_OK) return s;
+  if ((s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
+  if (!draft_tokens || !request_ids || !accept_len || !out_tokens || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature >= 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "temperature must be finite and >= 0");
+  if ((int)weight_mode < 0 || (int)weight_mode > 3 || (int)select_mode < 0 || (int)select_mode > 1)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad weight / select mode");
+  if (weight_mode == COSINE_W_POINT && select_mode == COSINE_SEL_SAMPLE)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "POINT weights need ARGMAX selection");
+  if (temperature == 0.f && (ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS || select_mode == COSINE_SEL_SAMPLE))
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "greedy (T = 0) needs PROBS drafts and ARGMAX selection");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P;
+  fill_common(P, ctx, B, k, N, temperature);
+  P.mode = kModeVerify;
+  P.ld_t = ld_t;
+  P.ld_q = ld_q;
+  P.target = target_logits;
+  P.draft = draft;
+  P.draft_tokens = draft_tokens;
+  P.draft_len = draft_len;
+  P.rids = request_ids;
+  P.step = step;
+  P.weight_mode = weight_mode;
+  P.select_mode = select_mode;
+  P.accept_len = accept_len;
+  P.out_tokens = out_tokens;
+  P.status = status;
+  if (debug) P.dbg = *debug;
+  if (ctx->cfg.nranks > 1) {  // vocabulary-sharded (cosine_shard.cuh)
+    if (select_mode != COSINE_SEL_ARGMAX)
+      return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary sharding takes ARGMAX selection");
+    SplitParams S;
+    memset(&S, 0, sizeof(S));
+    S.B = B; S.k = k; S.N = N;
+    S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+    S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+    S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+    S.rids = request_ids; S.seed = P.seed; S.step = step;
+    S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
+    return launch_shard(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                        ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+  }
+  if (select_mode == COSINE_SEL_ARGMAX) {
+    SplitParams S;
+    memset(&S, 0, sizeof(S));
+    S.B = B; S.k = k; S.N = N;
+    S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+    S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+    S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+    S.rids = request_ids; S.seed = P.seed; S.step = step;
+    S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
+    return launch_split(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                        ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+  }
+  return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
+                ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+}
+
+cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                         int32_t N, const void* target_logits, int64_t ld_t,
+                                         float temperature, const void* draft, int64_t ld_q,
+                                         const int32_t* draft_tokens, const int32_t* draft_len,
+                                         const uint64_t* request_ids, uint32_t step,
+                                         cosine_weight_mode_t weight_mode, int32_t* accept_len,
+                                         int32_t* out_tokens, int32_t* status,
+                                         const cosine_debug_t* debug) {
+  cosine_status_t s = check_common(ctx, B, k, N);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_verify_batch_lazy runs on unsharded contexts (nranks == 1)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, target_logits, ld_t, ctx->cfg.target_dtype, "target_logits")) != COSINE_OK) return s;
+  if ((s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
+  if (!draft_tokens || !request_ids || !accept_len || !out_tokens || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature >= 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "temperature must be finite and >= 0");
+  if ((int)weight_mode < 0 || (int)weight_mode > 3)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad weight mode");
+  if (temperature == 0.f && ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "greedy (T = 0) needs PROBS drafts");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P;
+  fill_common(P, ctx, B, k, N, temperature);
+  SplitParams S;
+  memset(&S, 0, sizeof(S));
+  S.B = B; S.k = k; S.N = N;
+  S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+  S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+  S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+  S.rids = request_ids; S.seed = P.seed; S.step = step;
+  S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status;
+  if (debug) S.dbg = *debug;
+  return launch_lazy(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                     ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+}
+
+static cosine_status_t verify_tree_impl(bool lazy, cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                   int32_t I, int32_t N, const int32_t* parent,
+                                   const int32_t* node_token, const int32_t* internal_row,
+                                   const void* target, int64_t ld_t, float temperature,
+                                   const void* draft, int64_t ld_q,
+                                   const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, cosine_weight_mode_t weight_mode,
+                                   int32_t* accept_len, int32_t* accepted_nodes,
+                                   int32_t* out_tokens, int32_t* status) {
+  cosine_status_t s = check_common(ctx, B, 1, N);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_verify_tree runs on unsharded contexts (nranks == 1)");
+  if (J < 0 || J + 1 > ctx->cfg.max_tree_nodes)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "J + 1 exceeds max_tree_nodes");
+  if (I < 0 || I > J + 1) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "I outside [0, J + 1]");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, target, ld_t, ctx->cfg.target_dtype, "target")) != COSINE_OK) return s;
+  if (I > 0 && (s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
+  if (!parent || !node_token || !internal_row || (I > 0 && !node_draft_tokens) || !request_ids ||
+      !accept_len || !accepted_nodes || !out_tokens || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature > 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "tree verification needs a finite temperature > 0");
+  if ((int)weight_mode < 0 || (int)weight_mode > 2)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "tree weight mode must be CONF, WINNER or UNIFORM");
+  const int64_t ngroups = (ctx->V + kGroup - 1) / kGroup;
+  const int nmax = N <= 4 ? 4 : 8;
+  const int esz = (int)std::max(esize(ctx->cfg.target_dtype), esize(ctx->cfg.draft_dtype));
+  const int tg = tree_tile_groups(nmax, esz);
+  if ((ngroups + tg - 1) / tg > kMaxSeg)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary too wide for the tree sampler");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P0;
+  fill_common(P0, ctx, B, 1, N, temperature);
+  TreeParams T;
+  memset(&T, 0, sizeof(T));
+  SplitParams& S = T.S;
+  S.B = B; S.k = 1; S.N = N;
+  S.V = P0.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P0.ngroups; S.gfull = P0.gfull;
+  S.k2f = P0.k2f; S.k2d = P0.k2d; S.greedy = 0; S.weight_mode = weight_mode;
+  S.target = target; S.draft = draft; S.rids = request_ids; S.seed = P0.seed; S.step = step;
+  S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status;
+  S.tree = 1; S.nn = J + 1; S.I = I; S.irow = internal_row;
+  S.parts = ctx->parts;
+  T.parent = parent; T.node_token = node_token; T.node_draft_tokens = node_draft_tokens;
+  T.ndec = ctx->ndec; T.cpq = ctx->cpq; T.accepted_nodes = accepted_nodes;
+  T.lazy = lazy ? 1 : 0;
+  const int64_t units = (int64_t)B * (J + 1);
+  const int C = stats_chunks(ctx, units, S.ngroups);
+  S.C = C;
+  S.cg = (S.ngroups + C - 1) / C;
+  KernelSet ks;
+  kernel_set(ctx->cfg.target_dtype, ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS, N, &ks);
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaError_t e = cudaSuccess;
+  if (!lazy) {
+    lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+    e = cudaLaunchKernelEx(&lc, ks.stats, S);  // every node's rows, once
+    if (e == cudaSuccess) {
+      lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, ks.tree_decide, T);
+    }
+  }
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)B, 1, 1);
+    lc.blockDim = dim3(kTreeBlock, 1, 1);
+    lc.dynamicSmemBytes = (size_t)tree_walk_smem(nmax, (ngroups + tg - 1) / tg);
+    cudaFuncAttributes fa;
+    int optin = 0;
+    e = cudaFuncGetAttributes(&fa, ks.tree_walk);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);
+    if (e == cudaSuccess && fa.sharedSizeBytes + lc.dynamicSmemBytes > (size_t)optin) {
+      ctx->last_launches = 2;
+      return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary too wide for the tree walk's shared memory");
+    }
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ks.tree_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.dynamicSmemBytes);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&lc, ks.tree_walk, T);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("tree kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = lazy ? 1 : 3;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_verify_tree(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                   int32_t I, int32_t N, const int32_t* parent,
+                                   const int32_t* node_token, const int32_t* internal_row,
+                                   const void* target, int64_t ld_t, float temperature,
+                                   const void* draft, int64_t ld_q,
+                                   const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                   uint32_t step, cosine_weight_mode_t weight_mode,
+                                   int32_t* accept_len, int32_t* accepted_nodes,
+                                   int32_t* out_tokens, int32_t* status) {
+  return verify_tree_impl(false, ctx, stream, B, J, I, N, parent, node_token, internal_row, target, ld_t,
+                          temperature, draft, ld_q, node_draft_tokens, request_ids, step, weight_mode,
+                          accept_len, accepted_nodes, out_tokens, status);
+}
+
+cosine_status_t cosine_fuse_step(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t N,
+                                 const void* logits, int64_t ld, float temperature, int32_t* own_tokens,
+                                 float* conf, int32_t* fused_token, int32_t* winner, int32_t* status) {
+  cosine_status_t s = check_common(ctx, B, 1, N);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_fuse_step runs on unsharded contexts (nranks == 1)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, logits, ld, ctx->cfg.draft_dtype, "logits")) != COSINE_OK) return s;
+  if (!own_tokens || !conf || !fused_token || !winner || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (!(temperature > 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "fuse_step needs a finite temperature > 0");
+  DeviceGuard dg(ctx->cfg.device);
+  FuseStepParams F;
+  memset(&F, 0, sizeof(F));
+  F.B = B; F.N = N; F.V = ctx->V; F.ld = ld;
+  F.ngroups = (ctx->V + kGroup - 1) / kGroup;
+  F.gfull = ctx->V / kGroup;
+  F.k2f = (float)(1.4426950408889634 / (double)temperature);
+  const int64_t rows = (int64_t)B * N;
+  // one row per CTA (16 B per load): ~32 groups per thread keep the per-CTA reduction cheap
+  int C = 1;
+  while (C < kMaxC && F.ngroups > (int64_t)C * kThreads * 32) C *= 2;
+  while (C < kMaxC && rows * C < 148 * 6 && F.ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
+  while (C > 1 && (size_t)(rows * C) > ctx->parts_cap) C /= 2;
+  if ((size_t)(rows * C) > ctx->parts_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "B * N exceeds the context's scratch (raise max_batch / max_draft_len)");
+  F.C = C;
+  F.cg = (F.ngroups + C - 1) / C;
+  F.logits = logits;
+  F.parts = ctx->parts;
+  F.own_tokens = own_tokens; F.conf = conf; F.fused_token = fused_token; F.winner = winner; F.status = status;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  lc.gridDim = dim3((unsigned)(rows * C), 1, 1);
+  cudaError_t e = (ctx->cfg.draft_dtype == COSINE_BF16)
+                      ? cudaLaunchKernelEx(&lc, fuse_step_stats_kernel<__nv_bfloat16>, F)
+                      : cudaLaunchKernelEx(&lc, fuse_step_stats_kernel<float>, F);
+  if (e == cudaSuccess) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    lc.gridDim = dim3((unsigned)((B + kWarps - 1) / kWarps), 1, 1);
+    e = cudaLaunchKernelEx(&lc, fuse_step_combine_kernel, F);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("fuse_step kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 2;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_route_update(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t N, int32_t K,
+                                    const int32_t* draft_tokens, const float* conf, const int32_t* accepted,
+                                    int64_t acc_stride, const int32_t* accept_len, const void* emb,
+                                    int64_t hidden, int64_t ld_e, cosine_dtype_t emb_dtype,
+                                    const uint8_t* participating, float decay, float* M, float* d_out,
+                                    int32_t* status) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  if (B < 0 || B > ctx->cfg.max_batch) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "B outside [0, max_batch]");
+  if (N < 1 || N > kWarps * 4 || K < 1 || acc_stride < K)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad N / K / acc_stride");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if (!draft_tokens || !conf || !accepted || !accept_len || !emb || !M || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if (emb_dtype != COSINE_BF16 && emb_dtype != COSINE_F32)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "embedding dtype must be COSINE_BF16 or COSINE_F32");
+  if (hidden < 8 || hidden % 8 != 0 || ld_e < hidden || !aligned16(emb) || ((uint64_t)ld_e * esize(emb_dtype)) % 16 != 0)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "embedding rows: hidden % 8 == 0, 16-byte aligned rows");
+  if (!(decay >= 0.f && decay <= 1.f)) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "decay outside [0, 1]");
+  DeviceGuard dg(ctx->cfg.device);
+  RouteParams R;
+  memset(&R, 0, sizeof(R));
+  R.B = B; R.N = N; R.K = K; R.V = ctx->cfg.vocab_size; R.Hd = hidden; R.ld_e = ld_e; R.acc_stride = acc_stride;
+  R.draft_tokens = draft_tokens; R.conf = conf; R.accepted = accepted; R.accept_len = accept_len; R.emb = emb;
+  R.participating = participating; R.decay = decay; R.eps = 1e-6f; R.M = M; R.d_out = d_out; R.status = status;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.gridDim = dim3((unsigned)B, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  cudaError_t e = (emb_dtype == COSINE_BF16) ? cudaLaunchKernelEx(&lc, route_update_kernel<__nv_bfloat16>, R)
+                                             : cudaLaunchKernelEx(&lc, route_update_kernel<float>, R);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("route_update: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 1;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_tree_select(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t S, int32_t K,
+                                   const int32_t* tokens, const float* conf, int32_t budget, int32_t* n_nodes,
+                                   int32_t* parent, int32_t* token, float* score, int32_t* depth) {
+  if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
+  if (B < 0 || S < 1 || K < 1 || budget < 0 || (int64_t)S * K + 1 > kSelMaxNodes)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "bad B / S / K / budget (S * K + 1 <= 1024)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if (!tokens || !conf || !n_nodes || !parent || !token || !score || !depth)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  DeviceGuard dg(ctx->cfg.device);
+  TreeSelParams T;
+  memset(&T, 0, sizeof(T));
+  T.B = B; T.S = S; T.K = K; T.budget = budget; T.tokens = tokens; T.conf = conf;
+  T.n_nodes = n_nodes; T.parent = parent; T.token = token; T.score = score; T.depth = depth;
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.gridDim = dim3((unsigned)B, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  const cudaError_t e = cudaLaunchKernelEx(&lc, tree_select_kernel, T);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("tree_select: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 1;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_verify_tree_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t J,
+                                        int32_t I, int32_t N, const int32_t* parent,
+                                        const int32_t* node_token, const int32_t* internal_row,
+                                        const void* target, int64_t ld_t, float temperature,
+                                        const void* draft, int64_t ld_q,
+                                        const int32_t* node_draft_tokens, const uint64_t* request_ids,
+                                        uint32_t step, cosine_weight_mode_t weight_mode,
+                                        int32_t* accept_len, int32_t* accepted_nodes,
+                                        int32_t* out_tokens, int32_t* status) {
+  return verify_tree_impl(true, ctx, stream, B, J, I, N, parent, node_token, internal_row, target, ld_t,
+                          temperature, draft, ld_q, node_draft_tokens, request_ids, step, weight_mode,
+                          accept_len, accepted_nodes, out_tokens, status);
+}
+
+cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B,
+                                       const void* target_rows, int64_t ld_t, float temperature,
+                                       const float* row_max, const float* row_sumexp,
+                                       const void* draft_rows, int64_t ld_q, const float* weights,
+                                       const float* draft_norm, int32_t N,
+                                       const uint32_t* node_ids, const uint64_t* request_ids,
+                                       uint32_t step, int32_t* out_token, int32_t* status) {
+  const int Nc = draft_rows ? N : 1;
+  cosine_status_t s = check_common(ctx, B, 1, Nc);
+  if (s != COSINE_OK) return s;
+  if (ctx->cfg.nranks > 1)
+    return fail(ctx, COSINE_ERR_UNSUPPORTED, "cosine_sample_residual runs on unsharded contexts (nranks == 1)");
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if ((s = check_rows(ctx, target_rows, ld_t, ctx->cfg.target_dtype, "target_rows")) != COSINE_OK) return s;
+  if (draft_rows) {
+    if ((s = check_rows(ctx, draft_rows, ld_q, ctx->cfg.draft_dtype, "draft_rows")) != COSINE_OK) return s;
+    if (!weights || !draft_norm) return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "weights / draft_norm are NULL");
+    if (ctx->cfg.draft_kind != COSINE_DRAFT_PROBS)
+      return fail(ctx, COSINE_ERR_UNSUPPORTED, "sample_residual takes PROBS drafter rows");
+  }
+  if (!node_ids || !request_ids || !out_token || !status)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "NULL required pointer");
+  if ((row_max == nullptr) != (row_sumexp == nullptr))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "row_max and row_sumexp must both be given or both NULL");
+  if (!(temperature >= 0.f) || !std::isfinite(temperature))
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "temperature must be finite and >= 0");
+  DeviceGuard dg(ctx->cfg.device);
+  Params P;
+  fill_common(P, ctx, B, 1, Nc, temperature);
+  P.mode = kModeSample;
+  P.ld_t = ld_t;
+  P.ld_q = ld_q;
+  P.target = target_rows;
+  P.draft = draft_rows;
+  P.row_max = row_max;
+  P.row_sumexp = row_sumexp;
+  P.w_in = weights;
+  P.norm_in = draft_norm;
+  P.node_ids = node_ids;
+  P.rids = request_ids;
+  P.step = step;
+  P.out_token = out_token;
+  P.status = status;
+  return launch(ctx, (cudaStream_t)stream, P, (int64_t)B, ctx->cfg.target_dtype,
+                ctx->cfg.draft_dtype, false);
+}
+
+}  // extern "C"

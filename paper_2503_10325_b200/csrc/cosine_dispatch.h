@@ -1,0 +1,33 @@
+// cosine_dispatch.h — the kernel set of one (target dtype, draft dtype, draft kind, N) combination.
+//
+// The heavy kernel templates are instantiated once per dtype pair in their own translation
+// unit (k_<tt><tq>.cu, compiled in parallel); the host code (cosine_abi.cu) picks a set here.
+#pragma once
+
+#include "cosine_tree.cuh"
+#include "cosine_unit.cuh"
+
+namespace cosine {
+
+using SplitFn = void (*)(SplitParams);
+using TreeFn = void (*)(TreeParams);
+using KernelFn = void (*)(Params);
+
+struct KernelSet {
+  SplitFn stats;         // stats_kernel (lazy rounds, tree all-nodes, sharded)
+  SplitFn lazy_decide;   // lazy round decisions (NEXT-1)
+  SplitFn decide;        // split path decisions (stats -> decide -> resample)
+  SplitFn resample;      // final draws
+  SplitFn shard_pack;    // vocabulary-sharded records
+  SplitFn shard_sample;  // vocabulary-sharded owner scan
+  TreeFn tree_decide;
+  TreeFn tree_walk;
+  KernelFn unit;         // legacy cluster kernel (SAMPLE select, fuse_drafts, sample_residual)
+};
+
+void kernel_set_bb(bool logits, int N, KernelSet* out);  // bf16 target, bf16 drafts
+void kernel_set_bf(bool logits, int N, KernelSet* out);  // bf16 target, fp32 drafts
+void kernel_set_fb(bool logits, int N, KernelSet* out);  // fp32 target, bf16 drafts
+void kernel_set_ff(bool logits, int N, KernelSet* out);  // fp32 target, fp32 drafts
+
+}  // namespace cosine

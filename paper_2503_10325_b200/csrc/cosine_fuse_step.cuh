@@ -12,6 +12,8 @@
 //     fp64) and fuses.
 #pragma once
 
+#include "cosine_common.cuh"
+
 namespace cosine {
 
 struct FuseStepParams {

@@ -83,6 +83,7 @@ struct Group<__nv_bfloat16> {
   __device__ __forceinline__ bool any_sign() const {
     return ((a.x | a.y | a.z | a.w) & 0x80008000u) != 0u;
   }
+  __device__ __forceinline__ void zero() { a = make_uint4(0u, 0u, 0u, 0u); }
 };
 
 template <>
@@ -105,6 +106,7 @@ struct Group<float> {
   __device__ __forceinline__ bool any_sign() const {
     return ((a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0x80000000u) != 0u;
   }
+  __device__ __forceinline__ void zero() { a = b = make_uint4(0u, 0u, 0u, 0u); }
 };
 
 __device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }

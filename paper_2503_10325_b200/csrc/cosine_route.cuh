@@ -6,6 +6,8 @@
 // Non-participating nodes decay toward 0.5.  Tokens outside [0, V): status 2, M kept.
 #pragma once
 
+#include "cosine_common.cuh"
+
 namespace cosine {
 
 struct RouteParams {

@@ -18,6 +18,8 @@
 //      (replicated) outputs on every rank.
 #pragma once
 
+#include "cosine_split.cuh"
+
 namespace cosine {
 
 struct YRec {  // the final token as seen by one rank
@@ -339,6 +341,8 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
   }
 }
 
+#ifndef COSINE_DTYPE_TU  // non-template kernel: defined in the host TU only
+
 // ---------------- 5. the replicated outputs (one thread per request) ----------------
 __global__ void __launch_bounds__(kThreads) shard_finish_kernel(const SplitParams P) {
   const int b = blockIdx.x * kThreads + threadIdx.x;
@@ -380,5 +384,7 @@ __global__ void __launch_bounds__(kThreads) shard_finish_kernel(const SplitParam
   if (P.dbg.residual_mass) P.dbg.residual_mass[b] = bonus ? (float)((double)yr.z / pds[v.L].S) : yr.z;
   if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
 }
+
+#endif
 
 }  // namespace cosine

@@ -1,21 +1,26 @@
-// cosine_split.cuh — the two kernels behind cosine_verify_batch (Eq. 4 ARGMAX fusion).
+// cosine_split.cuh — the streaming verification kernels (Eq. 4 ARGMAX fusion).
 //
-// Kernel A (stats_kernel): one CTA per (unit, vocabulary chunk), unit = (request b,
-//   position i <= gamma_b).  Each CTA streams its chunk of the unit's target logit row and N
-//   drafter rows exactly once with 128-bit read-only loads, reduces them (online max /
-//   sum-exp of the target, drafter row sums, greedy argmax) and writes a 128-byte partial
-//   record.  Nothing else: no decision code, so the kernel stays register-lean (high
-//   occupancy = many loads in flight) and never waits.
-// Kernel B (decide_sample_kernel): one thread-block cluster per request.  Every CTA combines
-//   the partial records of the request's positions (one warp per position), takes the
-//   decisions — confidences and Eq. 4 fusion, acceptance u * q(x*) < o(x*)
-//    — finds the first rejection L and the cluster draws the final token by
-//   inverse CDF over the residual norm(max(0, o - q)) of row L, or over o of the bonus row
-//   (P:133): pass A = per-warp segment sums, chunk sums exchanged over DSMEM; pass B = one
-//   warp scans the crossing segment.  CTA 0 writes the request's outputs.
+// stats_kernel (A): one CTA per (unit, vocabulary chunk), unit = (request b, position
+//   i <= gamma_b).  Each CTA streams its chunk of the unit's target logit row and N drafter
+//   rows exactly once with 128-bit read-only loads, reduces them (online max / sum-exp of the
+//   target, drafter row sums, greedy argmax) and writes a 128-byte partial record.
+//   Register-lean (high occupancy = many loads in flight); never waits.
+// decide_kernel (B1): one warp per unit — confidences and Eq. 4 fusion, acceptance
+//   u * q(x*) < o(x*) — a programmatic dependent of A that waits per unit.
+// resample_kernel (B2): the first rejection L and the final draw by inverse CDF over
+//   norm(max(0, o - q)) of row L, or over o of the bonus row; waits per request.
+// lazy_decide_kernel: the decisions of a lazy (NEXT-1) round.
 #pragma once
 
+#include "cosine_common.cuh"
+
 namespace cosine {
+
+template <bool B>
+struct BoolTag {
+  static constexpr bool value = B;
+};
+
 
 struct PartRec {  // one per (unit, chunk); 128 bytes
   float tmax;     // T > 0: chunk max logit; greedy: best value
@@ -27,6 +32,7 @@ struct PartRec {  // one per (unit, chunk); 128 bytes
 };
 
 constexpr int kMaxPos = 65;  // draft positions per request (k <= 64) in kernel B
+constexpr int kLazySpan = 2;  // positions per lazy round (NEXT-1)
 
 struct SplitParams {
   int B, k, N;
@@ -152,19 +158,22 @@ __device__ __forceinline__ int64_t warp_scan_range(const PP& P, const Decision& 
 }
 
 // ============================== kernel A ==============================
+// Resident CTAs per SM of the streaming kernels: register-lean (40 registers) for bf16 with
+// N <= 4, so that 48 warps of 128-bit loads are in flight per SM.
+template <typename TT, typename TQ, int NMAX>
+constexpr int stats_occupancy() {
+  return (NMAX <= 4 && sizeof(TT) == 2 && sizeof(TQ) == 2) ? 6 : 4;
+}
+
+// One CTA's share of a unit: chunk `rank` of the unit's target row and N drafter rows, streamed
+// once; writes the chunk's partial record.  Returns the unit's record index, or -1 when the CTA
+// has no rows (position past gamma_b, bad gamma_b, or a stopped lazy request).  Ends with the
+// record written by warp 0 (no trailing barrier).
 template <typename TT, typename TQ, bool kLogits, int NMAX>
-__global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && sizeof(TQ) == 2) ? 6 : 4)
-    stats_kernel(const SplitParams P) {
+__device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit, int rank) {
   const int C = P.C;
-  const int64_t unit = blockIdx.x / C;
-  const int rank = (int)(blockIdx.x % C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = P.N;
-  // every CTA of this grid is resident or done once all passed this point: kernel B (launched
-  // as a programmatic dependent) may then be scheduled into the tail wave (it waits per request)
-#ifndef COSINE_NO_LAUNCH_DEP
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
   int Nd;
   const TT* trow;
   const TQ* drow;
@@ -181,13 +190,13 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
     if (P.lazy) {  // lazy round (NEXT-1): positions r0 .. r0+span-1 of the requests still verifying
       b = (int)(unit / P.lazy_span);
       i = P.lazy - 1 + (int)(unit % P.lazy_span);
-      if (P.lazy > 1 && P.lz[b] != 0) return;
+      if (P.lazy > 1 && P.lz[b] != 0) return -1;
     } else {
       b = P.b_off + (int)(unit / (P.k + 1));
       i = (int)(unit % (P.k + 1));
     }
     const int g = P.draft_len ? P.draft_len[b] : P.k;
-    if (g < 1 || g > P.k || i > g) return;  // rows past gamma_b are never read
+    if (g < 1 || g > P.k || i > g) return -1;  // rows past gamma_b are never read
     Nd = (i < g) ? N : 0;
     gu = (int64_t)b * (P.k + 1) + i;
     trow = (const TT*)P.target + gu * P.ld_t;
@@ -370,9 +379,19 @@ __global__ void __launch_bounds__(kThreads, (NMAX <= 4 && sizeof(TT) == 2 && siz
       rec->dsum[n] = sacc;
     }
   }
-  if (P.fused) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
+  return gu;
+}
+
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX>()))
+    stats_kernel(const SplitParams P) {
+  // every CTA of this grid is resident or done once all passed this point: kernel B (launched
+  // as a programmatic dependent) may then be scheduled into the tail wave (it waits per unit)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t gu = stats_body<TT, TQ, kLogits, NMAX>(P, blockIdx.x / P.C, (int)(blockIdx.x % P.C));
+  if (P.fused && gu >= 0) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
     __syncthreads();
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
       __threadfence();  // the record before the count (release)
       atomicAdd(&P.ucnt[gu], 1);
     }
@@ -493,7 +512,8 @@ __device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i,
 // o(X_n) and q_m(X_n), lane 0 writes the decision to *out (and the diagnostics if asked).
 template <typename TT, typename TQ, bool kLogits>
 __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
-                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
+                                            int32_t* s_tokw, PosDec* out, bool write_debug,
+                                            PosDec* out2 = nullptr) {
   const int lane = threadIdx.x & 31;
   const int N = P.N, C = P.C;
   const int64_t unit = (int64_t)b * (P.k + 1) + i;
@@ -566,37 +586,37 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
       if (s_tokw[n] < 0 || (int64_t)s_tokw[n] >= P.V) tok_bad = true;
   decide_lane0<kLogits>(P, b, i, has_d, tok_bad, t_nf || d_nf, t_empty || d_empty, s_gxw, s_tokw, sig, dmax, pd);
   *out = pd;
+  if (out2) *out2 = pd;
   if (write_debug) write_pos_debug(P, b, i, has_d, pd);
 }
 
-// Kernel B1: one warp per (request, position) -> PosDec in global memory (+ diagnostics).
+// Kernel B1 (split path): one warp per (request, position) -> PosDec in global memory (+
+// diagnostics); a programmatic dependent of stats_kernel that waits per unit (device counter).
 template <typename TT, typename TQ, bool kLogits>
 __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
   __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
   __shared__ int32_t s_tok[kWarps][kMaxN];
-  if (!P.fused) asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel A's records (PDL)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (unit >= (int64_t)P.nb * (P.k + 1)) return;
-  const int b = P.b_off + (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  if (unit >= (int64_t)P.B * (P.k + 1)) return;
+  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
   const int g = P.draft_len ? P.draft_len[b] : P.k;
   if (g < 1 || g > P.k || i > g) return;
   const int64_t gu = (int64_t)b * (P.k + 1) + i;
-  if (P.fused) {  // this unit's C chunk records (every kernel-A CTA is resident or done by now)
-    if ((threadIdx.x & 31) == 0) {
-      uint32_t n;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.ucnt + gu) : "memory");
-        if ((int)n >= P.C) break;
-        __nanosleep(100);
-      }
+  // this unit's C chunk records (every stats CTA is resident or done once this CTA runs)
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t n;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.ucnt + gu) : "memory");
+      if ((int)n >= P.C) break;
+      __nanosleep(100);
     }
-    __syncwarp();
   }
+  __syncwarp();
   warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[gu], true);
-  if (P.fused && (threadIdx.x & 31) == 0) {
-    P.ucnt[gu] = 0;  // ready for the next call
+  if ((threadIdx.x & 31) == 0) {
+    P.ucnt[gu] = 0;   // ready for the next call
     __threadfence();  // the decision before its count (release)
     atomicAdd(&P.dcnt[b], 1);
   }
@@ -702,13 +722,21 @@ template <typename TT, typename TQ, int NMAX>
 struct RowGroups {
   Group<TT> t;
   Group<TQ> d[NMAX];
+  __device__ __forceinline__ void zero() {
+    t.zero();
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) d[n].zero();
+  }
+  // Every member is assigned on every path (zeros when not needed): a member left unset on
+  // one path forces the whole array into local memory.
   __device__ __forceinline__ void load(const TT* trow, const TQ* drow, int64_t ld_q, int Nd, bool need_t,
                                        bool need_q, int64_t gi) {
     if (need_t) t.load(trow, gi);
-    if (need_q) {
+    else t.zero();
 #pragma unroll
-      for (int n = 0; n < NMAX; ++n)
-        if (n < Nd) d[n].load(drow + (int64_t)n * ld_q, gi);
+    for (int n = 0; n < NMAX; ++n) {
+      if (need_q && n < Nd) d[n].load(drow + (int64_t)n * ld_q, gi);
+      else d[n].zero();
     }
   }
 };
@@ -802,105 +830,79 @@ __device__ __forceinline__ double warp_tile_crossing(const double* seg, int64_t 
   return Z;
 }
 
-// Kernel B2 (resample_kernel): CTA (request b, block of kSegTilesPerCta 2048-entry tiles).
-//  1. it reads the request's position decisions (kernel B1) and derives the first rejection L
-//     (P:132);
-//  2. the CTA streams its tiles of the (1+N) rows at L — same mapping as kernel A, two tiles of
-//     loads in flight — and writes each tile's residual (or bonus) mass;
-//  3. the LAST CTA of the request (device-scope counter) sums the tile masses in tile order,
+// The final draw of a request, split in parts of kSegTilesPerCta 2048-entry tiles:
+//  1. the request's position decisions give the first rejection L (request_view);
+//  2. each part streams its tiles of the (1+N) rows at L (or the bonus row) — same group
+//     mapping as the statistics pass, one tile of loads per thread in flight — and writes each
+//     tile's residual (or bonus) mass;
+//  3. the LAST part of the request (device-scope counter) sums the tile masses in tile order,
 //     finds the crossing tile, scans it block-wide (reading #10) and writes the outputs.
 constexpr int kSegTilesPerCta = 8;
-template <typename TT, typename TQ, bool kLogits, int NMAX>
-__global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams P) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
-  const int part = blockIdx.x % P.spr;
-  const int64_t tile0 = (int64_t)part * P.tpc;
-  __shared__ __align__(16) PosDec s_pd[kMaxPos];
-  __shared__ ReqView s_v;
-  __shared__ Decision s_d;
-  __shared__ double s_red[kWarps][kSegTilesPerCta];
-  __shared__ double s_scan[kWarps];
-  __shared__ int64_t s_wi[kWarps];
-  __shared__ int64_t s_found;
-  __shared__ float s_margin;
-  __shared__ int s_last;
 
-  const int g = P.draft_len ? P.draft_len[b] : P.k;
-  if (P.fused) {
-    // kernel A decides the units itself and counts them per request: wait for this request's
-    // g + 1 decisions only (every kernel-A CTA is resident or done once this CTA runs, so the
-    // wait always ends), not for the whole grid
-    if (g >= 1 && g <= P.k) {
-      if (tid == 0) {
-        uint32_t n;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.dcnt + b) : "memory");
-          if ((int)n >= g + 1) break;
-          __nanosleep(200);
-        }
-      }
-      __syncthreads();
-    }
-  } else {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // kernel B1's decisions (PDL)
-  }
-  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
-  if (g < 1 || g > P.k) {
-    if (P.shard) {  // the outputs come from shard_finish_kernel
-      if (part == 0 && tid == 0) P.zsend[b] = 0.0;
-      return;
-    }
-    if (part == 0 && tid == 0) {
-      P.accept_len[b] = -1;
-      for (int j = 0; j <= P.k; ++j) out[j] = -1;
-      P.status[b] = COSINE_REQ_BAD_DRAFT_LEN;
-    }
-    return;
-  }
-  const uint64_t rid = P.rids[b];
-  const PosDec* gpd = P.pdec + (int64_t)b * (P.k + 1);
-  // the request's decisions (kernel B1): positions 0..g, one round of loads
-  {
-    const int nw = (int)(sizeof(PosDec) / 4);
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(gpd);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(s_pd);
-    for (int w = tid; w < (g + 1) * nw; w += kThreads) dst[w] = __ldcg(src + w);
-  }
+struct ResampleSmem {
+  PosDec pd[kMaxPos];
+  ReqView v;
+  Decision d;
+  double red[kWarps][kSegTilesPerCta];
+  double scan[kWarps];
+  double seg[kMaxSeg];
+  int64_t wi[kWarps];
+  int64_t found, tstar;
+  double tc, Z;
+  float margin;
+  int last, kind, deg;
+};
+
+// All threads: request b's decisions (positions 0..g) into shared memory, the request view and,
+// when a final inverse-CDF draw is needed, its Decision.  Ends with a barrier.
+__device__ __forceinline__ void load_request(const SplitParams& P, int b, int g, ResampleSmem& s) {
+  const int tid = threadIdx.x;
+  const int nw = (int)(sizeof(PosDec) / 4);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(P.pdec + (int64_t)b * (P.k + 1));
+  uint32_t* dst = reinterpret_cast<uint32_t*>(s.pd);
+  for (int w = tid; w < (g + 1) * nw; w += kThreads) dst[w] = __ldcg(src + w);  // L2 (other CTAs wrote them)
   __syncthreads();
   if (tid == 0) {
-    const ReqView v = request_view(P, s_pd, g);
-    s_v = v;
-    if (v.sample) s_d = sample_decision(P, rid, s_pd[v.L], v);
+    const ReqView v = request_view(P, s.pd, g);
+    s.v = v;
+    if (v.sample) s.d = sample_decision(P, P.rids[b], s.pd[v.L], v);
   }
   __syncthreads();
-  const ReqView v = s_v;
-  if (!v.sample) {  // a per-request error, or greedy (y = argmax of row L, reading #7)
-    if (P.shard) {
-      if (part == 0 && tid == 0) P.zsend[b] = 0.0;
-      return;
-    }
-    if (P.fused && tid == 0) {  // the request's last B CTA resets the counters for the next call
-      const int old = atomicAdd(&P.counters[b], 1);
-      if (old == P.spr - 1) { P.counters[b] = 0; P.dcnt[b] = 0; }
-    }
-    if (part == 0) {
-      for (int j = tid; j <= P.k; j += kThreads)
-        out[j] = v.err ? -1 : ((j < v.L) ? s_pd[j].xstar : (j == v.L ? (int32_t)s_pd[v.L].amax : -1));
-      if (tid == 0) {
-        P.accept_len[b] = v.err ? -1 : v.L;
-        P.status[b] = v.err ? v.err : ((v.tm < 1e-6f) ? COSINE_INFO_NEAR_TIE : 0);
-        if (!v.err && P.dbg.tie_margin) P.dbg.tie_margin[b] = v.tm;
-      }
-    }
-    return;
+}
+
+// Outputs of a request without a final draw: a per-request error, or greedy (y = argmax of
+// row L, reading #7).  Threads of one CTA.
+__device__ __forceinline__ void write_plain_outputs(const SplitParams& P, int b, const ResampleSmem& s) {
+  const ReqView& v = s.v;
+  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
+  for (int j = threadIdx.x; j <= P.k; j += kThreads)
+    out[j] = v.err ? -1 : ((j < v.L) ? s.pd[j].xstar : (j == v.L ? (int32_t)s.pd[v.L].amax : -1));
+  if (threadIdx.x == 0) {
+    P.accept_len[b] = v.err ? -1 : v.L;
+    P.status[b] = v.err ? v.err : ((v.tm < 1e-6f) ? COSINE_INFO_NEAR_TIE : 0);
+    if (!v.err && P.dbg.tie_margin) P.dbg.tie_margin[b] = v.tm;
   }
-  const Decision d = s_d;
+}
+
+__device__ __forceinline__ void write_bad_len(const SplitParams& P, int b) {
+  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
+  P.accept_len[b] = -1;
+  for (int j = 0; j <= P.k; ++j) out[j] = -1;
+  P.status[b] = COSINE_REQ_BAD_DRAFT_LEN;
+}
+
+// Part `part` of request b's final draw (s loaded by load_request, s.v.sample set).
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int part, ResampleSmem& s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const ReqView v = s.v;
+  const Decision& d = s.d;
   const int kind0 = d.kind;
   const int Nd = (v.L < v.g) ? P.N : 0;
   const bool need_q = (kind0 == kWResidual);
   const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
   const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
+  const int64_t tile0 = (int64_t)part * P.tpc;
   const int ntiles = (int)min((int64_t)P.tpc, P.nseg - tile0);
 #pragma unroll 1
   for (int j = 0; j < ntiles; ++j) {  // one tile of (1+N) loads per thread in flight
@@ -916,38 +918,34 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
       m0 = (double)sum8(w);
     }
     m0 = warp_sum(m0);
-    if (lane == 0) s_red[warp][j] = m0;
+    if (lane == 0) s.red[warp][j] = m0;
   }
   __syncthreads();
   if (tid < ntiles) {
     double z = 0.0;
-    for (int w = 0; w < kWarps; ++w) z += s_red[w][tid];
+    for (int w = 0; w < kWarps; ++w) z += s.red[w][tid];
     P.segsum[(int64_t)b * P.nseg + tile0 + tid] = z;
   }
   __syncthreads();
   if (tid == 0) {
     __threadfence();
     const int old = atomicAdd(&P.counters[b], 1);
-    s_last = (old == P.spr - 1);
-    if (s_last && P.fused) P.dcnt[b] = 0;  // every B CTA of the request has passed its wait
+    s.last = (old == P.spr - 1);
+    if (s.last && P.fused) P.dcnt[b] = 0;  // every part of the request has passed its wait
   }
   __syncthreads();
-  if (!s_last) return;
-  // ---------------- the last CTA of the request: crossing tile, scan, outputs ----------------
+  if (!s.last) return;
+  // ---------------- the last part of the request: crossing tile, scan, outputs ----------------
   __threadfence();
-  __shared__ int64_t s_tstar;
-  __shared__ double s_tc, s_Z;
-  __shared__ int s_kind, s_deg;
-  __shared__ double s_seg[kMaxSeg];
   const double* ss = P.segsum + (int64_t)b * P.nseg;
   const bool in_smem = P.nseg <= kMaxSeg;
   if (in_smem)
-    for (int64_t t = tid; t < P.nseg; t += kThreads) s_seg[t] = __ldcg(ss + t);
+    for (int64_t t = tid; t < P.nseg; t += kThreads) s.seg[t] = __ldcg(ss + t);
   __syncthreads();
   if (warp == 0) {
     int64_t tstar = -1;
     double tc = 0.0;
-    const double Z = in_smem ? warp_tile_crossing<false>(s_seg, P.nseg, d.u, &tstar, &tc)
+    const double Z = in_smem ? warp_tile_crossing<false>(s.seg, P.nseg, d.u, &tstar, &tc)
                              : warp_tile_crossing<true>(ss, P.nseg, d.u, &tstar, &tc);
     if (lane == 0) {
       P.counters[b] = 0;  // ready for the next call
@@ -960,18 +958,18 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
           dg = 1;
           tstar = -1;
         }
-        s_Z = Z;
-        s_kind = kind;
-        s_deg = dg;
-        s_tstar = tstar;
-        s_tc = tc;
+        s.Z = Z;
+        s.kind = kind;
+        s.deg = dg;
+        s.tstar = tstar;
+        s.tc = tc;
       }
     }
   }
   if (P.shard) return;
   __syncthreads();
-  const int kind = s_kind, deg = s_deg;
-  double Z = s_Z;
+  const int kind = s.kind, deg = s.deg;
+  double Z = s.Z;
   int64_t y = -1;
   float margin = INFINITY;
   if (deg) {  // rare: the whole row from o, block-wide
@@ -981,20 +979,21 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
       group_weights<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, gi, w);
       acc += (double)sum8(w);
     }
-    Z = block_sum(acc, s_scan);
-    if (tid == 0) s_Z = Z;
+    Z = block_sum(acc, s.scan);
+    if (tid == 0) s.Z = Z;
     __syncthreads();
-    Z = s_Z;
-    y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, 0, P.ngroups, d.u * Z, Z, s_scan,
-                                          s_wi, &s_found, &s_margin);
-    margin = s_margin;
-  } else if (s_tstar >= 0) {
-    const int64_t sb = s_tstar * kTileGroups;
+    Z = s.Z;
+    y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, 0, P.ngroups, d.u * Z, Z, s.scan,
+                                          s.wi, &s.found, &s.margin);
+    margin = s.margin;
+  } else if (s.tstar >= 0) {
+    const int64_t sb = s.tstar * kTileGroups;
     y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sb, min(P.ngroups, sb + kTileGroups),
-                                          s_tc, Z, s_scan, s_wi, &s_found, &s_margin);
-    margin = s_margin;
+                                          s.tc, Z, s.scan, s.wi, &s.found, &s.margin);
+    margin = s.margin;
   }
-  for (int j = tid; j <= P.k; j += kThreads) out[j] = (j < v.L) ? s_pd[j].xstar : (j == v.L ? (int32_t)y : -1);
+  int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
+  for (int j = tid; j <= P.k; j += kThreads) out[j] = (j < v.L) ? s.pd[j].xstar : (j == v.L ? (int32_t)y : -1);
   if (tid == 0) {
     P.accept_len[b] = v.L;
     const float tm = fmin_(v.tm, margin);
@@ -1003,6 +1002,58 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     if (P.dbg.residual_mass) P.dbg.residual_mass[b] = (float)((kind == kWBonus) ? Z * (double)d.invS : Z);
     if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
   }
+}
+
+// Kernel B2 (lazy and vocabulary-sharded paths): CTA (request b, part), a programmatic
+// dependent of the kernel that wrote the decisions.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams P) {
+  __shared__ __align__(16) ResampleSmem s;
+  const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
+  const int part = blockIdx.x % P.spr;
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (P.fused) {
+    // split path: wait for this request's g + 1 decisions only (every decide_kernel CTA is
+    // resident or done once this CTA runs, so the wait always ends), not for the whole grid
+    if (g >= 1 && g <= P.k) {
+      if (threadIdx.x == 0) {
+        uint32_t n;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.dcnt + b) : "memory");
+          if ((int)n >= g + 1) break;
+          __nanosleep(200);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the decisions (PDL)
+  }
+  if (g < 1 || g > P.k) {
+    if (part == 0 && threadIdx.x == 0) {
+      if (P.shard) P.zsend[b] = 0.0;  // the outputs come from shard_finish_kernel
+      else write_bad_len(P, b);
+    }
+    return;
+  }
+  load_request(P, b, g, s);
+  if (!s.v.sample) {
+    if (P.fused && threadIdx.x == 0) {  // the request's last part resets the counters
+      if (atomicAdd(&P.counters[b], 1) == P.spr - 1) {
+        P.counters[b] = 0;
+        P.dcnt[b] = 0;
+      }
+    }
+    if (part == 0) {
+      if (P.shard) {
+        if (threadIdx.x == 0) P.zsend[b] = 0.0;
+      } else {
+        write_plain_outputs(P, b, s);
+      }
+    }
+    return;
+  }
+  resample_tiles<TT, TQ, kLogits, NMAX>(P, b, part, s);
 }
 
 }  // namespace cosine

@@ -12,6 +12,8 @@
 // final draw).
 #pragma once
 
+#include "cosine_split.cuh"
+
 namespace cosine {
 
 struct NodeDec {  // per node (b, j)

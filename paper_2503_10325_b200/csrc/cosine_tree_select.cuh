@@ -8,6 +8,8 @@
 //      output satisfies cosine_verify_tree's parent[j] < j / slot order.
 #pragma once
 
+#include "cosine_common.cuh"
+
 namespace cosine {
 
 constexpr int kSelMaxNodes = 1024;

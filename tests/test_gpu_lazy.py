@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2503_10325_b200 import synth, W_CONF, W_POINT, W_WINNER
+import synth
+from paper_2503_10325_b200 import W_CONF, W_POINT, W_WINNER
 from tests import parity
 
 

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2503_10325_b200 import synth
+import synth
 
 from . import parity
 

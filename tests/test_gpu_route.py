@@ -53,7 +53,7 @@ def test_route_update_matches_oracle(cuda_ok, dtype, H):
 
 def test_route_update_after_verification(cuda_ok):
     # the post-verification step of Alg. 1: out_tokens / accept_len of cosine_verify_batch
-    from paper_2503_10325_b200 import synth
+    import synth
     from tests import parity
     B, k, N, V = 32, 6, 3, 3001
     inp = synth.linear_inputs(B, k, N, V, dtype=torch.bfloat16, seed=11)

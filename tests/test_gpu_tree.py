@@ -4,7 +4,7 @@ import pytest
 import torch
 
 import oracle
-from paper_2503_10325_b200 import synth
+import synth
 
 pytestmark = pytest.mark.gpu
 

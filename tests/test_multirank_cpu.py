@@ -26,7 +26,8 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle
-    from paper_2503_10325_b200 import sharding, synth
+    import synth
+    from paper_2503_10325_b200 import sharding
     inp = synth.linear_inputs(10, 4, 3, 300, dtype=torch.float32, seed=3, sigma=3.0)
     b0, b1 = sharding.shard_range(10, world, rank)
     r = oracle.verify_batch(inp["target"][b0:b1], inp["draft"][b0:b1], inp["draft_tokens"][b0:b1],
@@ -53,7 +54,7 @@ def test_two_rank_batch_sharding():
         assert p.exitcode == 0
     assert t == 2.0 and n == 10
     import oracle
-    from paper_2503_10325_b200 import synth
+    import synth
     inp = synth.linear_inputs(10, 4, 3, 300, dtype=torch.float32, seed=3, sigma=3.0)
     full = oracle.verify_batch(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"], seed=11,
                                vocab=300)

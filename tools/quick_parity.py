@@ -1,7 +1,7 @@
 import sys, time, torch, numpy as np
 sys.path.insert(0, '.')
 import paper_2503_10325_b200 as cv
-from paper_2503_10325_b200 import synth
+import synth
 import oracle
 
 def run(B, k, N, V, dtype, T=1.0, wm=0, sm=0, draft_len=None, seed=0, kind='probs', cs=0):

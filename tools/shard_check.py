@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import paper_2503_10325_b200 as cv  # noqa: E402
-from paper_2503_10325_b200 import synth  # noqa: E402
+import synth  # noqa: E402
 from paper_2503_10325_b200.sharding import vocab_shard  # noqa: E402
 
 
