@@ -24,7 +24,7 @@ INFO_DEGENERATE = 0x100
 
 __all__ = [
     "build", "lib", "philox4x32_10", "uniform", "invcdf", "softmax", "residual",
-    "verify_batch", "verify_batch_parallel", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step", "route_update", "tree_select",
+    "verify_batch", "verify_batch_parallel", "by_request", "fuse_drafts", "sample_residual", "verify_tree", "fuse_step", "route_update", "tree_select",
     "TAG_ACCEPT", "TAG_SAMPLE", "TAG_FUSE", "TAG_TREE_GEN",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE",
     "DRAFT_PROBS", "DRAFT_LOGITS", "ST_OK", "ST_ZERO_PROB", "ST_TOKEN_RANGE",
@@ -169,27 +169,31 @@ def verify_batch(target, draft, draft_tokens, request_ids, *, temperature=1.0, s
     return out
 
 
-def verify_batch_parallel(target, draft, draft_tokens, request_ids, *, threads=None, draft_len=None,
-                          **kw):
-    """verify_batch over request slices on `threads` host threads (default: all cores).
-
-    Requests are independent (Alg. 2 "foreach draft ... in parallel") and every random
-    draw is keyed by the global request id (reading #8), so the slices' results are exactly the
-    whole batch's; ctypes releases the GIL inside the C oracle, so the slices run concurrently.
-    Same arguments and result as verify_batch."""
+def by_request(fn, *batch_args, threads=None, **kw):
+    """fn(*slices, **kw) over single-request slices of the batch-major arguments (None stays
+    None) on `threads` host threads (default: all cores); the per-request result dicts are
+    concatenated.  Requests are independent (Alg. 2 "foreach draft ... in parallel") and
+    every random draw is keyed by the global request id (reading #8), so the result equals the
+    whole-batch call; ctypes releases the GIL inside the C oracle, so requests run concurrently
+    and only `threads` requests are converted to fp64 at a time."""
     from concurrent.futures import ThreadPoolExecutor
-    B = int(target.shape[0])
+    B = int(batch_args[0].shape[0])
     threads = max(1, min(B, threads or os.cpu_count() or 1))
-    edges = [B * j // threads for j in range(threads + 1)]
 
-    def part(j):
-        sl = slice(edges[j], edges[j + 1])
-        return verify_batch(target[sl], draft[sl], draft_tokens[sl], request_ids[sl],
-                            draft_len=None if draft_len is None else draft_len[sl], **kw)
+    def one(b):
+        return fn(*[None if a is None else a[b:b + 1] for a in batch_args], **kw)
 
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        parts = list(ex.map(part, [j for j in range(threads) if edges[j + 1] > edges[j]]))
+        parts = list(ex.map(one, range(B)))
     return {n: np.concatenate([r[n] for r in parts]) for n in parts[0]}
+
+
+def verify_batch_parallel(target, draft, draft_tokens, request_ids, *, threads=None, draft_len=None,
+                          **kw):
+    """verify_batch, one request per task on `threads` host threads (by_request)."""
+    def fn(t, d, x, r, dl):
+        return verify_batch(t, d, x, r, draft_len=dl, **kw)
+    return by_request(fn, target, draft, draft_tokens, request_ids, draft_len, threads=threads)
 
 
 def fuse_drafts(draft, draft_tokens, request_ids, *, temperature=1.0, seed=0, step=0,

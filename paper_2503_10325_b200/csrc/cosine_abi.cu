@@ -60,6 +60,7 @@ struct cosine_ctx_s {
   PartRec* parts = nullptr;
   PosDec* pdec = nullptr;
   int32_t* counters = nullptr;
+  size_t counters_bytes = 0;
   NodeDec* ndec = nullptr;
   ChildPQ* cpq = nullptr;
   double* segsum = nullptr;
@@ -228,6 +229,10 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
+    // a later launch failed after stats_kernel was enqueued: its per-unit counts must not leak
+    // into the next call (the dependents reset them); clear the counter block on the stream
+    cudaMemsetAsync(ctx->counters, 0, ctx->counters_bytes, stream);
+    cudaGetLastError();
     ctx->last_launches = 0;
     return fail(ctx, COSINE_ERR_CUDA, std::string("verify kernels: ") + cudaGetErrorString(e));
   }
@@ -306,8 +311,12 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
     lc.numAttrs = 0;
     e = cudaLaunchKernelEx(&lc, shard_finish_kernel, S);
   }
-  if (e != cudaSuccess) {
+  if (e != cudaSuccess || r != ncclSuccess) {  // (as in launch_split3)
     cudaGetLastError();
+    cudaMemsetAsync(ctx->counters, 0, ctx->counters_bytes, stream);
+    cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
     ctx->last_launches = 0;
     return fail(ctx, COSINE_ERR_CUDA, std::string("sharded verify (") + stage + "): " + cudaGetErrorString(e));
   }
@@ -368,6 +377,9 @@ cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& 
     launches += 1;
   }
   if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaMemsetAsync(ctx->counters, 0, ctx->counters_bytes, stream);  // (as in launch_split3)
+    cudaMemsetAsync(ctx->lz, 0, (size_t)std::max(ctx->cfg.max_batch, 1) * sizeof(int32_t), stream);
     cudaGetLastError();
     ctx->last_launches = 0;
     return fail(ctx, COSINE_ERR_CUDA, std::string("lazy verify kernels: ") + cudaGetErrorString(e));
@@ -461,6 +473,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   if (e == cudaSuccess) e = cudaMalloc(&ctx->pdec, nu * sizeof(PosDec));
   // counters: [B] kernel-B CTAs per request | [B] decided units per request | [B][k+1] chunks per unit
   const size_t ncnt = 2 * nb + nb * (size_t)(cfg->max_draft_len + 1);
+  ctx->counters_bytes = ncnt * sizeof(int32_t);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->counters, ncnt * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->lz, nb * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, ncnt * sizeof(int32_t));

@@ -38,8 +38,9 @@ def test_fuse_drafts(cuda_ok, wm, sm):
     np.testing.assert_allclose(fq.cpu().numpy()[..., :V], r["fused_q"], rtol=1e-5, atol=1e-9)
 
 
-@pytest.mark.parametrize("with_stats,with_draft", [(False, True), (True, True), (False, False)])
-def test_sample_residual(cuda_ok, with_stats, with_draft):
+@pytest.mark.parametrize("with_stats,with_draft,T", [(False, True, 1.0), (True, True, 1.0), (False, False, 1.0),
+                                                     (True, True, 0.7), (True, False, 0.7), (False, True, 0.7)])
+def test_sample_residual(cuda_ok, with_stats, with_draft, T):
     import paper_2503_10325_b200 as cv
     B, N, V = 64, 3, 5003
     inp = synth.linear_inputs(B, 1, N, V, dtype=torch.bfloat16, seed=300)
@@ -54,11 +55,12 @@ def test_sample_residual(cuda_ok, with_stats, with_draft):
     if with_stats:
         l = rows[:, :V].double()
         rm = l.max(-1).values.float()
-        rs = torch.exp(l - rm.double()[:, None]).sum(-1).float()
+        rs = torch.exp((l - rm.double()[:, None]) / T).sum(-1).float()
     ctx = cv.cosine_verify_init(V, max_batch=B, max_draft_len=1, max_drafters=N, seed=9)
     y = torch.empty(B, dtype=torch.int32, device=dev)
     st = torch.empty(B, dtype=torch.int32, device=dev)
     cv.cosine_sample_residual(ctx, rows.to(dev), nodes.to(dev), inp["request_ids"].to(dev), y, st, step=4,
+                              temperature=T,
                               row_max=None if rm is None else rm.to(dev),
                               row_sumexp=None if rs is None else rs.to(dev),
                               draft_rows=drafts.to(dev) if with_draft else None,
@@ -66,7 +68,7 @@ def test_sample_residual(cuda_ok, with_stats, with_draft):
                               draft_norm=norms.to(dev) if with_draft else None)
     torch.cuda.synchronize()
     r = oracle.sample_residual(rows, nodes.numpy().astype(np.uint32), inp["request_ids"], seed=9, step=4,
-                               row_max=rm, row_sumexp=rs, draft=drafts if with_draft else None,
+                               temperature=T, row_max=rm, row_sumexp=rs, draft=drafts if with_draft else None,
                                weights=wts if with_draft else None, draft_norm=norms if with_draft else None,
                                vocab=V)
     cv.cosine_verify_destroy(ctx)
@@ -74,3 +76,40 @@ def test_sample_residual(cuda_ok, with_stats, with_draft):
     yy = y.cpu().numpy()
     assert not ((yy != r["out_token"]) & ~flagged).any()
     np.testing.assert_array_equal(st.cpu().numpy() & 0xff, r["status"] & 0xff)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_sample_residual_degenerate_fallback(cuda_ok, dtype):
+    # q == o exactly (reading #11): a two-point target o = (1/2, 1/2) at tokens 3 and V - 5 and
+    # drafter rows carrying the same two masses (two drafters, weights 1/2 each): the residual has no
+    # mass on either side, the draw falls back to o over the whole row and is flagged DEGENERATE
+    import paper_2503_10325_b200 as cv
+    B, N, V = 48, 2, 20001
+    dev = torch.device("cuda", 0)
+    ld = (V + 7) // 8 * 8
+    rows = torch.full((B, ld), float("-inf"), dtype=dtype)
+    rows[:, 3] = 0.0
+    rows[:, V - 5] = 0.0
+    rows[:, V:] = float("nan")
+    drafts = torch.zeros(B, N, ld, dtype=dtype)
+    drafts[:, :, 3] = 0.5
+    drafts[:, :, V - 5] = 0.5
+    drafts[:, :, V:] = float("nan")
+    wts = torch.full((B, N), 0.5)
+    norms = torch.ones(B, N)
+    nodes = torch.arange(B, dtype=torch.int32) % 5
+    rid = torch.arange(1000, 1000 + B, dtype=torch.int64)
+    ctx = cv.cosine_verify_init(V, max_batch=B, max_draft_len=1, max_drafters=N, seed=13, target_dtype=dtype,
+                                draft_dtype=dtype)
+    y = torch.empty(B, dtype=torch.int32, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    cv.cosine_sample_residual(ctx, rows.to(dev), nodes.to(dev), rid.to(dev), y, st, step=1,
+                              draft_rows=drafts.to(dev), weights=wts.to(dev), draft_norm=norms.to(dev))
+    torch.cuda.synchronize()
+    cv.cosine_verify_destroy(ctx)
+    r = oracle.sample_residual(rows, nodes.numpy().astype(np.uint32), rid, seed=13, step=1, draft=drafts,
+                               weights=wts, draft_norm=norms, vocab=V)
+    assert (r["status"] & oracle.INFO_DEGENERATE).all()
+    np.testing.assert_array_equal(y.cpu().numpy(), r["out_token"])
+    assert ((st.cpu().numpy() & cv.INFO_DEGENERATE) != 0).all()
+    assert set(np.unique(r["out_token"])) <= {3, V - 5}

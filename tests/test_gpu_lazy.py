@@ -46,9 +46,8 @@ def test_lazy_c3_full_size(cuda_ok):
     full = parity.gpu_verify(inp)
     lazy = parity.gpu_verify(inp, lazy=True)
     _same(lazy, full)
-    subset = np.arange(0, cfg["B"], 37)
-    r = parity.oracle_verify(inp, subset=torch.as_tensor(subset))
-    parity.compare(lazy, r, subset=subset, check_probs=False)
+    r = parity.oracle_verify(inp)  # every request
+    parity.compare(lazy, r, check_probs=False, name="c3 lazy")
 
 
 @pytest.mark.gpu

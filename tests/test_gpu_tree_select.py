@@ -36,8 +36,19 @@ def test_tree_select_matches_oracle(cuda_ok, S, K, vocab, budget):
     C = torch.rand(B, S, K, generator=g) * 0.9 + 0.05
     r = oracle.tree_select(X, C.double(), budget)
     o = _gpu(X, C, budget)
+    # near ties: the GPU ranks fp32 products of confidences, the oracle fp64 ones.  A request is
+    # flagged when two nodes adjacent in the oracle's full ranking (budget = every node) have
+    # scores within 2e-6 relative (> K fp32 roundings); its order may legitimately differ
+    full = oracle.tree_select(X, C.double(), S * K)
+    flagged = np.zeros(B, bool)
+    for b in range(B):
+        sc = np.sort(full["score"][b, 1:full["n_nodes"][b]])[::-1]
+        if sc.size > 1 and (np.abs(np.diff(sc)) <= 2e-6 * sc[1:]).any():
+            flagged[b] = True
+    assert flagged.sum() <= max(1, 0.05 * B), flagged.sum()
     np.testing.assert_array_equal(o["n_nodes"], r["n_nodes"])
-    np.testing.assert_array_equal(o["parent"], r["parent"])
-    np.testing.assert_array_equal(o["token"], r["token"])
-    np.testing.assert_array_equal(o["depth"], r["depth"])
-    np.testing.assert_allclose(o["score"], r["score"], rtol=1e-6)
+    ok = ~flagged
+    np.testing.assert_array_equal(o["parent"][ok], r["parent"][ok])
+    np.testing.assert_array_equal(o["token"][ok], r["token"][ok])
+    np.testing.assert_array_equal(o["depth"][ok], r["depth"][ok])
+    np.testing.assert_allclose(o["score"][ok], r["score"][ok], rtol=1e-6)

@@ -419,6 +419,67 @@ def test_sample_residual_matches_verify_path():
     np.testing.assert_array_equal(sb["out_token"], r["out_tokens"][~has_rej, k])
 
 
+def _scipy_residual_draw(l, T, d, w, sig, u):
+    """The final draw of P:132 from library routines: o = scipy softmax(l / T), q = sum_n w_n d_n /
+    sigma_n, r = max(0, o - q), y = the smallest v with cumsum(r)[v] > u * sum(r) (reading #10)."""
+    import scipy.special
+    o = scipy.special.softmax(l / T)
+    q = (w[:, None] * d / sig[:, None]).sum(0)
+    r = np.maximum(o - q, 0.0)
+    Z = r.sum()
+    return int(np.searchsorted(np.cumsum(r), u * Z, side="right")), Z
+
+
+def test_sample_residual_caller_stats_branch_at_T07():
+    # the caller-supplied row statistics branch (M = max l, S = sum exp((l - M) / T)) at T != 1:
+    # the draw must be the one from scipy's softmax at the same T (a misplaced / T, a wrong sign or
+    # a dropped normaliser moves the draw or Z)
+    import scipy.special
+    rng = np.random.default_rng(31)
+    B, N, V, T = 64, 3, 40, 0.7
+    l = rng.normal(size=(B, V)) * 2.5
+    d = rng.dirichlet(np.ones(V) * 0.7, size=(B, N))
+    sig = d.sum(-1)
+    w = rng.dirichlet(np.ones(N), size=B)
+    M = l.max(-1)
+    S = np.exp(scipy.special.logsumexp(l / T, axis=-1) - M / T)
+    nid = rng.integers(0, 9, size=B).astype(np.uint32)
+    rid = np.arange(100, 100 + B)
+    r = oracle.sample_residual(l, nid, rid, temperature=T, seed=9, step=2, row_max=M, row_sumexp=S, draft=d,
+                               weights=w, draft_norm=sig)
+    r0 = oracle.sample_residual(l, nid, rid, temperature=T, seed=9, step=2, draft=d, weights=w, draft_norm=sig)
+    for b in range(B):
+        u = oracle.uniform(9, int(rid[b]), int(nid[b]), 2, oracle.TAG_SAMPLE)
+        y, Z = _scipy_residual_draw(l[b], T, d[b], w[b], sig[b], u)
+        if r["tie_margin"][b] >= 1e-9:
+            assert r["out_token"][b] == y, b
+        assert abs(r["Z"][b] - Z) <= 1e-12 * max(1.0, Z)
+    np.testing.assert_array_equal(r["out_token"], r0["out_token"])  # both branches agree
+    # bonus (no drafter rows) through the caller-stats branch: a draw from softmax(l / T)
+    rb = oracle.sample_residual(l, nid, rid, temperature=T, seed=9, step=2, row_max=M, row_sumexp=S)
+    for b in range(B):
+        u = oracle.uniform(9, int(rid[b]), int(nid[b]), 2, oracle.TAG_SAMPLE)
+        o = scipy.special.softmax(l[b] / T)
+        assert rb["out_token"][b] == int(np.searchsorted(np.cumsum(o), u, side="right"))
+
+
+def test_sample_residual_degenerate_falls_back_to_target():
+    # q == o exactly (a two-point target, a drafter row carrying the same two masses): the
+    # residual has no mass, the draw falls back to o (reading #11) and is flagged
+    B, V = 32, 16
+    l = np.full((B, V), -np.inf)
+    l[:, 3] = 0.0
+    l[:, 11] = 0.0  # o = (1/2 at 3, 1/2 at 11)
+    d = np.zeros((B, 1, V))
+    d[:, 0, 3] = d[:, 0, 11] = 0.5
+    r = oracle.sample_residual(l, np.zeros(B, np.uint32), np.arange(B), seed=4, draft=d,
+                               weights=np.ones((B, 1)), draft_norm=np.ones((B, 1)))
+    assert (r["status"] & oracle.INFO_DEGENERATE).all()
+    for b in range(B):
+        u = oracle.uniform(4, b, 0, 0, oracle.TAG_SAMPLE)
+        assert r["out_token"][b] == (3 if u < 0.5 else 11)
+
+
 # --------------------------------------------------------------------------- tree
 def test_chain_tree_equals_linear():
     # a chain tree is the linear path, bit for bit under the same Philox stream
