@@ -19,13 +19,15 @@ from ._lib import (  # noqa: F401
     cosine_verify_destroy,
     cosine_verify_init,
     cosine_verify_tree,
+    cosine_verify_init_vgroup,
+    cosine_verify_batch_vgroup,
 )
 
 __all__ = [
     "Verifier", "cosine_verify_init", "cosine_verify_destroy", "cosine_fuse_drafts",
     "cosine_verify_batch", "cosine_sample_residual", "cosine_verify_tree", "cosine_last_launch_count",
     "cosine_nccl_unique_id", "cosine_verify_batch_lazy", "cosine_fuse_step",
-    "cosine_route_update", "cosine_tree_select",
+    "cosine_route_update", "cosine_tree_select", "cosine_verify_init_vgroup", "cosine_verify_batch_vgroup",
     "CosineError",
     "W_CONF", "W_WINNER", "W_UNIFORM", "W_POINT", "SEL_ARGMAX", "SEL_SAMPLE", "DRAFT_PROBS",
     "DRAFT_LOGITS",

@@ -85,6 +85,12 @@ _lib.cosine_route_update.restype = ctypes.c_int
 _lib.cosine_tree_select.argtypes = [_P, _P, _i32, _i32, _i32, _P, _P, _i32, _P, _P, _P, _P, _P]
 _lib.cosine_tree_select.restype = ctypes.c_int
 _lib.cosine_verify_tree_lazy.restype = ctypes.c_int
+_lib.cosine_verify_init_vgroup.argtypes = [ctypes.POINTER(cosine_config_t), _i32, ctypes.POINTER(_P)]
+_lib.cosine_verify_init_vgroup.restype = ctypes.c_int
+_lib.cosine_verify_batch_vgroup.argtypes = [ctypes.POINTER(_P), _i32, _P, _i32, _i32, _i32, ctypes.POINTER(_P), _i64,
+                                            _f32, ctypes.POINTER(_P), _i64, _P, _P, _P, _u32, ctypes.c_int,
+                                            ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)]
+_lib.cosine_verify_batch_vgroup.restype = ctypes.c_int
 _lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
 _lib.cosine_nccl_unique_id.restype = ctypes.c_int
 _lib.cosine_profile_enable.argtypes = [_P, _i32]
@@ -97,7 +103,8 @@ EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_
                     "cosine_last_launch_count", "cosine_profile_enable", "cosine_profile_read",
                     "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
                     "cosine_verify_tree_lazy", "cosine_fuse_step",
-                    "cosine_route_update", "cosine_tree_select")
+                    "cosine_route_update", "cosine_tree_select", "cosine_verify_init_vgroup",
+                    "cosine_verify_batch_vgroup")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -170,6 +177,40 @@ def cosine_verify_init(vocab_size: int, *, device: int = 0, max_batch: int, max_
     h = _P()
     _check(_lib.cosine_verify_init(ctypes.byref(cfg), ctypes.byref(h)), None)
     return Context(h, cfg)
+
+
+def cosine_verify_init_vgroup(vocab_size: int, shards, *, device: int = 0, max_batch: int, max_draft_len: int,
+                              max_drafters: int, target_dtype=torch.bfloat16, draft_dtype=torch.bfloat16,
+                              draft_kind: int = DRAFT_PROBS, seed: int = 0, cluster_size: int = 0):
+    """G contexts of a virtual vocabulary-sharded group on one device (test / diagnostic):
+    shards = [(begin, end)] per rank, tiling [0, vocab_size) in rank order."""
+    G = len(shards)
+    cfgs = (cosine_config_t * G)()
+    for g, (b, e) in enumerate(shards):
+        cfgs[g] = cosine_config_t(device=device, vocab_size=vocab_size, vocab_begin=b, vocab_end=e,
+                                  max_batch=max_batch, max_draft_len=max_draft_len, max_drafters=max_drafters,
+                                  max_tree_nodes=0, target_dtype=_DT[target_dtype], draft_dtype=_DT[draft_dtype],
+                                  draft_kind=draft_kind, seed=seed, nranks=G, rank=g, nccl_unique_id=None,
+                                  cluster_size=cluster_size)
+    hs = (_P * G)()
+    _check(_lib.cosine_verify_init_vgroup(cfgs, G, hs), None)
+    return [Context(_P(hs[g]), cfgs[g]) for g in range(G)]
+
+
+def cosine_verify_batch_vgroup(ctxs, targets, drafts, draft_tokens, request_ids, accept_lens, out_tokens, statuses,
+                               *, temperature=1.0, draft_len=None, step=0, weight_mode=W_CONF, stream=None):
+    """The collective sharded call of a virtual group: targets[g] [B][k+1][ld_t] / drafts[g]
+    [B][k][N][ld_q] are rank g's column shards; outputs per rank."""
+    G = len(ctxs)
+    B, kp1, ld_t = targets[0].shape
+    N, ld_q = drafts[0].shape[2], drafts[0].shape[3]
+    arr = lambda ts: (_P * G)(*[t.data_ptr() for t in ts])
+    hs = (_P * G)(*[c._as_parameter_ for c in ctxs])
+    rc = _lib.cosine_verify_batch_vgroup(hs, G, _stream(stream, targets[0].device), B, kp1 - 1, N, arr(targets),
+                                         ld_t, temperature, arr(drafts), ld_q, _ptr(draft_tokens), _ptr(draft_len),
+                                         _ptr(request_ids), step, weight_mode, arr(accept_lens), arr(out_tokens),
+                                         arr(statuses))
+    _check(rc, ctxs[0])
 
 
 def cosine_verify_destroy(ctx) -> None:

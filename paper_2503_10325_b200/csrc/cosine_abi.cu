@@ -39,6 +39,8 @@ __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
   if (j < n) { done[j] = 0; first_rej[j] = kNoReject; }
 }
 
+constexpr int kMaxShardSlices = 8;  // request slices of the vocabulary-sharded call
+
 void kernel_set(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, KernelSet* ks) {
   if (tt == COSINE_BF16 && tq == COSINE_BF16) kernel_set_bb(logits, N, ks);
   else if (tt == COSINE_BF16 && tq == COSINE_F32) kernel_set_bf(logits, N, ks);
@@ -84,6 +86,11 @@ struct cosine_ctx_s {
   double* zall = nullptr;
   YRec* ysend = nullptr;
   YRec* yall = nullptr;
+  // sliced exchange: the slices' all-gathers and B phase run on `aux` while `stream` streams the
+  // next slice's statistics (fork / join by events)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t sev[kMaxShardSlices + 1] = {};
+  bool vgroup = false;  // a cosine_verify_init_vgroup context (device copies instead of NCCL)
 };
 
 static thread_local std::string g_init_error;
@@ -250,14 +257,19 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   return launch_split3(ctx, stream, S, ks);
 }
 
-// Vocabulary-sharded verification (cosine_shard.cuh): 7 kernels and 3 all-gathers on `stream`.
-cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, cosine_dtype_t tt,
-                             cosine_dtype_t tq, bool logits) {
-  KernelSet ks;
-  kernel_set(tt, tq, logits, S.N, &ks);
+// ---------------------------------------------------------------------------------------
+// Vocabulary-sharded verification (cosine_shard.cuh).  The batch is cut into request slices;
+// each slice runs the same four phases with three exchanges between them:
+//   A: stats_kernel (local columns) -> shard_pack_kernel      X1: records   [G][units][words]
+//   B: shard_decide_kernel -> resample_kernel (local masses)  X2: masses    [G][B] doubles
+//   C: shard_sample_kernel (the owner of t scans)             X3: tokens    [G][B] YRec
+//   D: shard_finish_kernel (replicated outputs)
+// A slice is a view of the call with every per-request pointer (inputs, outputs, diagnostics,
+// scratch, exchange regions) offset to its first request, so every kernel sees a smaller batch.
+// ---------------------------------------------------------------------------------------
+void shard_setup(cosine_ctx_t ctx, SplitParams& S) {
   const int64_t units = (int64_t)S.B * (S.k + 1);
-  const int C = stats_chunks(ctx, units, S.ngroups);
-  fill_scratch(ctx, S, C);
+  fill_scratch(ctx, S, stats_chunks(ctx, units, S.ngroups));
   S.fused = 0;
   S.shard = 1;
   S.G = ctx->cfg.nranks;
@@ -271,61 +283,215 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   S.zall = ctx->zall;
   S.ysend = ctx->ysend;
   S.yall = ctx->yall;
-  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
-    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+}
+
+// The view of requests [b0, b0 + nb) of a (set-up) call.
+SplitParams shard_slice(const SplitParams& F, int b0, int nb, size_t tsz, size_t qsz) {
+  SplitParams S = F;
+  const int64_t kp1 = F.k + 1, k = F.k, N = F.N, G = F.G;
+  const int64_t u0 = (int64_t)b0 * kp1;
+  S.B = nb;
+  S.nb = nb;
+  S.target = (const char*)F.target + (size_t)(u0 * F.ld_t) * tsz;
+  S.draft = (const char*)F.draft + (size_t)((int64_t)b0 * k * N * F.ld_q) * qsz;
+  S.draft_tokens = F.draft_tokens + (int64_t)b0 * k * N;
+  if (F.draft_len) S.draft_len = F.draft_len + b0;
+  S.rids = F.rids + b0;
+  S.accept_len = F.accept_len + b0;
+  S.out_tokens = F.out_tokens + u0;
+  S.status = F.status + b0;
+  cosine_debug_t& D = S.dbg;
+  if (D.p_x) D.p_x += (int64_t)b0 * k;
+  if (D.q_x) D.q_x += (int64_t)b0 * k;
+  if (D.accept_u) D.accept_u += (int64_t)b0 * k;
+  if (D.row_max) D.row_max += u0;
+  if (D.row_sumexp) D.row_sumexp += u0;
+  if (D.draft_norm) D.draft_norm += (int64_t)b0 * k * N;
+  if (D.conf) D.conf += (int64_t)b0 * k * N;
+  if (D.weights) D.weights += (int64_t)b0 * k * N;
+  if (D.fused_tokens) D.fused_tokens += (int64_t)b0 * k;
+  if (D.residual_mass) D.residual_mass += b0;
+  if (D.tie_margin) D.tie_margin += b0;
+  S.parts = F.parts + u0 * F.C;
+  S.pdec = F.pdec + u0;
+  S.segsum = F.segsum + (int64_t)b0 * F.nseg;
+  S.counters = F.counters + b0;
+  S.rec_send = F.rec_send + u0 * F.rec_words;
+  S.rec_all = F.rec_all + G * u0 * F.rec_words;  // [G][nb (k+1)][words]
+  S.zsend = F.zsend + b0;
+  S.zall = F.zall + G * b0;  // [G][nb]
+  S.ysend = F.ysend + b0;
+  S.yall = F.yall + G * b0;  // [G][nb]
+  return S;
+}
+
+int shard_slices(int B) { return B >= 256 ? 4 : (B >= 64 ? 2 : 1); }
+
+struct ShardLaunch {
   cudaLaunchConfig_t lc;
-  memset(&lc, 0, sizeof(lc));
-  lc.blockDim = dim3(kThreads, 1, 1);
-  lc.stream = stream;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  const unsigned unit_blocks = (unsigned)((units + kWarps - 1) / kWarps);
-  auto launch = [&](SplitFn f, unsigned grid, bool pdl) {
+  explicit ShardLaunch(cudaStream_t s) {
+    memset(&lc, 0, sizeof(lc));
+    lc.blockDim = dim3(kThreads, 1, 1);
+    lc.stream = s;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cudaError_t operator()(SplitFn f, unsigned grid, bool pdl, const SplitParams& S) {
     lc.gridDim = dim3(grid, 1, 1);
     lc.attrs = pdl ? at : nullptr;
     lc.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&lc, f, S);
-  };
-  const char* stage = "stats";
+  }
+};
+
+// Phase A of a slice: local statistics and the slice's records.
+cudaError_t shard_phase_a(cosine_ctx_t ctx, cudaStream_t s, const SplitParams& S, const KernelSet& ks,
+                          const char** stage) {
+  ShardLaunch L(s);
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  *stage = "stats";
   const auto pe = prof_events(ctx);
-  if (pe.first) cudaEventRecord(pe.first, stream);
-  cudaError_t e = launch(ks.stats, (unsigned)(units * C), false);  // local row statistics
-  if (pe.second) cudaEventRecord(pe.second, stream);
-  if (e == cudaSuccess) { stage = "pack"; e = launch(ks.shard_pack, unit_blocks, pe.second == nullptr); }
-  ncclResult_t r = ncclSuccess;
+  if (pe.first) cudaEventRecord(pe.first, s);
+  cudaError_t e = L(ks.stats, (unsigned)(units * S.C), false, S);
+  if (pe.second) cudaEventRecord(pe.second, s);
   if (e == cudaSuccess) {
-    r = ncclAllGather(ctx->rec_send, ctx->rec_all, (size_t)units * S.rec_words * 4, ncclUint8, ctx->comm, stream);
+    *stage = "pack";
+    e = L(ks.shard_pack, (unsigned)((units + kWarps - 1) / kWarps), pe.second == nullptr, S);
   }
-  if (e == cudaSuccess && r == ncclSuccess) { stage = "decide"; e = launch(logits ? shard_decide_kernel<true> : shard_decide_kernel<false>, unit_blocks, false); }
-  if (e == cudaSuccess && r == ncclSuccess) { stage = "resample"; e = launch(ks.resample, (unsigned)(S.B * S.spr), false); }
-  if (e == cudaSuccess && r == ncclSuccess)
-    r = ncclAllGather(ctx->zsend, ctx->zall, (size_t)S.B * sizeof(double), ncclUint8, ctx->comm, stream);
-  if (e == cudaSuccess && r == ncclSuccess) { stage = "sample"; e = launch(ks.shard_sample, (unsigned)S.B, false); }
-  if (e == cudaSuccess && r == ncclSuccess)
-    r = ncclAllGather(ctx->ysend, ctx->yall, (size_t)S.B * sizeof(YRec), ncclUint8, ctx->comm, stream);
-  if (e == cudaSuccess && r == ncclSuccess) {
-    stage = "finish";
-    lc.gridDim = dim3((unsigned)((S.B + kThreads - 1) / kThreads), 1, 1);
-    lc.attrs = nullptr;
-    lc.numAttrs = 0;
-    e = cudaLaunchKernelEx(&lc, shard_finish_kernel, S);
+  return e;
+}
+// Phase B: decisions from the gathered records, local masses of the final draw.
+cudaError_t shard_phase_b(cudaStream_t s, const SplitParams& S, const KernelSet& ks, bool logits, const char** stage) {
+  ShardLaunch L(s);
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  *stage = "decide";
+  cudaError_t e = L(logits ? shard_decide_kernel<true> : shard_decide_kernel<false>,
+                    (unsigned)((units + kWarps - 1) / kWarps), false, S);
+  if (e == cudaSuccess) {
+    *stage = "resample";
+    e = L(ks.resample, (unsigned)(S.B * S.spr), true, S);
   }
-  if (e != cudaSuccess || r != ncclSuccess) {  // (as in launch_split3)
-    cudaGetLastError();
-    cudaMemsetAsync(ctx->counters, 0, ctx->counters_bytes, stream);
-    cudaGetLastError();
-  }
-  if (e != cudaSuccess) {
-    ctx->last_launches = 0;
+  return e;
+}
+cudaError_t shard_phase_c(cudaStream_t s, const SplitParams& S, const KernelSet& ks, const char** stage) {
+  ShardLaunch L(s);
+  *stage = "sample";
+  return L(ks.shard_sample, (unsigned)S.B, false, S);
+}
+cudaError_t shard_phase_d(cudaStream_t s, const SplitParams& S, const char** stage) {
+  ShardLaunch L(s);
+  *stage = "finish";
+  return L(shard_finish_kernel, (unsigned)((S.B + kThreads - 1) / kThreads), false, S);
+}
+size_t shard_x_bytes(const SplitParams& S, int x) {  // bytes one rank contributes to exchange x
+  if (x == 1) return (size_t)S.B * (S.k + 1) * S.rec_words * 4;
+  if (x == 2) return (size_t)S.B * sizeof(double);
+  return (size_t)S.B * sizeof(YRec);
+}
+ncclResult_t shard_allgather(cosine_ctx_t ctx, cudaStream_t s, const SplitParams& S, int x) {
+  const void* src = x == 1 ? (const void*)S.rec_send : (x == 2 ? (const void*)S.zsend : (const void*)S.ysend);
+  void* dst = x == 1 ? (void*)S.rec_all : (x == 2 ? (void*)S.zall : (void*)S.yall);
+  return ncclAllGather(src, dst, shard_x_bytes(S, x), ncclUint8, ctx->comm, s);
+}
+
+cosine_status_t shard_fail(cosine_ctx_t ctx, cudaStream_t s, cudaError_t e, ncclResult_t r, const char* stage) {
+  cudaGetLastError();
+  cudaMemsetAsync(ctx->counters, 0, ctx->counters_bytes, s);  // (as in launch_split3)
+  cudaGetLastError();
+  ctx->last_launches = 0;
+  if (e != cudaSuccess)
     return fail(ctx, COSINE_ERR_CUDA, std::string("sharded verify (") + stage + "): " + cudaGetErrorString(e));
+  return fail(ctx, COSINE_ERR_NCCL, std::string("sharded verify all-gather: ") + ncclGetErrorString(r));
+}
+
+// One rank's collective call (NCCL).  Slice c's phase A runs on `stream`; its exchanges and
+// phases B-D on the context's aux stream, overlapping slice c + 1's statistics.
+cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& F, cosine_dtype_t tt,
+                             cosine_dtype_t tq, bool logits) {
+  KernelSet ks;
+  kernel_set(tt, tq, logits, F.N, &ks);
+  shard_setup(ctx, F);
+  if ((size_t)F.B * (size_t)F.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  const int nsl = shard_slices(F.B);
+  const int per = (F.B + nsl - 1) / nsl;
+  const size_t tsz = esize(tt), qsz = esize(tq);
+  const char* stage = "fork";
+  cudaError_t e = cudaEventRecord(ctx->sev[kMaxShardSlices], stream);  // aux follows the caller's stream
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->sev[kMaxShardSlices], 0);
+  ncclResult_t r = ncclSuccess;
+  int launches = 0;
+  for (int c = 0; c < nsl && e == cudaSuccess && r == ncclSuccess; ++c) {
+    const int b0 = c * per, nb = std::min(per, F.B - b0);
+    if (nb <= 0) break;
+    const SplitParams S = shard_slice(F, b0, nb, tsz, qsz);
+    e = shard_phase_a(ctx, stream, S, ks, &stage);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->sev[c], stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->sev[c], 0);
+    if (e == cudaSuccess) r = shard_allgather(ctx, ctx->aux, S, 1);
+    if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_b(ctx->aux, S, ks, logits, &stage);
+    if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, ctx->aux, S, 2);
+    if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_c(ctx->aux, S, ks, &stage);
+    if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, ctx->aux, S, 3);
+    if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_d(ctx->aux, S, &stage);
+    launches += 6;
   }
-  if (r != ncclSuccess) {
-    ctx->last_launches = 0;
-    return fail(ctx, COSINE_ERR_NCCL, std::string("sharded verify all-gather: ") + ncclGetErrorString(r));
+  if (e == cudaSuccess && r == ncclSuccess) {  // join: the caller's stream waits for the outputs
+    stage = "join";
+    e = cudaEventRecord(ctx->sev[kMaxShardSlices], ctx->aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ctx->sev[kMaxShardSlices], 0);
   }
-  ctx->last_launches = 7;
-  ctx->last_cluster = C;
+  if (e != cudaSuccess || r != ncclSuccess) return shard_fail(ctx, stream, e, r, stage);
+  ctx->last_launches = launches;
+  ctx->last_cluster = F.C;
+  return COSINE_OK;
+}
+
+// The call of a virtual group (cosine_verify_batch_vgroup): G contexts, one stream, phase by
+// phase over all ranks, each exchange done by device copies into every rank's gather buffer in
+// rank order — the same kernels, slices and record layouts as launch_shard.
+cosine_status_t launch_shard_vgroup(const cosine_ctx_t* ctxs, int G, cudaStream_t stream, SplitParams* F,
+                                    cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+  KernelSet ks;
+  kernel_set(tt, tq, logits, F[0].N, &ks);
+  for (int g = 0; g < G; ++g) {
+    shard_setup(ctxs[g], F[g]);
+    if ((size_t)F[g].B * (size_t)F[g].nseg > ctxs[g]->segsum_cap)
+      return fail(ctxs[g], COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  }
+  const int B = F[0].B;
+  const int nsl = shard_slices(B);
+  const int per = (B + nsl - 1) / nsl;
+  const size_t tsz = esize(tt), qsz = esize(tq);
+  const char* stage = "stats";
+  cudaError_t e = cudaSuccess;
+  std::vector<SplitParams> S(G);
+  auto exchange = [&](int x) {
+    for (int g = 0; g < G && e == cudaSuccess; ++g) {
+      const size_t n = shard_x_bytes(S[g], x);
+      const void* src = x == 1 ? (const void*)S[g].rec_send
+                               : (x == 2 ? (const void*)S[g].zsend : (const void*)S[g].ysend);
+      for (int h = 0; h < G && e == cudaSuccess; ++h) {
+        char* dst = (char*)(x == 1 ? (void*)S[h].rec_all : (x == 2 ? (void*)S[h].zall : (void*)S[h].yall));
+        e = cudaMemcpyAsync(dst + (size_t)g * n, src, n, cudaMemcpyDeviceToDevice, stream);
+      }
+    }
+  };
+  for (int c = 0; c < nsl && e == cudaSuccess; ++c) {
+    const int b0 = c * per, nb = std::min(per, B - b0);
+    if (nb <= 0) break;
+    for (int g = 0; g < G; ++g) S[g] = shard_slice(F[g], b0, nb, tsz, qsz);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_a(ctxs[g], stream, S[g], ks, &stage);
+    exchange(1);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_b(stream, S[g], ks, logits, &stage);
+    exchange(2);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_c(stream, S[g], ks, &stage);
+    exchange(3);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_d(stream, S[g], &stage);
+  }
+  if (e != cudaSuccess) return shard_fail(ctxs[0], stream, e, ncclSuccess, stage);
+  for (int g = 0; g < G; ++g) ctxs[g]->last_launches = 6 * nsl;
   return COSINE_OK;
 }
 
@@ -426,7 +592,7 @@ cosine_status_t check_common(cosine_ctx_t ctx, int B, int k, int N) {
 
 extern "C" {
 
-cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out) {
+static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, bool vgroup) {
   if (!out) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (!cfg) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cfg is NULL");
@@ -449,7 +615,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks must be in [1, 32] and rank in [0, nranks)");
   if (cfg->nranks == 1 && (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab_size))
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "an unsharded context covers [0, vocab_size)");
-  if (cfg->nranks > 1 && !cfg->nccl_unique_id)
+  if (cfg->nranks > 1 && !cfg->nccl_unique_id && !vgroup)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks > 1 needs nccl_unique_id (cosine_nccl_unique_id on rank 0)");
   if (cfg->cluster_size != 0 && cfg->cluster_size != 1 && cfg->cluster_size != 2 &&
       cfg->cluster_size != 4 && cfg->cluster_size != 8 && cfg->cluster_size != 16)
@@ -457,6 +623,7 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
   cosine_ctx_t ctx = new (std::nothrow) cosine_ctx_s();
   if (!ctx) return fail(nullptr, COSINE_ERR_OUT_OF_MEMORY, "host allocation failed");
   ctx->cfg = *cfg;
+  ctx->vgroup = vgroup;
   ctx->cfg.nccl_unique_id = nullptr;
   ctx->V = cfg->vocab_end - cfg->vocab_begin;
   DeviceGuard dg(cfg->device);
@@ -492,10 +659,13 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     if (e == cudaSuccess) e = cudaMalloc(&ctx->zall, nb * sizeof(double) * (size_t)cfg->nranks);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->ysend, nb * sizeof(YRec));
     if (e == cudaSuccess) e = cudaMalloc(&ctx->yall, nb * sizeof(YRec) * (size_t)cfg->nranks);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+    for (int j = 0; j <= kMaxShardSlices && e == cudaSuccess; ++j)
+      e = cudaEventCreateWithFlags(&ctx->sev[j], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ncclResult_t nr = ncclSuccess;
-  if (e == cudaSuccess && cfg->nranks > 1) {
+  if (e == cudaSuccess && cfg->nranks > 1 && !vgroup) {
     ncclUniqueId uid;
     memcpy(&uid, cfg->nccl_unique_id, sizeof(uid));
     nr = ncclCommInitRank(&ctx->comm, cfg->nranks, uid, cfg->rank);
@@ -510,6 +680,9 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     cudaFree(ctx->zall);
     cudaFree(ctx->ysend);
     cudaFree(ctx->yall);
+    for (int j = 0; j <= kMaxShardSlices; ++j)
+      if (ctx->sev[j]) cudaEventDestroy(ctx->sev[j]);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     cudaFree(ctx->lz);
     cudaGetLastError();
     cudaFree(ctx->recs);
@@ -526,6 +699,34 @@ cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out
     return fail(nullptr, e == cudaErrorMemoryAllocation ? COSINE_ERR_OUT_OF_MEMORY : COSINE_ERR_CUDA, msg);
   }
   *out = ctx;
+  return COSINE_OK;
+}
+
+cosine_status_t cosine_verify_init(const cosine_config_t* cfg, cosine_ctx_t* out) {
+  return init_impl(cfg, out, false);
+}
+
+cosine_status_t cosine_verify_init_vgroup(const cosine_config_t* cfgs, int32_t G, cosine_ctx_t* out) {
+  if (!cfgs || !out || G < 2 || G > 32) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "bad cfgs / out / G");
+  for (int g = 0; g < G; ++g) out[g] = nullptr;
+  for (int g = 0; g < G; ++g) {
+    const cosine_config_t& c = cfgs[g];
+    if (c.nranks != G || c.rank != g || c.vocab_size != cfgs[0].vocab_size ||
+        c.vocab_begin != (g == 0 ? 0 : cfgs[g - 1].vocab_end) || (g == G - 1 && c.vocab_end != c.vocab_size) ||
+        c.target_dtype != cfgs[0].target_dtype || c.draft_dtype != cfgs[0].draft_dtype ||
+        c.draft_kind != cfgs[0].draft_kind || c.seed != cfgs[0].seed || c.max_batch != cfgs[0].max_batch ||
+        c.max_draft_len != cfgs[0].max_draft_len || c.max_drafters != cfgs[0].max_drafters) {
+      for (int h = 0; h < g; ++h) cosine_verify_destroy(out[h]);
+      return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT,
+                  "vgroup: cfgs[g] must be rank g of G with shards tiling [0, vocab_size) and equal settings");
+    }
+    const cosine_status_t s = init_impl(&c, &out[g], true);
+    if (s != COSINE_OK) {
+      for (int h = 0; h < g; ++h) cosine_verify_destroy(out[h]);
+      out[g] = nullptr;
+      return s;
+    }
+  }
   return COSINE_OK;
 }
 
@@ -550,6 +751,9 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->zall);
   cudaFree(ctx->ysend);
   cudaFree(ctx->yall);
+  for (int j = 0; j <= kMaxShardSlices; ++j)
+    if (ctx->sev[j]) cudaEventDestroy(ctx->sev[j]);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   for (auto& pe : ctx->prof_ev) {
     cudaEventDestroy(pe.first);
     cudaEventDestroy(pe.second);
@@ -645,18 +849,14 @@ cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int
                 ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
 }
 
-cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
-                                    int32_t N, const void* target_logits, int64_t ld_t,
-                                    float temperature, const void* draft, int64_t ld_q,
-                                    const int32_t* draft_tokens, const int32_t* draft_len,
-                                    const uint64_t* request_ids, uint32_t step,
-                                    cosine_weight_mode_t weight_mode,
-                                    cosine_select_mode_t select_mode, int32_t* accept_len,
-                                    int32_t* out_tokens, int32_t* status,
-                                    const cosine_debug_t* debug) {
+// Argument checks shared by cosine_verify_batch and cosine_verify_batch_vgroup.
+static cosine_status_t check_verify(cosine_ctx_t ctx, int32_t B, int32_t k, int32_t N, const void* target_logits,
+                                    int64_t ld_t, float temperature, const void* draft, int64_t ld_q,
+                                    const int32_t* draft_tokens, const uint64_t* request_ids,
+                                    cosine_weight_mode_t weight_mode, cosine_select_mode_t select_mode,
+                                    int32_t* accept_len, int32_t* out_tokens, int32_t* status) {
   cosine_status_t s = check_common(ctx, B, k, N);
   if (s != COSINE_OK) return s;
-  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
   if ((s = check_rows(ctx, target_logits, ld_t, ctx->cfg.target_dtype, "target_logits")) != COSINE_OK) return s;
   if ((s = check_rows(ctx, draft, ld_q, ctx->cfg.draft_dtype, "draft")) != COSINE_OK) return s;
   if (!draft_tokens || !request_ids || !accept_len || !out_tokens || !status)
@@ -669,6 +869,43 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "POINT weights need ARGMAX selection");
   if (temperature == 0.f && (ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS || select_mode == COSINE_SEL_SAMPLE))
     return fail(ctx, COSINE_ERR_UNSUPPORTED, "greedy (T = 0) needs PROBS drafts and ARGMAX selection");
+  return COSINE_OK;
+}
+
+// The split-kernel parameters of a verify call (everything but the launch configuration).
+static SplitParams make_split(cosine_ctx_t ctx, int32_t B, int32_t k, int32_t N, const void* target_logits,
+                              int64_t ld_t, float temperature, const void* draft, int64_t ld_q,
+                              const int32_t* draft_tokens, const int32_t* draft_len, const uint64_t* request_ids,
+                              uint32_t step, cosine_weight_mode_t weight_mode, int32_t* accept_len,
+                              int32_t* out_tokens, int32_t* status, const cosine_debug_t* debug) {
+  Params P;
+  fill_common(P, ctx, B, k, N, temperature);
+  SplitParams S;
+  memset(&S, 0, sizeof(S));
+  S.B = B; S.k = k; S.N = N;
+  S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
+  S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+  S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
+  S.rids = request_ids; S.seed = P.seed; S.step = step;
+  S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status;
+  if (debug) S.dbg = *debug;
+  return S;
+}
+
+cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
+                                    int32_t N, const void* target_logits, int64_t ld_t,
+                                    float temperature, const void* draft, int64_t ld_q,
+                                    const int32_t* draft_tokens, const int32_t* draft_len,
+                                    const uint64_t* request_ids, uint32_t step,
+                                    cosine_weight_mode_t weight_mode,
+                                    cosine_select_mode_t select_mode, int32_t* accept_len,
+                                    int32_t* out_tokens, int32_t* status,
+                                    const cosine_debug_t* debug) {
+  cosine_status_t s = check_verify(ctx, B, k, N, target_logits, ld_t, temperature, draft, ld_q, draft_tokens,
+                                   request_ids, weight_mode, select_mode, accept_len, out_tokens, status);
+  if (s != COSINE_OK) return s;
+  if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
+  if (ctx->vgroup) return fail(ctx, COSINE_ERR_UNSUPPORTED, "a vgroup context runs through cosine_verify_batch_vgroup");
   DeviceGuard dg(ctx->cfg.device);
   Params P;
   fill_common(P, ctx, B, k, N, temperature);
@@ -715,6 +952,37 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   }
   return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
                 ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+}
+
+cosine_status_t cosine_verify_batch_vgroup(const cosine_ctx_t* ctxs, int32_t G, cosine_stream_t stream, int32_t B,
+                                           int32_t k, int32_t N, const void* const* target_logits, int64_t ld_t,
+                                           float temperature, const void* const* draft, int64_t ld_q,
+                                           const int32_t* draft_tokens, const int32_t* draft_len,
+                                           const uint64_t* request_ids, uint32_t step,
+                                           cosine_weight_mode_t weight_mode, int32_t* const* accept_len,
+                                           int32_t* const* out_tokens, int32_t* const* status) {
+  if (!ctxs || G < 2 || !target_logits || !draft || !accept_len || !out_tokens || !status)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "vgroup: NULL argument or G < 2");
+  for (int g = 0; g < G; ++g) {
+    if (!ctxs[g] || !ctxs[g]->vgroup || ctxs[g]->cfg.nranks != G || ctxs[g]->cfg.rank != g)
+      return fail(ctxs[g], COSINE_ERR_INVALID_ARGUMENT, "vgroup: ctxs[g] must be rank g of a G-context vgroup");
+    cosine_status_t s = check_verify(ctxs[g], B, k, N, target_logits[g], ld_t, temperature, draft[g], ld_q,
+                                     draft_tokens, request_ids, weight_mode, COSINE_SEL_ARGMAX, accept_len[g],
+                                     out_tokens[g], status[g]);
+    if (s != COSINE_OK) return s;
+  }
+  if (B == 0) return COSINE_OK;
+  DeviceGuard dg(ctxs[0]->cfg.device);
+  for (int g = 1; g < G; ++g)
+    if (ctxs[g]->cfg.device != ctxs[0]->cfg.device)
+      return fail(ctxs[g], COSINE_ERR_UNSUPPORTED, "vgroup: every context on one device");
+  std::vector<SplitParams> S(G);
+  for (int g = 0; g < G; ++g)
+    S[g] = make_split(ctxs[g], B, k, N, target_logits[g], ld_t, temperature, draft[g], ld_q, draft_tokens, draft_len,
+                      request_ids, step, weight_mode, accept_len[g], out_tokens[g], status[g], nullptr);
+  const cosine_config_t& c = ctxs[0]->cfg;
+  return launch_shard_vgroup(ctxs, G, (cudaStream_t)stream, S.data(), c.target_dtype, c.draft_dtype,
+                             c.draft_kind == COSINE_DRAFT_LOGITS);
 }
 
 cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,

@@ -16,7 +16,7 @@ def _run(world: int, tmp_path):
     out = tmp_path / f"shard_{world}.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tools", "shard_check.py"),
-           "--out", str(out)]
+           "--out", str(out), "--c5"]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-4000:]
     res = json.loads(out.read_text())

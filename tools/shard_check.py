@@ -33,7 +33,7 @@ def column_shard(x: torch.Tensor, b: int, e: int, pad=float("nan")) -> torch.Ten
     """Columns [b, e) of the last dim into a fresh 16-byte-aligned buffer (ld = round_up(e-b, 8))."""
     w = e - b
     ld = (w + 7) // 8 * 8
-    out = torch.full(x.shape[:-1] + (ld,), pad, dtype=x.dtype)
+    out = torch.full(x.shape[:-1] + (ld,), pad, dtype=x.dtype, device=x.device)
     out[..., :w] = x[..., b:e]
     return out
 
@@ -50,9 +50,19 @@ CASES = [
     ("unaligned_split", 16, 5, 3, 5003, torch.bfloat16, dict(T=1.0, split="odd")),
     ("errors", 16, 4, 3, 3001, torch.bfloat16, dict(T=1.0, inject=True)),
 ]
+# BASELINE config c5 at full size (B = 1024, V = 128256): run with --c5
+C5_CASE = ("c5_full", 1024, 8, 4, 128256, torch.bfloat16, dict(T=1.0, gpu_gen=True))
 
 
 def make_inputs(B, k, N, V, dtype, kw, seed):
+    if kw.get("gpu_gen"):  # large cases: generated on the GPU in request slices of 64
+        dev = torch.device("cuda", torch.cuda.current_device())
+        parts = [synth.linear_inputs(64, k, N, V, dtype=dtype, seed=seed + b0, device=dev, rid_base=b0)
+                 for b0 in range(0, B, 64)]
+        return dict(target=torch.cat([p["target"] for p in parts]), draft=torch.cat([p["draft"] for p in parts]),
+                    draft_tokens=torch.cat([p["draft_tokens"] for p in parts]),
+                    request_ids=torch.cat([p["request_ids"] for p in parts]), draft_len=None, V=V,
+                    ld=parts[0]["ld"])
     dl = "random" if kw.get("draft_len") == "random" else None
     inp = synth.linear_inputs(B, k, N, V, dtype=dtype, seed=seed, draft_len=dl,
                               draft_kind=kw.get("draft_kind", "probs"))
@@ -118,13 +128,14 @@ def run_case(name, B, k, N, V, dtype, kw, world, rank, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--c5", action="store_true", help="also run BASELINE config c5 at full size")
     args = ap.parse_args()
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(dev)
     results, ok = [], True
-    for name, B, k, N, V, dtype, kw in CASES:
+    for name, B, k, N, V, dtype, kw in CASES + ([C5_CASE] if args.c5 else []):
         try:
             results.append(run_case(name, B, k, N, V, dtype, kw, world, rank, dev))
         except Exception as ex:  # keep the ranks in step: report and go on
