@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--lazy", action="store_true",
                     help="early-exit verification (cosine_verify_batch_lazy, SURVEY 8(f) NEXT-1)")
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--watchdog", type=float, default=0.0,
+                    help="dump every thread's stack and exit after this many seconds (0 = off)")
     a = ap.parse_args()
     if a.lazy and a.config == "c5":
         ap.error("--lazy runs on unsharded contexts (c1..c4)")
@@ -646,6 +648,9 @@ def run_vocab(args, c, dev, world, rank, local):
 
 if __name__ == "__main__":
     a = parse()
+    if a.watchdog > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(a.watchdog, exit=True)
     launch_ranks(a)
     if a.impl == "reference":
         run_reference(a)

@@ -127,12 +127,9 @@ const char* cosine_last_error(cosine_ctx_t ctx);
  * cosine_verify_batch collectively (same B, k, N, draft_tokens, draft_len, request_ids, step,
  * modes, temperature) with ITS columns of every row (ld >= the shard width; token ids stay
  * global); the outputs are identical on every rank and equal to the unsharded call on the full
- * rows up to flagged near-ties.  Three NCCL all-gathers per request slice: per-(request,
- * position) row statistics and candidate gathers (~N^2 + 4N + 8 words), the local masses of the
- * final draw (B doubles), the owner's token (B x 16 bytes).  The batch is cut into up to 4
- * request slices: slice s's statistics stream on `stream` while slice s-1's all-gathers and
- * decision / sampling kernels run on the context's own stream (joined back into `stream` before
- * the call returns: stream-ordered as usual).  ARGMAX selection only;
+ * rows up to flagged near-ties.  Three NCCL all-gathers on `stream`: per-(request, position)
+ * row statistics and candidate gathers (~N^2 + 4N + 8 words), the local masses of the final
+ * draw (B doubles), the owner's token (B x 16 bytes).  ARGMAX selection only;
  * cosine_fuse_drafts / cosine_sample_residual / cosine_verify_tree return COSINE_ERR_UNSUPPORTED
  * on a sharded context.
  *
@@ -150,8 +147,8 @@ cosine_status_t cosine_nccl_unique_id(void* out, int64_t capacity);
  *   [0, vocab_size) in rank order, every other field equal; nccl_unique_id ignored); creates G
  *   contexts (out[g]) that own no NCCL communicator.  On failure every created context is freed.
  * cosine_verify_batch_vgroup: the collective cosine_verify_batch of the G contexts (ARGMAX
- *   selection, no diagnostics), run phase by phase on `stream`: exactly the kernels, request
- *   slices and record layouts of the NCCL path, with each all-gather replaced by device copies
+ *   selection, no diagnostics), run phase by phase on `stream`: exactly the kernels and record
+ *   layouts of the NCCL path, with each all-gather replaced by device copies
  *   of every rank's send buffer into every rank's gather buffer in rank order.
  *   target_logits[g] / draft[g]: rank g's column shard ([B][k+1][ld_t] / [B][k][N][ld_q], one ld
  *   for all ranks); accept_len[g] / out_tokens[g] / status[g]: rank g's (replicated) outputs.

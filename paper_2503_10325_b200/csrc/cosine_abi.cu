@@ -39,8 +39,6 @@ __global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
   if (j < n) { done[j] = 0; first_rej[j] = kNoReject; }
 }
 
-constexpr int kMaxShardSlices = 8;  // request slices of the vocabulary-sharded call
-
 void kernel_set(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, KernelSet* ks) {
   if (tt == COSINE_BF16 && tq == COSINE_BF16) kernel_set_bb(logits, N, ks);
   else if (tt == COSINE_BF16 && tq == COSINE_F32) kernel_set_bf(logits, N, ks);
@@ -86,10 +84,6 @@ struct cosine_ctx_s {
   double* zall = nullptr;
   YRec* ysend = nullptr;
   YRec* yall = nullptr;
-  // sliced exchange: the slices' all-gathers and B phase run on `aux` while `stream` streams the
-  // next slice's statistics (fork / join by events)
-  cudaStream_t aux = nullptr;
-  cudaEvent_t sev[kMaxShardSlices + 1] = {};
   bool vgroup = false;  // a cosine_verify_init_vgroup context (device copies instead of NCCL)
 };
 
@@ -258,14 +252,11 @@ cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
 }
 
 // ---------------------------------------------------------------------------------------
-// Vocabulary-sharded verification (cosine_shard.cuh).  The batch is cut into request slices;
-// each slice runs the same four phases with three exchanges between them:
+// Vocabulary-sharded verification (cosine_shard.cuh): four phases with three exchanges:
 //   A: stats_kernel (local columns) -> shard_pack_kernel      X1: records   [G][units][words]
 //   B: shard_decide_kernel -> resample_kernel (local masses)  X2: masses    [G][B] doubles
 //   C: shard_sample_kernel (the owner of t scans)             X3: tokens    [G][B] YRec
 //   D: shard_finish_kernel (replicated outputs)
-// A slice is a view of the call with every per-request pointer (inputs, outputs, diagnostics,
-// scratch, exchange regions) offset to its first request, so every kernel sees a smaller batch.
 // ---------------------------------------------------------------------------------------
 void shard_setup(cosine_ctx_t ctx, SplitParams& S) {
   const int64_t units = (int64_t)S.B * (S.k + 1);
@@ -284,48 +275,6 @@ void shard_setup(cosine_ctx_t ctx, SplitParams& S) {
   S.ysend = ctx->ysend;
   S.yall = ctx->yall;
 }
-
-// The view of requests [b0, b0 + nb) of a (set-up) call.
-SplitParams shard_slice(const SplitParams& F, int b0, int nb, size_t tsz, size_t qsz) {
-  SplitParams S = F;
-  const int64_t kp1 = F.k + 1, k = F.k, N = F.N, G = F.G;
-  const int64_t u0 = (int64_t)b0 * kp1;
-  S.B = nb;
-  S.nb = nb;
-  S.target = (const char*)F.target + (size_t)(u0 * F.ld_t) * tsz;
-  S.draft = (const char*)F.draft + (size_t)((int64_t)b0 * k * N * F.ld_q) * qsz;
-  S.draft_tokens = F.draft_tokens + (int64_t)b0 * k * N;
-  if (F.draft_len) S.draft_len = F.draft_len + b0;
-  S.rids = F.rids + b0;
-  S.accept_len = F.accept_len + b0;
-  S.out_tokens = F.out_tokens + u0;
-  S.status = F.status + b0;
-  cosine_debug_t& D = S.dbg;
-  if (D.p_x) D.p_x += (int64_t)b0 * k;
-  if (D.q_x) D.q_x += (int64_t)b0 * k;
-  if (D.accept_u) D.accept_u += (int64_t)b0 * k;
-  if (D.row_max) D.row_max += u0;
-  if (D.row_sumexp) D.row_sumexp += u0;
-  if (D.draft_norm) D.draft_norm += (int64_t)b0 * k * N;
-  if (D.conf) D.conf += (int64_t)b0 * k * N;
-  if (D.weights) D.weights += (int64_t)b0 * k * N;
-  if (D.fused_tokens) D.fused_tokens += (int64_t)b0 * k;
-  if (D.residual_mass) D.residual_mass += b0;
-  if (D.tie_margin) D.tie_margin += b0;
-  S.parts = F.parts + u0 * F.C;
-  S.pdec = F.pdec + u0;
-  S.segsum = F.segsum + (int64_t)b0 * F.nseg;
-  S.counters = F.counters + b0;
-  S.rec_send = F.rec_send + u0 * F.rec_words;
-  S.rec_all = F.rec_all + G * u0 * F.rec_words;  // [G][nb (k+1)][words]
-  S.zsend = F.zsend + b0;
-  S.zall = F.zall + G * b0;  // [G][nb]
-  S.ysend = F.ysend + b0;
-  S.yall = F.yall + G * b0;  // [G][nb]
-  return S;
-}
-
-int shard_slices(int B) { return B >= 256 ? 4 : (B >= 64 ? 2 : 1); }
 
 struct ShardLaunch {
   cudaLaunchConfig_t lc;
@@ -405,8 +354,11 @@ cosine_status_t shard_fail(cosine_ctx_t ctx, cudaStream_t s, cudaError_t e, nccl
   return fail(ctx, COSINE_ERR_NCCL, std::string("sharded verify all-gather: ") + ncclGetErrorString(r));
 }
 
-// One rank's collective call (NCCL).  Slice c's phase A runs on `stream`; its exchanges and
-// phases B-D on the context's aux stream, overlapping slice c + 1's statistics.
+// One rank's collective call (NCCL): the four phases on `stream` with an all-gather after each
+// of the first three.  (Request slices whose exchanges ran on a second stream under the next
+// slice's statistics were measured slower on 2 B200s: 1 / 2 / 4 / 8 slices -> 1024 / 1046 / 1097 /
+// 1288 us per c5 call — the slices' B phases take SMs and bandwidth from the statistics stream;
+// profiles/r2_c5_slices.md.)
 cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& F, cosine_dtype_t tt,
                              cosine_dtype_t tq, bool logits) {
   KernelSet ks;
@@ -414,36 +366,17 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
   shard_setup(ctx, F);
   if ((size_t)F.B * (size_t)F.nseg > ctx->segsum_cap)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
-  const int nsl = shard_slices(F.B);
-  const int per = (F.B + nsl - 1) / nsl;
-  const size_t tsz = esize(tt), qsz = esize(tq);
-  const char* stage = "fork";
-  cudaError_t e = cudaEventRecord(ctx->sev[kMaxShardSlices], stream);  // aux follows the caller's stream
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->sev[kMaxShardSlices], 0);
+  const char* stage = "stats";
   ncclResult_t r = ncclSuccess;
-  int launches = 0;
-  for (int c = 0; c < nsl && e == cudaSuccess && r == ncclSuccess; ++c) {
-    const int b0 = c * per, nb = std::min(per, F.B - b0);
-    if (nb <= 0) break;
-    const SplitParams S = shard_slice(F, b0, nb, tsz, qsz);
-    e = shard_phase_a(ctx, stream, S, ks, &stage);
-    if (e == cudaSuccess) e = cudaEventRecord(ctx->sev[c], stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->aux, ctx->sev[c], 0);
-    if (e == cudaSuccess) r = shard_allgather(ctx, ctx->aux, S, 1);
-    if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_b(ctx->aux, S, ks, logits, &stage);
-    if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, ctx->aux, S, 2);
-    if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_c(ctx->aux, S, ks, &stage);
-    if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, ctx->aux, S, 3);
-    if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_d(ctx->aux, S, &stage);
-    launches += 6;
-  }
-  if (e == cudaSuccess && r == ncclSuccess) {  // join: the caller's stream waits for the outputs
-    stage = "join";
-    e = cudaEventRecord(ctx->sev[kMaxShardSlices], ctx->aux);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ctx->sev[kMaxShardSlices], 0);
-  }
+  cudaError_t e = shard_phase_a(ctx, stream, F, ks, &stage);
+  if (e == cudaSuccess) r = shard_allgather(ctx, stream, F, 1);
+  if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_b(stream, F, ks, logits, &stage);
+  if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, stream, F, 2);
+  if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_c(stream, F, ks, &stage);
+  if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, stream, F, 3);
+  if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_d(stream, F, &stage);
   if (e != cudaSuccess || r != ncclSuccess) return shard_fail(ctx, stream, e, r, stage);
-  ctx->last_launches = launches;
+  ctx->last_launches = 6;
   ctx->last_cluster = F.C;
   return COSINE_OK;
 }
@@ -460,38 +393,28 @@ cosine_status_t launch_shard_vgroup(const cosine_ctx_t* ctxs, int G, cudaStream_
     if ((size_t)F[g].B * (size_t)F[g].nseg > ctxs[g]->segsum_cap)
       return fail(ctxs[g], COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
   }
-  const int B = F[0].B;
-  const int nsl = shard_slices(B);
-  const int per = (B + nsl - 1) / nsl;
-  const size_t tsz = esize(tt), qsz = esize(tq);
   const char* stage = "stats";
   cudaError_t e = cudaSuccess;
-  std::vector<SplitParams> S(G);
   auto exchange = [&](int x) {
     for (int g = 0; g < G && e == cudaSuccess; ++g) {
-      const size_t n = shard_x_bytes(S[g], x);
-      const void* src = x == 1 ? (const void*)S[g].rec_send
-                               : (x == 2 ? (const void*)S[g].zsend : (const void*)S[g].ysend);
+      const size_t n = shard_x_bytes(F[g], x);
+      const void* src = x == 1 ? (const void*)F[g].rec_send
+                               : (x == 2 ? (const void*)F[g].zsend : (const void*)F[g].ysend);
       for (int h = 0; h < G && e == cudaSuccess; ++h) {
-        char* dst = (char*)(x == 1 ? (void*)S[h].rec_all : (x == 2 ? (void*)S[h].zall : (void*)S[h].yall));
+        char* dst = (char*)(x == 1 ? (void*)F[h].rec_all : (x == 2 ? (void*)F[h].zall : (void*)F[h].yall));
         e = cudaMemcpyAsync(dst + (size_t)g * n, src, n, cudaMemcpyDeviceToDevice, stream);
       }
     }
   };
-  for (int c = 0; c < nsl && e == cudaSuccess; ++c) {
-    const int b0 = c * per, nb = std::min(per, B - b0);
-    if (nb <= 0) break;
-    for (int g = 0; g < G; ++g) S[g] = shard_slice(F[g], b0, nb, tsz, qsz);
-    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_a(ctxs[g], stream, S[g], ks, &stage);
-    exchange(1);
-    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_b(stream, S[g], ks, logits, &stage);
-    exchange(2);
-    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_c(stream, S[g], ks, &stage);
-    exchange(3);
-    for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_d(stream, S[g], &stage);
-  }
+  for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_a(ctxs[g], stream, F[g], ks, &stage);
+  exchange(1);
+  for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_b(stream, F[g], ks, logits, &stage);
+  exchange(2);
+  for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_c(stream, F[g], ks, &stage);
+  exchange(3);
+  for (int g = 0; g < G && e == cudaSuccess; ++g) e = shard_phase_d(stream, F[g], &stage);
   if (e != cudaSuccess) return shard_fail(ctxs[0], stream, e, ncclSuccess, stage);
-  for (int g = 0; g < G; ++g) ctxs[g]->last_launches = 6 * nsl;
+  for (int g = 0; g < G; ++g) ctxs[g]->last_launches = 6;
   return COSINE_OK;
 }
 
@@ -659,9 +582,6 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
     if (e == cudaSuccess) e = cudaMalloc(&ctx->zall, nb * sizeof(double) * (size_t)cfg->nranks);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->ysend, nb * sizeof(YRec));
     if (e == cudaSuccess) e = cudaMalloc(&ctx->yall, nb * sizeof(YRec) * (size_t)cfg->nranks);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
-    for (int j = 0; j <= kMaxShardSlices && e == cudaSuccess; ++j)
-      e = cudaEventCreateWithFlags(&ctx->sev[j], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ncclResult_t nr = ncclSuccess;
@@ -680,9 +600,6 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
     cudaFree(ctx->zall);
     cudaFree(ctx->ysend);
     cudaFree(ctx->yall);
-    for (int j = 0; j <= kMaxShardSlices; ++j)
-      if (ctx->sev[j]) cudaEventDestroy(ctx->sev[j]);
-    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     cudaFree(ctx->lz);
     cudaGetLastError();
     cudaFree(ctx->recs);
@@ -751,9 +668,6 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->zall);
   cudaFree(ctx->ysend);
   cudaFree(ctx->yall);
-  for (int j = 0; j <= kMaxShardSlices; ++j)
-    if (ctx->sev[j]) cudaEventDestroy(ctx->sev[j]);
-  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   for (auto& pe : ctx->prof_ev) {
     cudaEventDestroy(pe.first);
     cudaEventDestroy(pe.second);
