@@ -347,8 +347,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     prof_ms, prof_n = cv.cosine_profile_read(ver.ctx)
     cv.cosine_profile_enable(ver.ctx, False)
-    kernel_name = "cosine::verify_kernel (the whole call: one launch)"
-    kernel_regex = "verify_kernel"
+    kernel_name = "cosine::stats_kernel (streams every input byte once; 1 of the call's 3 launches)"
+    kernel_regex = "stats_kernel"
     if args.lazy:  # no single dominant launch: the whole call against its realised bytes
         # rows read per request: target 0..L, drafters at positions 0..min(L, k-1) — the round
         # holding L (kLazySpan = 2 positions per round) also streamed its other position — and
@@ -360,9 +360,6 @@ def run_ours(args):
         alg_bytes = int(rows.sum()) * V * esz
         prof_ms, prof_n = statistics.mean(kern_ms), 1
         kernel_name, kernel_regex = "whole lazy call (rounds of stats + lazy_decide, then resample)", "stats_kernel"
-    elif sm == 1:
-        kernel_name = "cosine::unit_kernel (legacy SAMPLE-select path)"
-        kernel_regex = "unit_kernel"
     elapsed_ms = sharding.max_over_ranks(elapsed_ms, device=dev)  # the slowest rank's device time
     acc = ver.accept_len[:B].float().mean().item()
     status_nonzero = int((ver.status[:B] & 0xff).ne(0).sum().item())

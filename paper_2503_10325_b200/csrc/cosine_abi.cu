@@ -198,7 +198,8 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_events(cosine_ctx_t ctx) {
 // The split path: stats_kernel -> decide_kernel -> resample_kernel, the latter two programmatic
 // dependents waiting per unit / per request on device counters (scheduled into the previous
 // grid's tail wave; the waits always end because every CTA they wait for is resident or done).
-cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, const KernelSet& ks) {
+cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, const KernelSet& ks,
+                              bool sample) {
   const int64_t units = (int64_t)S.B * (S.k + 1);
   fill_scratch(ctx, S, stats_chunks(ctx, units, S.ngroups));
   if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
@@ -217,10 +218,11 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
   cudaError_t e = cudaLaunchKernelEx(&lc, ks.stats, S);
   if (pe.second) cudaEventRecord(pe.second, stream);
   if (e == cudaSuccess) {
-    lc.gridDim = dim3((unsigned)((units + kWarps - 1) / kWarps), 1, 1);
+    // ARGMAX: a warp per unit; SAMPLE: a CTA per unit (the draw scans one chunk block-wide)
+    lc.gridDim = dim3((unsigned)(sample ? units : (units + kWarps - 1) / kWarps), 1, 1);
     lc.attrs = pe.second ? nullptr : at;  // (an event record between the two breaks PDL)
     lc.numAttrs = pe.second ? 0 : 1;
-    e = cudaLaunchKernelEx(&lc, ks.decide, S);
+    e = cudaLaunchKernelEx(&lc, sample ? ks.sample_decide : ks.decide, S);
   }
   if (e == cudaSuccess) {
     lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
@@ -242,13 +244,13 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
   return COSINE_OK;
 }
 
-// cosine_verify_batch on one GPU (ARGMAX selection).
+// cosine_verify_batch on one GPU.
 cosine_status_t launch_split(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S,
-                             cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+                             cosine_dtype_t tt, cosine_dtype_t tq, bool logits, bool sample) {
   KernelSet ks;
   memset(&ks, 0, sizeof(ks));
   kernel_set(tt, tq, logits, S.N, &ks);
-  return launch_split3(ctx, stream, S, ks);
+  return launch_split3(ctx, stream, S, ks, sample);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -821,51 +823,18 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
   if (B == 0) { ctx->last_launches = 0; return COSINE_OK; }
   if (ctx->vgroup) return fail(ctx, COSINE_ERR_UNSUPPORTED, "a vgroup context runs through cosine_verify_batch_vgroup");
   DeviceGuard dg(ctx->cfg.device);
-  Params P;
-  fill_common(P, ctx, B, k, N, temperature);
-  P.mode = kModeVerify;
-  P.ld_t = ld_t;
-  P.ld_q = ld_q;
-  P.target = target_logits;
-  P.draft = draft;
-  P.draft_tokens = draft_tokens;
-  P.draft_len = draft_len;
-  P.rids = request_ids;
-  P.step = step;
-  P.weight_mode = weight_mode;
-  P.select_mode = select_mode;
-  P.accept_len = accept_len;
-  P.out_tokens = out_tokens;
-  P.status = status;
-  if (debug) P.dbg = *debug;
   if (ctx->cfg.nranks > 1) {  // vocabulary-sharded (cosine_shard.cuh)
     if (select_mode != COSINE_SEL_ARGMAX)
       return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary sharding takes ARGMAX selection");
-    SplitParams S;
-    memset(&S, 0, sizeof(S));
-    S.B = B; S.k = k; S.N = N;
-    S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
-    S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
-    S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
-    S.rids = request_ids; S.seed = P.seed; S.step = step;
-    S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
+    SplitParams S = make_split(ctx, B, k, N, target_logits, ld_t, temperature, draft, ld_q, draft_tokens, draft_len,
+                               request_ids, step, weight_mode, accept_len, out_tokens, status, debug);
     return launch_shard(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
                         ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
   }
-  if (select_mode == COSINE_SEL_ARGMAX) {
-    SplitParams S;
-    memset(&S, 0, sizeof(S));
-    S.B = B; S.k = k; S.N = N;
-    S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
-    S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
-    S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
-    S.rids = request_ids; S.seed = P.seed; S.step = step;
-    S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status; S.dbg = P.dbg;
-    return launch_split(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
-                        ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
-  }
-  return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * (k + 1), ctx->cfg.target_dtype,
-                ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+  SplitParams S = make_split(ctx, B, k, N, target_logits, ld_t, temperature, draft, ld_q, draft_tokens, draft_len,
+                             request_ids, step, weight_mode, accept_len, out_tokens, status, debug);
+  return launch_split(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
+                      ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS, select_mode == COSINE_SEL_SAMPLE);
 }
 
 cosine_status_t cosine_verify_batch_vgroup(const cosine_ctx_t* ctxs, int32_t G, cosine_stream_t stream, int32_t B,

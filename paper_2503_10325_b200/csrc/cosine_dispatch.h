@@ -17,6 +17,7 @@ struct KernelSet {
   SplitFn stats;         // stats_kernel (lazy rounds, tree all-nodes, sharded)
   SplitFn lazy_decide;   // lazy round decisions (NEXT-1)
   SplitFn decide;        // split path decisions (stats -> decide -> resample)
+  SplitFn sample_decide; // the same with SAMPLE selection (x* ~ fused q)
   SplitFn resample;      // final draws
   SplitFn shard_pack;    // vocabulary-sharded records
   SplitFn shard_sample;  // vocabulary-sharded owner scan

@@ -440,7 +440,8 @@ __device__ __forceinline__ void write_pos_debug(const SplitParams& P, int b, int
 template <bool kLogits>
 __device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i, bool has_d, bool tok_bad,
                                              bool nonfinite, bool empty, const float* gx, const int32_t* tok,
-                                             const double* sig, const float* dmax, PosDec& pd) {
+                                             const double* sig, const float* dmax, PosDec& pd,
+                                             double* w_sample = nullptr) {
   const int N = P.N;
   const bool greedy = P.greedy != 0;
   const double k2 = (double)P.k2f;
@@ -480,6 +481,18 @@ __device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i,
     } else {
       for (int n = 0; n < N; ++n) w[n] = (n == ns) ? 1.0 : 0.0;
     }
+    if (w_sample) {  // SAMPLE selection: x* ~ q is drawn by the caller (sample_decide_kernel)
+      if (P.weight_mode != COSINE_W_WINNER) pd.m_fa = INFINITY;  // n* does not matter then
+      for (int n = 0; n < N; ++n) {
+        w_sample[n] = w[n];
+        pd.a[n] = (float)(w[n] / sig[n]);
+        pd.dm[n] = dmax[n];
+        pd.sig[n] = (float)sig[n];
+        pd.c[n] = (float)c[n];
+        pd.w[n] = (float)w[n];
+      }
+      return;
+    }
     pd.xstar = tok[ns];
     if (P.weight_mode == COSINE_W_POINT) {
       pd.qx = 1.0;
@@ -507,17 +520,20 @@ __device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i,
   }
 }
 
-// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131):
-// lane r combines chunk r's partial record (fixed-order shuffle reductions, fp64), lanes gather
-// o(X_n) and q_m(X_n), lane 0 writes the decision to *out (and the diagnostics if asked).
+// One warp: the gathers of the drafters' own tokens (lane m * N + n: d_m(X_n), m == N: l(X_n);
+// `diag_only`: d_n(X_n) only) and the combination of unit's C chunk records (chunk r in lane r,
+// fixed-order shuffle reductions, fp64).  Results in lane 0 (pd.M / pd.S / pd.amax, sig, dmax,
+// the error flags).
+struct UnitFlags {
+  bool t_nf, t_empty, d_nf, d_empty, tok_bad;
+};
 template <typename TT, typename TQ, bool kLogits>
-__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
-                                            int32_t* s_tokw, PosDec* out, bool write_debug,
-                                            PosDec* out2 = nullptr) {
+__device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, int i, bool has_d, bool diag_only,
+                                                  float* s_gxw, int32_t* s_tokw, PosDec& pd, double* sig,
+                                                  float* dmax) {
   const int lane = threadIdx.x & 31;
   const int N = P.N, C = P.C;
   const int64_t unit = (int64_t)b * (P.k + 1) + i;
-  const bool has_d = i < g;
   const bool greedy = P.greedy != 0;
   const double k2 = (double)P.k2f;
   const int ng = has_d ? N * (N + 1) : 0;
@@ -525,7 +541,7 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     const int n = lane % N, m = lane / N;
     const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
     float v = 0.f;
-    if (tk >= 0 && (int64_t)tk < P.V) {
+    if (tk >= 0 && (int64_t)tk < P.V && (!diag_only || m == n)) {
       if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
       else v = load_one((const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t, tk);
     }
@@ -537,15 +553,14 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
   const bool own = lane < C;
   const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
   const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
-  PosDec pd;
   init_posdec(pd);
-  bool t_nf = false, t_empty = false, d_nf = false, d_empty = false, tok_bad = false;
+  UnitFlags f = {false, false, false, false, false};
   if (greedy) {
     float bv = own ? tmax : -INFINITY;
     int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
     warp_argmax(bv, bi);
-    t_nf = (bad & 1) != 0;
-    t_empty = (bi < 0);
+    f.t_nf = (bad & 1) != 0;
+    f.t_empty = (bi < 0);
     pd.amax = bi;
     pd.M = bv;
   } else {
@@ -554,13 +569,11 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
     pd.M = M;
     pd.S = S;
-    t_nf = !isfinite(S) || !isfinite(M);
-    t_empty = !t_nf && !(S > 0.0);
+    f.t_nf = !isfinite(S) || !isfinite(M);
+    f.t_empty = !f.t_nf && !(S > 0.0);
   }
-  double sig[kMaxN];
-  float dmax[kMaxN];
   if (has_d) {
-    if (bad & 2) d_nf = true;
+    if (bad & 2) f.d_nf = true;
     for (int n = 0; n < N; ++n) {
       double sv;
       float mx = kNegBig;
@@ -569,22 +582,37 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
         const float dmr = own ? __ldcg(&parts[lane].dmax[n]) : kNegBig;
         mx = warp_max(dmr);
         sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
-        if (!isfinite(mx)) d_nf = true;
+        if (!isfinite(mx)) f.d_nf = true;
       } else {
         sv = warp_sum(ds);
       }
       sig[n] = sv;
       dmax[n] = mx;
-      if (!isfinite(sv)) d_nf = true;
-      else if (!(sv > 0.0)) d_empty = true;
+      if (!isfinite(sv)) f.d_nf = true;
+      else if (!(sv > 0.0)) f.d_empty = true;
     }
   }
   __syncwarp();
-  if (lane != 0) return;
-  if (has_d)
+  if (lane == 0 && has_d)
     for (int n = 0; n < N; ++n)
-      if (s_tokw[n] < 0 || (int64_t)s_tokw[n] >= P.V) tok_bad = true;
-  decide_lane0<kLogits>(P, b, i, has_d, tok_bad, t_nf || d_nf, t_empty || d_empty, s_gxw, s_tokw, sig, dmax, pd);
+      if (s_tokw[n] < 0 || (int64_t)s_tokw[n] >= P.V) f.tok_bad = true;
+  return f;
+}
+
+// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131); lane 0
+// writes the decision to *out (and the diagnostics if asked).
+template <typename TT, typename TQ, bool kLogits>
+__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
+                                            int32_t* s_tokw, PosDec* out, bool write_debug,
+                                            PosDec* out2 = nullptr) {
+  const bool has_d = i < g;
+  PosDec pd;
+  double sig[kMaxN];
+  float dmax[kMaxN];
+  const UnitFlags f = warp_combine<TT, TQ, kLogits>(P, b, i, has_d, false, s_gxw, s_tokw, pd, sig, dmax);
+  if ((threadIdx.x & 31) != 0) return;
+  decide_lane0<kLogits>(P, b, i, has_d, f.tok_bad, f.t_nf || f.d_nf, f.t_empty || f.d_empty, s_gxw, s_tokw, sig,
+                        dmax, pd);
   *out = pd;
   if (out2) *out2 = pd;
   if (write_debug) write_pos_debug(P, b, i, has_d, pd);
@@ -616,6 +644,153 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   __syncwarp();
   warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[gu], true);
   if ((threadIdx.x & 31) == 0) {
+    P.ucnt[gu] = 0;   // ready for the next call
+    __threadfence();  // the decision before its count (release)
+    atomicAdd(&P.dcnt[b], 1);
+  }
+}
+
+// Kernel B1 for SAMPLE selection (reading #3: x*_i ~ the fused q_i, the distribution-exact
+// fusion; "direct ensemble sampling"): one CTA per unit, a programmatic dependent
+// of stats_kernel that waits for its unit's C chunk records.
+//  1. warp 0 combines the records (M, S, sigma) and the own-token gathers: confidences and the
+//     fusion weights w (Eq. 4 weights; decide_lane0 stopped before x*);
+//  2. the chunk masses of q come free from the statistics pass: chunk r holds
+//     sum_n (w_n / sigma_n) dsum_{n,r} (rescaled to the row max for LOGITS drafts); the crossing
+//     chunk of t = u Q, u = U(rid, i+1, FUSE), is found in one warp prefix over the C chunks;
+//  3. the CTA scans only that chunk (block scan, reading #10) for x*, gathers o(x*), q_m(x*) and
+//     takes the acceptance test u' q(x*) < o(x*).
+// One chunk of the unit's N drafter rows (1/C of them) is re-read: the draw costs no full pass.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitParams P) {
+  __shared__ float s_gx[(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kMaxN];
+  __shared__ PosDec s_pd;
+  __shared__ Decision s_d;
+  __shared__ double s_w[kMaxN], s_sig[kMaxN];
+  __shared__ float s_dmax[kMaxN];
+  __shared__ double s_scan[kWarps];
+  __shared__ int64_t s_wi[kWarps];
+  __shared__ int64_t s_found, s_g0, s_g1;
+  __shared__ float s_margin;
+  __shared__ double s_tc, s_Q;
+  __shared__ int s_go;
+  const int tid = threadIdx.x, lane = tid & 31;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t unit = blockIdx.x;
+  if (unit >= (int64_t)P.B * (P.k + 1)) return;
+  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (g < 1 || g > P.k || i > g) return;
+  const int64_t gu = (int64_t)b * (P.k + 1) + i;
+  const int N = P.N, C = P.C;
+  const bool has_d = i < g;
+  const double k2 = (double)P.k2f;
+  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
+  const TT* trow = (const TT*)P.target + gu * P.ld_t;
+  if (tid == 0) {  // this unit's C chunk records (every stats CTA is resident or done by now)
+    uint32_t n;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.ucnt + gu) : "memory");
+      if ((int)n >= C) break;
+      __nanosleep(100);
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    PosDec pd;
+    double sig[kMaxN];
+    float dmax[kMaxN];
+    const UnitFlags f = warp_combine<TT, TQ, kLogits>(P, b, i, has_d, true, s_gx, s_tok, pd, sig, dmax);
+    if (lane == 0) {
+      decide_lane0<kLogits>(P, b, i, has_d, f.tok_bad, f.t_nf || f.d_nf, f.t_empty || f.d_empty, s_gx, s_tok, sig,
+                            dmax, pd, s_w);
+      s_go = (has_d && pd.status == 0) ? 1 : 0;
+      for (int n = 0; n < N; ++n) { s_sig[n] = sig[n]; s_dmax[n] = dmax[n]; }
+      s_pd = pd;
+    }
+    __syncwarp();
+    if (s_go) {
+      // the fused q's mass over chunk `lane` (PROBS: raw sums; LOGITS: relative to the chunk max)
+      double m = 0.0;
+      if (lane < C) {
+        const PartRec* pr = P.parts + gu * C + lane;
+        for (int n = 0; n < N; ++n) {
+          const double ds = __ldcg(&pr->dsum[n]);
+          double sc = 1.0;
+          if (kLogits) sc = exp2((double)__ldcg(&pr->dmax[n]) * k2 - (double)s_dmax[n] * k2);
+          if (ds != 0.0) m += (s_w[n] / s_sig[n]) * ds * sc;
+        }
+      }
+      double incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nb;
+      }
+      const double Q = __shfl_sync(0xffffffffu, incl, 31);
+      const double u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagFuse);
+      const double t = u * Q;
+      const unsigned hit = __ballot_sync(0xffffffffu, lane < C && m > 0.0 && incl > t);
+      const unsigned pos = __ballot_sync(0xffffffffu, lane < C && m > 0.0);
+      int r;
+      double tc;
+      if (hit) {
+        r = __ffs(hit) - 1;
+        tc = t - (__shfl_sync(0xffffffffu, incl, r) - __shfl_sync(0xffffffffu, m, r));
+      } else {  // rounding past the total: the last positive chunk's last positive entry
+        r = pos ? 31 - __clz(pos) : 0;
+        tc = INFINITY;
+      }
+      if (lane == 0) {
+        s_g0 = (int64_t)r * P.cg;
+        s_g1 = min(P.ngroups, s_g0 + P.cg);
+        s_tc = tc;
+        s_Q = Q;
+        Decision d;
+        d.need = 1;
+        d.kind = kWFuseQ;
+        d.xstar = -1;
+        d.node = (uint32_t)(i + 1);
+        d.u = u;
+        d.M = 0.f;
+        d.invS = 0.f;
+        d.k2 = P.k2f;
+        for (int n = 0; n < kMaxN; ++n) {
+          d.a[n] = (n < N) ? (float)(s_w[n] / s_sig[n]) : 0.f;
+          d.dm[n] = (n < N) ? s_dmax[n] : 0.f;
+        }
+        s_d = d;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_go) {
+    const int64_t y = scan_range<TT, TQ, kLogits, NMAX>(P, s_d, kWFuseQ, trow, drow, N, s_g0, s_g1, s_tc, s_Q,
+                                                        s_scan, s_wi, &s_found, &s_margin);
+    if (tid == 0) {
+      PosDec& pd = s_pd;
+      pd.xstar = (int32_t)y;
+      if (y >= 0) {
+        double q = 0.0;
+        for (int m = 0; m < N; ++m) {
+          const double dv = (double)load_one(drow + (int64_t)m * P.ld_q, y);
+          q += s_w[m] * (kLogits ? exp2(dv * k2 - (double)s_dmax[m] * k2) / s_sig[m] : dv / s_sig[m]);
+        }
+        pd.qx = q;
+        pd.u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
+        // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
+        pd.px = exp2((double)load_one(trow, y) * k2 - (double)pd.M * k2) / pd.S;
+        pd.accept = (pd.u * pd.qx < pd.px);
+        pd.m_fa = fmin_(fmin_(pd.m_fa, s_margin), (float)fabs(pd.u - pd.px / pd.qx));
+      } else {
+        pd.status = COSINE_REQ_EMPTY_ROW;  // unreachable: q has mass (every w_n, sigma_n > 0)
+      }
+    }
+  }
+  if (tid == 0) {
+    P.pdec[gu] = s_pd;
+    write_pos_debug(P, b, i, has_d, s_pd);
     P.ucnt[gu] = 0;   // ready for the next call
     __threadfence();  // the decision before its count (release)
     atomicAdd(&P.dcnt[b], 1);

@@ -13,6 +13,10 @@ import oracle
 TIE = 1e-6        # north_star: ties within 1e-6 of a threshold are flagged, not failures
 PROB_RTOL = 1e-5  # north_star: probabilities within 1e-5 relative (fp32)
 MAX_FLAG_FRAC = 0.01  # a flagged near tie is rare (margins < 1e-6); more than 1% means a regression
+# SAMPLE selection draws x*_i ~ q_i at every position (k draws per request, not one): a draw that
+# lands in a bin of mass < 1e-6 (absolute, ~V^-1 for V = 128256) is flagged, so ~k times more
+# requests are flagged (measured: 8 of 256 at c3); the bound scales with the draws
+MAX_FLAG_FRAC_SAMPLE = 0.05
 
 
 def record(name, **counts):
@@ -58,7 +62,7 @@ def oracle_verify(inp, *, T=1.0, seed=7, step=0, wm=0, sm=0, draft_kind="probs",
                                weight_mode=wm, select_mode=sm, vocab=inp["V"])
 
 
-def compare(g, r, subset=None, check_probs=True, greedy=False, name=""):
+def compare(g, r, subset=None, check_probs=True, greedy=False, name="", max_flag_frac=MAX_FLAG_FRAC):
     """Bit-exact accept_len / out_tokens / status except where the oracle flags a near tie; the
     flagged requests are counted and bounded (MAX_FLAG_FRAC)."""
     idx = np.arange(len(r["accept_len"])) if subset is None else np.asarray(subset)
@@ -70,7 +74,7 @@ def compare(g, r, subset=None, check_probs=True, greedy=False, name=""):
     nflag = int(flagged.sum())
     record(name, requests=int(len(idx)), mismatches=int(len(mism)), unflagged_mismatches=len(bad),
            flagged=nflag)
-    assert nflag <= max(1, MAX_FLAG_FRAC * len(idx)), f"{nflag} of {len(idx)} requests flagged as near ties"
+    assert nflag <= max(1, max_flag_frac * len(idx)), f"{nflag} of {len(idx)} requests flagged as near ties"
     assert not bad, f"unflagged mismatches at {bad[:5]}: gpu {ga[bad[0]]} {go[bad[0]]} " \
                     f"oracle {r['accept_len'][bad[0]]} {r['out_tokens'][bad[0]]} margin {r['tie_margin'][bad[0]]}"
     if check_probs:
@@ -78,9 +82,19 @@ def compare(g, r, subset=None, check_probs=True, greedy=False, name=""):
         pairs = [("q_x", "q_x"), ("draft_norm", "sigma"), ("conf", "conf"), ("weights", "weights")]
         if not greedy:  # T = 0 has no softmax statistics
             pairs += [("p_x", "p_x"), ("row_sumexp", "S")]
+        # p(x*), q(x*) are values AT the fused token: compare them where both sides fused the same
+        # token.  Under SAMPLE selection a position after the first rejection is not on the
+        # realised path (its draw is discarded), so a near tie there may pick another token
+        # without being flagged; on the path (positions < L) the tokens are equal (checked above).
+        same_x = g["fused_tokens"][idx][ok] == r["fused_tokens"][ok]
+        L = r["accept_len"][ok]
+        on_path = (np.arange(same_x.shape[1])[None, :] < L[:, None]) & ~flagged[ok][:, None]
+        assert same_x[on_path].all()
         for gk, rk in pairs:
             gv, rv = g[gk][idx][ok], r[rk][ok]
             m = np.isfinite(rv) & (np.abs(rv) > 1e-30)
+            if rk in ("q_x", "p_x"):
+                m &= same_x
             if rk == "S":
                 m &= rv > 0
             if m.any():

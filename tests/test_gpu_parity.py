@@ -19,7 +19,8 @@ def _run(inp, name="", **kw):
     g = parity.gpu_verify(inp, **kw)
     kw.pop("cluster_size", None)
     r = parity.oracle_verify(inp, subset=subset, **kw)
-    return g, r, parity.compare(g, r, subset=subset, greedy=kw.get("T", 1.0) == 0.0, name=name)
+    frac = parity.MAX_FLAG_FRAC_SAMPLE if kw.get("sm", 0) == 1 else parity.MAX_FLAG_FRAC
+    return g, r, parity.compare(g, r, subset=subset, greedy=kw.get("T", 1.0) == 0.0, name=name, max_flag_frac=frac)
 
 
 def test_c1_full(cuda_ok):
@@ -45,7 +46,7 @@ def test_ragged_vocab(cuda_ok, V, dtype):
 
 
 @pytest.mark.parametrize("wm,sm", [(W_CONF, 0), (W_WINNER, 0), (W_UNIFORM, 0), (W_POINT, 0),
-                                   (W_CONF, 1), (W_UNIFORM, 1)])
+                                   (W_CONF, 1), (W_WINNER, 1), (W_UNIFORM, 1)])
 def test_weight_and_select_modes(cuda_ok, wm, sm):
     inp = synth.linear_inputs(32, 6, 3, 7000, dtype=torch.bfloat16, seed=100 + wm + 10 * sm)
     _run(inp, wm=wm, sm=sm)
@@ -139,6 +140,28 @@ def test_c3_full_size_all_requests(cuda_ok):
     g = parity.gpu_verify(inp)
     r = parity.oracle_verify(inp)
     parity.compare(g, r, name="c3")
+
+
+@pytest.mark.parametrize("wm", [W_CONF, W_WINNER])
+def test_c3_full_size_sample_select(cuda_ok, wm):
+    # SAMPLE selection (x* ~ fused q, reading #3) at BASELINE config c3: every request
+    c = synth.CONFIGS["c3"]
+    inp = synth.linear_inputs(c["B"], c["k"], c["N"], c["V"], dtype=c["dtype"], seed=1235, device="cuda")
+    _run(inp, wm=wm, sm=1, name=f"c3 SAMPLE wm={wm}")
+
+
+@pytest.mark.parametrize("T", [0.7, 1.3])
+def test_sample_select_logits_drafts(cuda_ok, T):
+    inp = synth.linear_inputs(24, 5, 3, 6007, dtype=torch.float32, seed=37, draft_kind="logits",
+                              draft_len="random")
+    _run(inp, T=T, draft_kind="logits", sm=1, name=f"SAMPLE logits T={T}")
+
+
+@pytest.mark.parametrize("cs", [1, 4, 16])
+def test_sample_select_chunking(cuda_ok, cs):
+    # the draw's crossing chunk comes from the statistics pass's chunk records: any chunking
+    inp = synth.linear_inputs(16, 6, 4, 20000, dtype=torch.bfloat16, seed=52)
+    _run(inp, sm=1, cluster_size=cs, name=f"SAMPLE C={cs}")
 
 
 @pytest.mark.slow
