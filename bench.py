@@ -298,7 +298,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     alg_bytes = synth.algorithmic_bytes(B, k, N, V, esz, esz)
     flush = args.flush == "on" or (args.flush == "auto" and alg_bytes < 4 * L2_BYTES)
-    scratch = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
+    # read (not write) 2x L2 between timed calls: the inputs are evicted and L2 holds only clean
+    # lines, so the timed call pays no write-back of a memset's dirty lines
+    scratch = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
 
     def step():
         ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"],
@@ -322,7 +324,7 @@ def run_ours(args):
     t_start.record(stream)
     for s in range(args.steps):
         if flush:
-            scratch.zero_()  # evict the inputs from L2 (untimed: outside this call's events)
+            scratch.sum()  # evict the inputs from L2 (untimed: outside this call's events)
         ev[s][0].record(stream)
         launches += step()
         ev[s][1].record(stream)
@@ -342,7 +344,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     for s in range(args.steps):
         if flush:
-            scratch.zero_()
+            scratch.sum()
         step()
     torch.cuda.synchronize()
     prof_ms, prof_n = cv.cosine_profile_read(ver.ctx)
@@ -427,7 +429,7 @@ def run_ours(args):
                        "weights": args.weights, "select": args.select,
                        "batch_per_gpu": B, "global_batch": B * world,
                        "k": k, "drafters": N, "vocab": V, "parallelism": f"batch-sharded x{world}",
-                       "l2": (f"L2 flushed between timed calls ({2 * L2_BYTES >> 20} MiB memset, outside the "
+                       "l2": (f"L2 flushed between timed calls (a {2 * L2_BYTES >> 20} MiB read, outside the "
                               f"timed events; inputs {alg_bytes / 1e6:.1f} MB)") if flush else
                              f"inputs {alg_bytes / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)",
                        "mean_accept_len": acc, "request_errors": status_nonzero},

@@ -171,7 +171,10 @@ void fill_scratch(const cosine_ctx_t ctx, SplitParams& S, int C) {
   S.C = C;
   S.cg = (S.ngroups + C - 1) / C;
   S.nseg = (S.ngroups + kTileGroups - 1) / kTileGroups;
+  // tiles per resample CTA: 8 for large batches; fewer (more, shorter CTAs) while the final
+  // draws of the batch fill less than ~2 waves — small batches are latency-bound
   S.tpc = kSegTilesPerCta;
+  while (S.tpc > 1 && (int64_t)S.B * ((S.nseg + S.tpc - 1) / S.tpc) < 2 * 148 * 5) S.tpc /= 2;
   S.spr = (int)((S.nseg + S.tpc - 1) / S.tpc);
   S.parts = ctx->parts;
   S.pdec = ctx->pdec;
