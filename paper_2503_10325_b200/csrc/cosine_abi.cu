@@ -34,9 +34,20 @@
 
 namespace cosine {
 
-__global__ void init_scratch(int32_t* done, int32_t* first_rej, int n) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) { done[j] = 0; first_rej[j] = kNoReject; }
+__global__ void __launch_bounds__(kThreads) fuse_finish_kernel(const SplitParams P) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the decisions (PDL)
+  const int b = blockIdx.x * kThreads + threadIdx.x;
+  if (b >= P.B) return;
+  int err = 0;
+  float tm = INFINITY;
+  for (int i = 0; i < P.k && !err; ++i) {
+    const PosDec& pd = P.pdec[(int64_t)b * P.k + i];
+    err = pd.status;
+    tm = fmin_(tm, pd.m_fa);
+  }
+  if (err)
+    for (int i = 0; i < P.k; ++i) P.fuse_tokens[(int64_t)b * P.k + i] = -1;
+  P.status[b] = err ? err : (tm < 1e-6f ? COSINE_INFO_NEAR_TIE : 0);
 }
 
 void kernel_set(cosine_dtype_t tt, cosine_dtype_t tq, bool logits, int N, KernelSet* ks) {
@@ -56,7 +67,6 @@ using namespace cosine;
 struct cosine_ctx_s {
   cosine_config_t cfg;
   int64_t V;
-  UnitRec* recs = nullptr;
   PartRec* parts = nullptr;
   PosDec* pdec = nullptr;
   int32_t* counters = nullptr;
@@ -69,8 +79,6 @@ struct cosine_ctx_s {
   int prof_on = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
   size_t prof_n = 0;
-  int32_t* done = nullptr;
-  int32_t* first_rej = nullptr;
   std::string err;
   int32_t last_launches = 0;
   int32_t last_cluster = 0, last_ncl = 0;
@@ -112,50 +120,6 @@ cosine_status_t fail(cosine_ctx_t ctx, cosine_status_t s, const std::string& msg
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 size_t esize(cosine_dtype_t t) { return t == COSINE_BF16 ? 2 : 4; }
-
-int pick_cluster(const cosine_ctx_t ctx, int64_t units, int64_t ngroups) {
-  if (ctx->cfg.cluster_size > 0) return std::min(ctx->cfg.cluster_size, 8);
-  // ~8 groups (64 elements per row) per thread, then widen while the grid is small
-  int C = 1;
-  while (C < 8 && ngroups > (int64_t)C * kThreads * 8) C *= 2;
-  while (C < 8 && units * C < 148 * 8 && ngroups >= (int64_t)C * 2 * kThreads) C *= 2;
-  return C;
-}
-
-cosine_status_t launch(cosine_ctx_t ctx, cudaStream_t stream, Params& P, int64_t units,
-                       cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
-  const int C = pick_cluster(ctx, units, P.ngroups);
-  P.C = C;
-  P.gpc = (P.ngroups + C - 1) / C;
-  P.recs = ctx->recs;
-  P.done = ctx->done;
-  P.first_rej = ctx->first_rej;
-  if (units == 0) { ctx->last_launches = 0; return COSINE_OK; }
-  KernelSet ks;
-  kernel_set(tt, tq, logits, P.N, &ks);
-  KernelFn fn = ks.unit;
-  cudaLaunchConfig_t lc;
-  memset(&lc, 0, sizeof(lc));
-  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
-  lc.blockDim = dim3(kThreads, 1, 1);
-  lc.dynamicSmemBytes = 0;
-  lc.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, fn, P);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    ctx->last_launches = 0;
-    return fail(ctx, COSINE_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
-  }
-  ctx->last_launches = 1;
-  return COSINE_OK;
-}
 
 // Chunk CTAs per unit of the streaming kernels: ~8 groups (64 elements per row) per thread,
 // then widen while the grid has fewer than ~8 CTAs per SM.
@@ -483,20 +447,24 @@ cosine_status_t launch_lazy(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& 
   return COSINE_OK;
 }
 
-void fill_common(Params& P, const cosine_ctx_t ctx, int B, int k, int N, float T) {
-  memset(&P, 0, sizeof(P));
-  P.B = B;
-  P.k = k;
-  P.N = N;
-  P.V = ctx->V;
-  P.ngroups = (ctx->V + kGroup - 1) / kGroup;
-  P.gfull = ctx->V / kGroup;
-  P.T = T;
-  P.greedy = (T == 0.f);
-  const double k2 = (T > 0.f) ? 1.4426950408889634 / (double)T : 0.0;
-  P.k2d = k2;
-  P.k2f = (float)k2;
-  P.seed = ctx->cfg.seed;
+// The vocabulary geometry and temperature constants of a call.
+struct CallDims {
+  int64_t V, ngroups, gfull;
+  int greedy;
+  float k2f;  // log2(e) / T (T = 0: greedy, 0)
+  double k2d;
+  uint64_t seed;
+};
+CallDims call_dims(const cosine_ctx_t ctx, float T) {
+  CallDims D;
+  D.V = ctx->V;
+  D.ngroups = (ctx->V + kGroup - 1) / kGroup;
+  D.gfull = ctx->V / kGroup;
+  D.greedy = (T == 0.f);
+  D.k2d = (T > 0.f) ? 1.4426950408889634 / (double)T : 0.0;
+  D.k2f = (float)D.k2d;
+  D.seed = ctx->cfg.seed;
+  return D;
 }
 
 cosine_status_t check_rows(cosine_ctx_t ctx, const void* p, int64_t ld, cosine_dtype_t t,
@@ -556,9 +524,7 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
   ctx->V = cfg->vocab_end - cfg->vocab_begin;
   DeviceGuard dg(cfg->device);
   const size_t nb = (size_t)std::max(cfg->max_batch, 1);
-  cudaError_t e = cudaMalloc(&ctx->recs, nb * (size_t)(cfg->max_draft_len + 1) * sizeof(UnitRec));
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->done, nb * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->first_rej, nb * sizeof(int32_t));
+  cudaError_t e = cudaSuccess;
   const size_t nu = nb * (size_t)std::max(cfg->max_draft_len + 1, std::max(cfg->max_tree_nodes, 1));
   const size_t nt = nb * (size_t)std::max(cfg->max_tree_nodes, 1);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ndec, nt * sizeof(NodeDec));
@@ -574,10 +540,6 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
   if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, ncnt * sizeof(int32_t));
   ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
-  if (e == cudaSuccess) {
-    init_scratch<<<(unsigned)((nb + 255) / 256), 256>>>(ctx->done, ctx->first_rej, (int)nb);
-    e = cudaGetLastError();
-  }
   if (e == cudaSuccess && cfg->nranks > 1) {  // vocabulary-sharded: exchange buffers + communicator
     const size_t units = nb * (size_t)(cfg->max_draft_len + 1);
     const size_t rb = units * (size_t)shard_rec_words(cfg->max_drafters) * 4;
@@ -607,9 +569,6 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
     cudaFree(ctx->yall);
     cudaFree(ctx->lz);
     cudaGetLastError();
-    cudaFree(ctx->recs);
-    cudaFree(ctx->done);
-    cudaFree(ctx->first_rej);
     cudaFree(ctx->parts);
     cudaFree(ctx->pdec);
     cudaFree(ctx->counters);
@@ -656,9 +615,6 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   if (!ctx) return COSINE_OK;
   DeviceGuard dg(ctx->cfg.device);
   cudaDeviceSynchronize();
-  cudaFree(ctx->recs);
-  cudaFree(ctx->done);
-  cudaFree(ctx->first_rej);
   cudaFree(ctx->parts);
   cudaFree(ctx->pdec);
   cudaFree(ctx->counters);
@@ -747,25 +703,56 @@ cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int
   if (fused_q && (ld_fq < ctx->V || !aligned16(fused_q) || (ld_fq * 4) % 16 != 0))
     return fail(ctx, COSINE_ERR_UNSUPPORTED, "fused_q must be 16-byte aligned with ld_fq >= V");
   DeviceGuard dg(ctx->cfg.device);
-  Params P;
-  fill_common(P, ctx, B, k, N, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS ? temperature : 1.f);
-  P.greedy = 0;
-  P.mode = kModeFuse;
-  P.ld_q = ld_q;
-  P.ld_fq = ld_fq;
-  P.draft = draft;
-  P.draft_tokens = draft_tokens;
-  P.rids = request_ids;
-  P.step = step;
-  P.weight_mode = weight_mode;
-  P.select_mode = select_mode;
-  P.fused_tokens = fused_tokens;
-  P.w_out = weights;
-  P.norm_out = draft_norm;
-  P.fused_q = fused_q;
-  P.status = status;
-  return launch(ctx, (cudaStream_t)stream, P, (int64_t)B * k, ctx->cfg.target_dtype,
-                ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
+  const CallDims P0 = call_dims(ctx, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS ? temperature : 1.f);
+  SplitParams S;
+  memset(&S, 0, sizeof(S));
+  S.mode = kSplitFuse;
+  S.B = B; S.k = k; S.N = N;
+  S.V = P0.V; S.ld_t = ld_q; S.ld_q = ld_q; S.ngroups = P0.ngroups; S.gfull = P0.gfull;
+  S.k2f = P0.k2f; S.k2d = P0.k2d; S.greedy = 0; S.weight_mode = weight_mode; S.select = select_mode;
+  S.draft = draft; S.target = draft; S.draft_tokens = draft_tokens; S.rids = request_ids; S.seed = P0.seed;
+  S.step = step; S.status = status;
+  S.fuse_tokens = fused_tokens; S.fuse_w = weights; S.fuse_sig = draft_norm; S.fused_q = fused_q; S.ld_fq = ld_fq;
+  const int64_t units = (int64_t)B * k;
+  fill_scratch(ctx, S, stats_chunks(ctx, units, S.ngroups));
+  // the drafter rows stand in for the (absent) target rows of the statistics kernel, so it runs
+  // with the drafters' dtype on both (stats_body, kSplitFuse)
+  KernelSet ks;
+  kernel_set(ctx->cfg.draft_dtype, ctx->cfg.draft_dtype, ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS, N, &ks);
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.gridDim = dim3((unsigned)(units * S.C), 1, 1);
+  cudaError_t e = cudaLaunchKernelEx(&lc, ks.stats, S);
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int launches = 1;
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)units, 1, 1);
+    e = cudaLaunchKernelEx(&lc, ks.fuse_decide, S);
+    ++launches;
+  }
+  if (e == cudaSuccess && fused_q) {
+    lc.gridDim = dim3((unsigned)(units * S.C), 1, 1);
+    e = cudaLaunchKernelEx(&lc, ks.fuse_write_q, S);
+    ++launches;
+  }
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)((B + kThreads - 1) / kThreads), 1, 1);
+    e = cudaLaunchKernelEx(&lc, fuse_finish_kernel, S);
+    ++launches;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("fuse_drafts kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = launches;
+  return COSINE_OK;
 }
 
 // Argument checks shared by cosine_verify_batch and cosine_verify_batch_vgroup.
@@ -796,14 +783,14 @@ static SplitParams make_split(cosine_ctx_t ctx, int32_t B, int32_t k, int32_t N,
                               int64_t ld_t, float temperature, const void* draft, int64_t ld_q,
                               const int32_t* draft_tokens, const int32_t* draft_len, const uint64_t* request_ids,
                               uint32_t step, cosine_weight_mode_t weight_mode, int32_t* accept_len,
-                              int32_t* out_tokens, int32_t* status, const cosine_debug_t* debug) {
-  Params P;
-  fill_common(P, ctx, B, k, N, temperature);
+                              int32_t* out_tokens, int32_t* status, const cosine_debug_t* debug,
+                              cosine_select_mode_t select_mode = COSINE_SEL_ARGMAX) {
+  const CallDims P = call_dims(ctx, temperature);
   SplitParams S;
   memset(&S, 0, sizeof(S));
   S.B = B; S.k = k; S.N = N;
   S.V = P.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P.ngroups; S.gfull = P.gfull;
-  S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode;
+  S.k2f = P.k2f; S.k2d = P.k2d; S.greedy = P.greedy; S.weight_mode = weight_mode; S.select = select_mode;
   S.target = target_logits; S.draft = draft; S.draft_tokens = draft_tokens; S.draft_len = draft_len;
   S.rids = request_ids; S.seed = P.seed; S.step = step;
   S.accept_len = accept_len; S.out_tokens = out_tokens; S.status = status;
@@ -835,7 +822,7 @@ cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, in
                         ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS);
   }
   SplitParams S = make_split(ctx, B, k, N, target_logits, ld_t, temperature, draft, ld_q, draft_tokens, draft_len,
-                             request_ids, step, weight_mode, accept_len, out_tokens, status, debug);
+                             request_ids, step, weight_mode, accept_len, out_tokens, status, debug, select_mode);
   return launch_split(ctx, (cudaStream_t)stream, S, ctx->cfg.target_dtype, ctx->cfg.draft_dtype,
                       ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS, select_mode == COSINE_SEL_SAMPLE);
 }
@@ -895,8 +882,7 @@ cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t strea
   if (temperature == 0.f && ctx->cfg.draft_kind == COSINE_DRAFT_LOGITS)
     return fail(ctx, COSINE_ERR_UNSUPPORTED, "greedy (T = 0) needs PROBS drafts");
   DeviceGuard dg(ctx->cfg.device);
-  Params P;
-  fill_common(P, ctx, B, k, N, temperature);
+  const CallDims P = call_dims(ctx, temperature);
   SplitParams S;
   memset(&S, 0, sizeof(S));
   S.B = B; S.k = k; S.N = N;
@@ -943,8 +929,7 @@ static cosine_status_t verify_tree_impl(bool lazy, cosine_ctx_t ctx, cosine_stre
   if ((ngroups + tg - 1) / tg > kMaxSeg)
     return fail(ctx, COSINE_ERR_UNSUPPORTED, "vocabulary too wide for the tree sampler");
   DeviceGuard dg(ctx->cfg.device);
-  Params P0;
-  fill_common(P0, ctx, B, 1, N, temperature);
+  const CallDims P0 = call_dims(ctx, temperature);
   TreeParams T;
   memset(&T, 0, sizeof(T));
   SplitParams& S = T.S;
@@ -1190,24 +1175,49 @@ cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream,
   if (!(temperature >= 0.f) || !std::isfinite(temperature))
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "temperature must be finite and >= 0");
   DeviceGuard dg(ctx->cfg.device);
-  Params P;
-  fill_common(P, ctx, B, 1, Nc, temperature);
-  P.mode = kModeSample;
-  P.ld_t = ld_t;
-  P.ld_q = ld_q;
-  P.target = target_rows;
-  P.draft = draft_rows;
-  P.row_max = row_max;
-  P.row_sumexp = row_sumexp;
-  P.w_in = weights;
-  P.norm_in = draft_norm;
-  P.node_ids = node_ids;
-  P.rids = request_ids;
-  P.step = step;
-  P.out_token = out_token;
-  P.status = status;
-  return launch(ctx, (cudaStream_t)stream, P, (int64_t)B, ctx->cfg.target_dtype,
-                ctx->cfg.draft_dtype, false);
+  const CallDims P0 = call_dims(ctx, temperature);
+  SplitParams S;
+  memset(&S, 0, sizeof(S));
+  S.mode = kSplitSample;
+  S.B = B; S.k = 1; S.N = draft_rows ? N : 0;
+  S.V = P0.V; S.ld_t = ld_t; S.ld_q = ld_q; S.ngroups = P0.ngroups; S.gfull = P0.gfull;
+  S.k2f = P0.k2f; S.k2d = P0.k2d; S.greedy = P0.greedy; S.weight_mode = COSINE_W_CONF;
+  S.target = target_rows; S.draft = draft_rows; S.rids = request_ids; S.seed = P0.seed; S.step = step;
+  S.row_max = row_max; S.row_sumexp = row_sumexp; S.w_in = weights; S.norm_in = draft_norm;
+  S.node_ids = node_ids; S.out_token = out_token; S.status = status;
+  fill_scratch(ctx, S, stats_chunks(ctx, B, S.ngroups));
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
+    return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
+  KernelSet ks;
+  kernel_set(ctx->cfg.target_dtype, ctx->cfg.draft_dtype, false, std::max(N, 1), &ks);
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.gridDim = dim3((unsigned)((int64_t)B * S.C), 1, 1);
+  cudaError_t e = cudaLaunchKernelEx(&lc, ks.stats, S);  // row statistics and validity checks
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)((B + kWarps - 1) / kWarps), 1, 1);
+    e = cudaLaunchKernelEx(&lc, ks.sample_prep, S);
+  }
+  if (e == cudaSuccess) {
+    lc.gridDim = dim3((unsigned)(B * S.spr), 1, 1);
+    e = cudaLaunchKernelEx(&lc, ks.resample, S);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaMemsetAsync(ctx->counters, 0, ctx->counters_bytes, (cudaStream_t)stream);
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    return fail(ctx, COSINE_ERR_CUDA, std::string("sample_residual kernels: ") + cudaGetErrorString(e));
+  }
+  ctx->last_launches = 3;
+  return COSINE_OK;
 }
 
 }  // extern "C"

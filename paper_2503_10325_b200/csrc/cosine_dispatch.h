@@ -5,25 +5,25 @@
 #pragma once
 
 #include "cosine_tree.cuh"
-#include "cosine_unit.cuh"
 
 namespace cosine {
 
 using SplitFn = void (*)(SplitParams);
 using TreeFn = void (*)(TreeParams);
-using KernelFn = void (*)(Params);
 
 struct KernelSet {
   SplitFn stats;         // stats_kernel (lazy rounds, tree all-nodes, sharded)
   SplitFn lazy_decide;   // lazy round decisions (NEXT-1)
   SplitFn decide;        // split path decisions (stats -> decide -> resample)
   SplitFn sample_decide; // the same with SAMPLE selection (x* ~ fused q)
+  SplitFn fuse_decide;   // cosine_fuse_drafts: Eq. 4 fusion per unit
+  SplitFn fuse_write_q;  // cosine_fuse_drafts: the fused distribution rows
+  SplitFn sample_prep;   // cosine_sample_residual: the request records
   SplitFn resample;      // final draws
   SplitFn shard_pack;    // vocabulary-sharded records
   SplitFn shard_sample;  // vocabulary-sharded owner scan
   TreeFn tree_decide;
   TreeFn tree_walk;
-  KernelFn unit;         // legacy cluster kernel (SAMPLE select, fuse_drafts, sample_residual)
 };
 
 void kernel_set_bb(bool logits, int N, KernelSet* out);  // bf16 target, bf16 drafts

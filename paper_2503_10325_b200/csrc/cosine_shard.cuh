@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
   if (tid == 0) {
     const ReqView v = request_view(P, s_pd, g);
     s_v = v;
-    if (v.sample) s_d = sample_decision(P, P.rids[b], s_pd[v.L], v);
+    if (v.sample) s_d = sample_decision(P, b, s_pd[v.L], v);
   }
   __syncthreads();
   const ReqView v = s_v;

@@ -34,7 +34,23 @@ struct PartRec {  // one per (unit, chunk); 128 bytes
 constexpr int kMaxPos = 65;  // draft positions per request (k <= 64) in kernel B
 constexpr int kLazySpan = 2;  // positions per lazy round (NEXT-1)
 
+enum SplitMode : int { kSplitVerify = 0, kSplitFuse = 1, kSplitSample = 2 };
+
 struct SplitParams {
+  int mode;  // kSplitVerify (cosine_verify_batch / _lazy / _tree), kSplitFuse, kSplitSample
+  // cosine_fuse_drafts outputs
+  int32_t* fuse_tokens;
+  float* fuse_w;
+  float* fuse_sig;
+  float* fused_q;
+  int64_t ld_fq;
+  // cosine_sample_residual inputs / outputs (mode kSplitSample: request b = one row group)
+  const float* row_max;
+  const float* row_sumexp;
+  const float* w_in;
+  const float* norm_in;
+  const uint32_t* node_ids;
+  int32_t* out_token;
   int B, k, N;
   int64_t V, ld_t, ld_q, ngroups, gfull;
   int C;          // CTAs per unit (kernel A)
@@ -43,7 +59,7 @@ struct SplitParams {
   int64_t cg2;    // groups per chunk (kernel B)
   float k2f;
   double k2d;
-  int greedy, weight_mode;
+  int greedy, weight_mode, select;
   const void* target;
   const void* draft;
   const int32_t* draft_tokens;
@@ -178,7 +194,21 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
   const TT* trow;
   const TQ* drow;
   int64_t gu;  // the unit's index in the partial-record array
-  if (P.tree) {  // node (b, j): target row j, the N drafter rows of its internal row (if any)
+  if (P.mode == kSplitFuse) {  // cosine_fuse_drafts: unit (b, i < k), drafter rows only
+    // (no target row: the "target" statistics of the record are taken over drafter row 0 —
+    // its second load of each group is an L2 hit — and ignored by fuse_decide_kernel; this
+    // keeps the streaming loop free of a target-present branch)
+    const int b = (int)(unit / P.k), i = (int)(unit % P.k);
+    Nd = N;
+    drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
+    trow = reinterpret_cast<const TT*>(drow);
+    gu = unit;
+  } else if (P.mode == kSplitSample) {  // cosine_sample_residual: unit b = one target row (+ N drafter rows)
+    Nd = P.draft ? N : 0;
+    trow = (const TT*)P.target + unit * P.ld_t;
+    drow = (const TQ*)P.draft + unit * N * P.ld_q;
+    gu = unit;
+  } else if (P.tree) {  // node (b, j): target row j, the N drafter rows of its internal row (if any)
     const int b = (int)(unit / P.nn);
     const int ir = P.irow[unit];
     Nd = (ir >= 0 && ir < P.I) ? N : 0;
@@ -481,8 +511,10 @@ __device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i,
     } else {
       for (int n = 0; n < N; ++n) w[n] = (n == ns) ? 1.0 : 0.0;
     }
-    if (w_sample) {  // SAMPLE selection: x* ~ q is drawn by the caller (sample_decide_kernel)
-      if (P.weight_mode != COSINE_W_WINNER) pd.m_fa = INFINITY;  // n* does not matter then
+    if (w_sample) {  // x* is the caller's (SAMPLE: a draw from q; cosine_fuse_drafts)
+      pd.xstar = tok[ns];
+      // n* matters for the ARGMAX token and for WINNER weights only
+      if (P.weight_mode != COSINE_W_WINNER && P.select != COSINE_SEL_ARGMAX) pd.m_fa = INFINITY;
       for (int n = 0; n < N; ++n) {
         w_sample[n] = w[n];
         pd.a[n] = (float)(w[n] / sig[n]);
@@ -530,10 +562,11 @@ struct UnitFlags {
 template <typename TT, typename TQ, bool kLogits>
 __device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, int i, bool has_d, bool diag_only,
                                                   float* s_gxw, int32_t* s_tokw, PosDec& pd, double* sig,
-                                                  float* dmax) {
+                                                  float* dmax, bool has_t = true) {
   const int lane = threadIdx.x & 31;
   const int N = P.N, C = P.C;
-  const int64_t unit = (int64_t)b * (P.k + 1) + i;
+  // the unit's record index (cosine_fuse_drafts units have no target row: b * k + i)
+  const int64_t unit = has_t ? (int64_t)b * (P.k + 1) + i : (int64_t)b * P.k + i;
   const bool greedy = P.greedy != 0;
   const double k2 = (double)P.k2f;
   const int ng = has_d ? N * (N + 1) : 0;
@@ -541,7 +574,7 @@ __device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, i
     const int n = lane % N, m = lane / N;
     const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
     float v = 0.f;
-    if (tk >= 0 && (int64_t)tk < P.V && (!diag_only || m == n)) {
+    if (tk >= 0 && (int64_t)tk < P.V && (!diag_only || m == n) && (m < N || has_t)) {
       if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
       else v = load_one((const TT*)P.target + ((int64_t)b * (P.k + 1) + i) * P.ld_t, tk);
     }
@@ -555,7 +588,9 @@ __device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, i
   const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
   init_posdec(pd);
   UnitFlags f = {false, false, false, false, false};
-  if (greedy) {
+  if (!has_t) {
+    // no target row (its record fields are ignored)
+  } else if (greedy) {
     float bv = own ? tmax : -INFINITY;
     int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
     warp_argmax(bv, bi);
@@ -650,6 +685,72 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   }
 }
 
+// One warp: the crossing chunk of t = u Q for a draw from the fused q = sum_n w_n q_n of record
+// unit `rec` (SAMPLE selection, reading #3; u = U(rid, node, FUSE)).  The chunk masses come from
+// the statistics pass's records: chunk r holds sum_n (w_n / sigma_n) dsum_{n,r} (LOGITS drafts:
+// rescaled from the chunk max to the row max).  Lane 0 writes the kWFuseQ decision and the
+// chunk's group range [g0, g1) with the target tc = t - (mass before the chunk) (reading #10;
+// rounding past the total: the last positive chunk with tc = +inf).
+template <bool kLogits>
+__device__ __forceinline__ void chunk_crossing_warp(const SplitParams& P, int64_t rec, uint32_t node, uint64_t rid,
+                                                    const double* s_w, const double* s_sig, const float* s_dmax,
+                                                    Decision* s_d, int64_t* s_g0, int64_t* s_g1, double* s_tc,
+                                                    double* s_Q) {
+  const int lane = threadIdx.x & 31;
+  const int N = P.N, C = P.C;
+  const double k2 = (double)P.k2f;
+  double m = 0.0;
+  if (lane < C) {
+    const PartRec* pr = P.parts + rec * C + lane;
+    for (int n = 0; n < N; ++n) {
+      const double ds = __ldcg(&pr->dsum[n]);
+      double sc = 1.0;
+      if (kLogits) sc = exp2((double)__ldcg(&pr->dmax[n]) * k2 - (double)s_dmax[n] * k2);
+      if (ds != 0.0) m += (s_w[n] / s_sig[n]) * ds * sc;
+    }
+  }
+  double incl = m;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += nb;
+  }
+  const double Q = __shfl_sync(0xffffffffu, incl, 31);
+  const double u = philox_u24(P.seed, rid, node, P.step, kTagFuse);
+  const double t = u * Q;
+  const unsigned hit = __ballot_sync(0xffffffffu, lane < C && m > 0.0 && incl > t);
+  const unsigned pos = __ballot_sync(0xffffffffu, lane < C && m > 0.0);
+  int r;
+  double tc;
+  if (hit) {
+    r = __ffs(hit) - 1;
+    tc = t - (__shfl_sync(0xffffffffu, incl, r) - __shfl_sync(0xffffffffu, m, r));
+  } else {
+    r = pos ? 31 - __clz(pos) : 0;
+    tc = INFINITY;
+  }
+  if (lane == 0) {
+    *s_g0 = (int64_t)r * P.cg;
+    *s_g1 = min(P.ngroups, *s_g0 + P.cg);
+    *s_tc = tc;
+    *s_Q = Q;
+    Decision d;
+    d.need = 1;
+    d.kind = kWFuseQ;
+    d.xstar = -1;
+    d.node = node;
+    d.u = u;
+    d.M = 0.f;
+    d.invS = 0.f;
+    d.k2 = P.k2f;
+    for (int n = 0; n < kMaxN; ++n) {
+      d.a[n] = (n < N) ? (float)(s_w[n] / s_sig[n]) : 0.f;
+      d.dm[n] = (n < N) ? s_dmax[n] : 0.f;
+    }
+    *s_d = d;
+  }
+}
+
 // Kernel B1 for SAMPLE selection (reading #3: x*_i ~ the fused q_i, the distribution-exact
 // fusion; "direct ensemble sampling"): one CTA per unit, a programmatic dependent
 // of stats_kernel that waits for its unit's C chunk records.
@@ -710,59 +811,8 @@ __global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitPara
       s_pd = pd;
     }
     __syncwarp();
-    if (s_go) {
-      // the fused q's mass over chunk `lane` (PROBS: raw sums; LOGITS: relative to the chunk max)
-      double m = 0.0;
-      if (lane < C) {
-        const PartRec* pr = P.parts + gu * C + lane;
-        for (int n = 0; n < N; ++n) {
-          const double ds = __ldcg(&pr->dsum[n]);
-          double sc = 1.0;
-          if (kLogits) sc = exp2((double)__ldcg(&pr->dmax[n]) * k2 - (double)s_dmax[n] * k2);
-          if (ds != 0.0) m += (s_w[n] / s_sig[n]) * ds * sc;
-        }
-      }
-      double incl = m;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double nb = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += nb;
-      }
-      const double Q = __shfl_sync(0xffffffffu, incl, 31);
-      const double u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagFuse);
-      const double t = u * Q;
-      const unsigned hit = __ballot_sync(0xffffffffu, lane < C && m > 0.0 && incl > t);
-      const unsigned pos = __ballot_sync(0xffffffffu, lane < C && m > 0.0);
-      int r;
-      double tc;
-      if (hit) {
-        r = __ffs(hit) - 1;
-        tc = t - (__shfl_sync(0xffffffffu, incl, r) - __shfl_sync(0xffffffffu, m, r));
-      } else {  // rounding past the total: the last positive chunk's last positive entry
-        r = pos ? 31 - __clz(pos) : 0;
-        tc = INFINITY;
-      }
-      if (lane == 0) {
-        s_g0 = (int64_t)r * P.cg;
-        s_g1 = min(P.ngroups, s_g0 + P.cg);
-        s_tc = tc;
-        s_Q = Q;
-        Decision d;
-        d.need = 1;
-        d.kind = kWFuseQ;
-        d.xstar = -1;
-        d.node = (uint32_t)(i + 1);
-        d.u = u;
-        d.M = 0.f;
-        d.invS = 0.f;
-        d.k2 = P.k2f;
-        for (int n = 0; n < kMaxN; ++n) {
-          d.a[n] = (n < N) ? (float)(s_w[n] / s_sig[n]) : 0.f;
-          d.dm[n] = (n < N) ? s_dmax[n] : 0.f;
-        }
-        s_d = d;
-      }
-    }
+    if (s_go) chunk_crossing_warp<kLogits>(P, gu, (uint32_t)(i + 1), P.rids[b], s_w, s_sig, s_dmax, &s_d, &s_g0, &s_g1,
+                                           &s_tc, &s_Q);
   }
   __syncthreads();
   if (s_go) {
@@ -795,6 +845,202 @@ __global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitPara
     __threadfence();  // the decision before its count (release)
     atomicAdd(&P.dcnt[b], 1);
   }
+}
+
+// ============================== cosine_fuse_drafts ==============================
+// Eq. 4 token fusion alone (Alg. 1 TokenFusion P:376-381) on the split kernels:
+// stats_kernel (P.mode = kSplitFuse: unit (b, i < k), the N drafter rows) -> fuse_decide_kernel
+// (CTA per unit: sigma, confidences, weights, x* = X_{n*} or x* ~ q) -> [fuse_write_q_kernel]
+// -> fuse_finish_kernel (per-request status: the first erroring position voids the request).
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads) fuse_decide_kernel(const SplitParams P) {
+  __shared__ float s_gx[(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kMaxN];
+  __shared__ PosDec s_pd;
+  __shared__ Decision s_d;
+  __shared__ double s_w[kMaxN], s_sig[kMaxN];
+  __shared__ float s_dmax[kMaxN];
+  __shared__ double s_scan[kWarps];
+  __shared__ int64_t s_wi[kWarps];
+  __shared__ int64_t s_found, s_g0, s_g1;
+  __shared__ float s_margin;
+  __shared__ double s_tc, s_Q;
+  __shared__ int s_go;
+  const int tid = threadIdx.x, lane = tid & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // stats_kernel's records (PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t unit = blockIdx.x;  // b * k + i
+  if (unit >= (int64_t)P.B * P.k) return;
+  const int b = (int)(unit / P.k), i = (int)(unit % P.k);
+  const int N = P.N;
+  const TQ* drow = (const TQ*)P.draft + unit * N * P.ld_q;
+  if (tid < 32) {
+    PosDec pd;
+    double sig[kMaxN];
+    float dmax[kMaxN];
+    const UnitFlags f = warp_combine<TT, TQ, kLogits>(P, b, i, true, true, s_gx, s_tok, pd, sig, dmax, false);
+    if (lane == 0) {
+      decide_lane0<kLogits>(P, b, i, true, f.tok_bad, f.d_nf, f.d_empty, s_gx, s_tok, sig, dmax, pd, s_w);
+      s_go = (pd.status == 0 && P.select == COSINE_SEL_SAMPLE) ? 1 : 0;
+      for (int n = 0; n < N; ++n) { s_sig[n] = sig[n]; s_dmax[n] = dmax[n]; }
+      s_pd = pd;
+    }
+    __syncwarp();
+    if (s_go) chunk_crossing_warp<kLogits>(P, unit, (uint32_t)(i + 1), P.rids[b], s_w, s_sig, s_dmax, &s_d, &s_g0,
+                                           &s_g1, &s_tc, &s_Q);
+  }
+  __syncthreads();
+  if (s_go) {  // SAMPLE: x* ~ q, scanned in its crossing chunk (reading #10)
+    const int64_t y = scan_range<TT, TQ, kLogits, NMAX>(P, s_d, kWFuseQ, reinterpret_cast<const TT*>(drow), drow, N,
+                                                        s_g0, s_g1, s_tc, s_Q, s_scan, s_wi, &s_found, &s_margin);
+    if (tid == 0) {
+      s_pd.xstar = (int32_t)y;
+      s_pd.m_fa = fmin_(s_pd.m_fa, s_margin);
+      if (y < 0) s_pd.status = COSINE_REQ_EMPTY_ROW;  // unreachable: q has mass
+    }
+  }
+  if (tid == 0) {
+    const PosDec& pd = s_pd;
+    P.pdec[unit] = pd;  // status, x*, margin, a = w / sigma (fuse_write_q_kernel, fuse_finish_kernel)
+    P.fuse_tokens[unit] = pd.status ? -1 : pd.xstar;
+    for (int n = 0; n < N; ++n) {
+      if (P.fuse_w) P.fuse_w[unit * N + n] = pd.status ? NAN : pd.w[n];
+      if (P.fuse_sig) P.fuse_sig[unit * N + n] = pd.status ? NAN : pd.sig[n];
+    }
+  }
+}
+
+// The fused distribution q_i(v) = sum_n w_n d_n(v) / sigma_n (POINT: delta_{x*}) into
+// fused_q [B][k][ld_fq] fp32: CTA (unit, chunk), one group per thread per step.
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads) fuse_write_q_kernel(const SplitParams P) {
+  __shared__ PosDec s_pd;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // fuse_decide_kernel's decisions (PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t unit = blockIdx.x / P.C;
+  const int rank = (int)(blockIdx.x % P.C);
+  const int N = P.N;
+  if (threadIdx.x == 0) s_pd = P.pdec[unit];
+  __syncthreads();
+  if (s_pd.status) return;
+  Decision d;
+  d.k2 = P.k2f;
+  for (int n = 0; n < kMaxN; ++n) {
+    d.a[n] = s_pd.a[n];
+    d.dm[n] = s_pd.dm[n];
+  }
+  const TQ* drow = (const TQ*)P.draft + unit * N * P.ld_q;
+  float* qrow = P.fused_q + unit * P.ld_fq;
+  const int64_t gb = (int64_t)rank * P.cg, ge = min(P.ngroups, gb + P.cg);
+  for (int64_t gi = gb + threadIdx.x; gi < ge; gi += kThreads) {
+    float w[8];
+    if (P.weight_mode == COSINE_W_POINT) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w[e] = (gi * kGroup + e == (int64_t)s_pd.xstar) ? 1.f : 0.f;
+    } else {
+      group_weights<TT, TQ, kLogits, NMAX>(P, d, kWWriteQ, reinterpret_cast<const TT*>(drow), drow, N, gi, w);
+    }
+    if (gi < P.gfull) {
+      float4* o = reinterpret_cast<float4*>(qrow + gi * kGroup);
+      o[0] = make_float4(w[0], w[1], w[2], w[3]);
+      o[1] = make_float4(w[4], w[5], w[6], w[7]);
+    } else {
+      for (int e = 0; e < 8; ++e)
+        if (gi * kGroup + e < P.V) qrow[gi * kGroup + e] = w[e];
+    }
+  }
+}
+
+// Per request: the first erroring position's status voids every fused token (as the oracle
+// does); otherwise INFO_NEAR_TIE when a decision margin is < 1e-6 (reading #18).
+__global__ void __launch_bounds__(kThreads) fuse_finish_kernel(const SplitParams P);
+
+// ============================== cosine_sample_residual ==============================
+// The final-token draw alone on the split kernels: stats_kernel (mode kSplitSample:
+// unit b = request b's row, + its N drafter rows for the residual's validity checks) ->
+// sample_prep_kernel (warp per request: the row statistics — or the caller's M, S — and the
+// caller's weights / normalisers as the request's two position records: position 0 "rejected"
+// (residual, g = 1) or accepted (bonus)) -> resample_kernel (the tile masses and the scan).
+template <typename TT, typename TQ>
+__global__ void __launch_bounds__(kThreads) sample_prep_kernel(const SplitParams P) {
+  __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kWarps][kMaxN];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // stats_kernel's records (PDL)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int b = blockIdx.x * kWarps + warp;
+  if (b >= P.B) return;
+  const int N = P.N;
+  const bool has_d = P.draft != nullptr;
+  const bool greedy = P.greedy != 0;
+  // the records of unit b: combine as warp_combine does (no gathers)
+  const PartRec* parts = P.parts + (int64_t)b * P.C;
+  const bool own = lane < P.C;
+  const double k2 = (double)P.k2f;
+  const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
+  float M = 0.f;
+  double S = 0.0;
+  int64_t amax = -1;
+  bool t_nf = false, t_empty = false, d_nf = false;
+  if (greedy) {
+    float bv = own ? tmax : -INFINITY;
+    int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
+    warp_argmax(bv, bi);
+    t_nf = (bad & 1) != 0;
+    t_empty = bi < 0;
+    amax = bi;
+    M = bv;
+  } else {
+    M = warp_max(tmax);
+    const double tsum = own ? __ldcg(&parts[lane].tsum) : 0.0;
+    S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
+    // NaN / +inf anywhere in the row makes the (recomputed) sum non-finite
+    t_nf = !isfinite(S) || !isfinite(M);
+    t_empty = !t_nf && !(S > 0.0);
+  }
+  if (has_d) {
+    if (bad & 2) d_nf = true;
+    for (int n = 0; n < N; ++n) {
+      const double sv = warp_sum(own ? __ldcg(&parts[lane].dsum[n]) : 0.0);
+      if (!isfinite(sv)) d_nf = true;
+    }
+  }
+  (void)s_gx;
+  (void)s_tok;
+  if (lane != 0) return;
+  int st = 0;
+  if (!greedy && P.row_max) {  // the caller's statistics (M = max l, S = sum exp((l - M) / T))
+    M = P.row_max[b];
+    S = (double)P.row_sumexp[b];
+    t_empty = !t_nf && !(S > 0.0 && isfinite(S) && isfinite(M));
+  }
+  if (t_nf) st = COSINE_REQ_NONFINITE_INPUT;
+  else if (t_empty) st = COSINE_REQ_EMPTY_ROW;
+  if (!st && !greedy && has_d) {
+    if (d_nf) st = COSINE_REQ_NONFINITE_INPUT;
+    for (int n = 0; n < N && !st; ++n) {
+      const float nv = P.norm_in[(int64_t)b * N + n];
+      if (!(nv > 0.f) || !isfinite(nv)) st = COSINE_REQ_EMPTY_ROW;
+    }
+  }
+  PosDec pd;
+  init_posdec(pd);
+  pd.status = st;
+  pd.M = M;
+  pd.S = S;
+  pd.amax = amax;
+  pd.m_fa = INFINITY;
+  for (int n = 0; n < N; ++n) {
+    pd.a[n] = has_d ? (float)((double)P.w_in[(int64_t)b * N + n] / (double)P.norm_in[(int64_t)b * N + n]) : 0.f;
+    pd.dm[n] = 0.f;
+  }
+  // position 0 rejected -> the residual of position 0 (L = 0 < g = 1); accepted -> the bonus (L = g)
+  pd.accept = has_d ? 0 : 1;
+  PosDec* out = P.pdec + (int64_t)b * 2;
+  out[0] = pd;
+  pd.status = 0;
+  out[1] = pd;
 }
 
 // Lazy round r (NEXT-1): one warp per request still verifying decides position r (as
@@ -875,15 +1121,17 @@ __device__ __forceinline__ ReqView request_view(const SplitParams& P, const PosD
   return v;
 }
 
-__device__ __forceinline__ Decision sample_decision(const SplitParams& P, uint64_t rid, const PosDec& pl,
+__device__ __forceinline__ Decision sample_decision(const SplitParams& P, int b, const PosDec& pl,
                                                     const ReqView& v) {
+  const uint64_t rid = P.rids[b];
   const bool resid = v.L < v.g;
   Decision d;
   d.need = 1;
   d.kind = resid ? ((P.weight_mode == COSINE_W_POINT) ? kWPoint : kWResidual) : kWBonus;
   d.xstar = pl.xstar - (int32_t)P.v0;  // local column (vocabulary-sharded mode)
-  d.node = (uint32_t)v.L;
-  d.u = philox_u24(P.seed, rid, (uint32_t)v.L, P.step, kTagSample);
+  // Philox node of the draw: L (reading #19); cosine_sample_residual: the caller's node id
+  d.node = (P.mode == kSplitSample) ? P.node_ids[b] : (uint32_t)v.L;
+  d.u = philox_u24(P.seed, rid, d.node, P.step, kTagSample);
   d.M = pl.M;
   d.invS = (float)(1.0 / pl.S);
   d.k2 = P.k2f;
@@ -1040,7 +1288,7 @@ __device__ __forceinline__ void load_request(const SplitParams& P, int b, int g,
   if (tid == 0) {
     const ReqView v = request_view(P, s.pd, g);
     s.v = v;
-    if (v.sample) s.d = sample_decision(P, P.rids[b], s.pd[v.L], v);
+    if (v.sample) s.d = sample_decision(P, b, s.pd[v.L], v);
   }
   __syncthreads();
 }
@@ -1049,6 +1297,13 @@ __device__ __forceinline__ void load_request(const SplitParams& P, int b, int g,
 // row L, reading #7).  Threads of one CTA.
 __device__ __forceinline__ void write_plain_outputs(const SplitParams& P, int b, const ResampleSmem& s) {
   const ReqView& v = s.v;
+  if (P.mode == kSplitSample) {  // cosine_sample_residual: an error, or greedy (the row's argmax)
+    if (threadIdx.x == 0) {
+      P.out_token[b] = v.err ? -1 : (int32_t)s.pd[0].amax;
+      P.status[b] = v.err;
+    }
+    return;
+  }
   int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
   for (int j = threadIdx.x; j <= P.k; j += kThreads)
     out[j] = v.err ? -1 : ((j < v.L) ? s.pd[j].xstar : (j == v.L ? (int32_t)s.pd[v.L].amax : -1));
@@ -1075,8 +1330,9 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
   const int kind0 = d.kind;
   const int Nd = (v.L < v.g) ? P.N : 0;
   const bool need_q = (kind0 == kWResidual);
-  const TT* trow = (const TT*)P.target + ((int64_t)b * (P.k + 1) + v.L) * P.ld_t;
-  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + v.L) * P.N * P.ld_q;
+  const bool smode = P.mode == kSplitSample;  // cosine_sample_residual: request b's own row group
+  const TT* trow = (const TT*)P.target + (smode ? (int64_t)b : (int64_t)b * (P.k + 1) + v.L) * P.ld_t;
+  const TQ* drow = (const TQ*)P.draft + (smode ? (int64_t)b : (int64_t)b * P.k + v.L) * P.N * P.ld_q;
   const int64_t tile0 = (int64_t)part * P.tpc;
   const int ntiles = (int)min((int64_t)P.tpc, P.nseg - tile0);
 #pragma unroll 1
@@ -1166,6 +1422,14 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
     y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sb, min(P.ngroups, sb + kTileGroups),
                                           s.tc, Z, s.scan, s.wi, &s.found, &s.margin);
     margin = s.margin;
+  }
+  if (smode) {
+    if (tid == 0) {
+      P.out_token[b] = (int32_t)y;
+      P.status[b] = (deg ? COSINE_INFO_DEGENERATE_RESIDUAL : 0) | (margin < 1e-6f ? COSINE_INFO_NEAR_TIE : 0) |
+                    (y < 0 ? 0xff : 0);
+    }
+    return;
   }
   int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
   for (int j = tid; j <= P.k; j += kThreads) out[j] = (j < v.L) ? s.pd[j].xstar : (j == v.L ? (int32_t)y : -1);
