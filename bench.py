@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--lazy", action="store_true",
                     help="early-exit verification (cosine_verify_batch_lazy, SURVEY 8(f) NEXT-1)")
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl"],
+                    help="c5: in-kernel NVLink peer writes when available (auto) or NCCL all-gathers")
     ap.add_argument("--watchdog", type=float, default=0.0,
                     help="dump every thread's stack and exit after this many seconds (0 = off)")
     a = ap.parse_args()
@@ -572,11 +574,13 @@ def run_vocab(args, c, dev, world, rank, local):
     toks, rid = torch.cat(xs), torch.cat(rids)
     if world > 1:
         ctx = sharding.init_vocab_sharded(V, device=local, max_batch=B, max_draft_len=k, max_drafters=N,
-                                          target_dtype=dt, draft_dtype=dt, seed=args.seed)
+                                          target_dtype=dt, draft_dtype=dt, seed=args.seed,
+                                          exchange=1 if args.exchange == "nccl" else 0)
     else:
         ctx = cv.cosine_verify_init(V, device=local, max_batch=B, max_draft_len=k, max_drafters=N,
                                     target_dtype=dt, draft_dtype=dt, seed=args.seed)
     ver = cv.Verifier(V, max_batch=B, k=k, N=N, device=local, ctx=ctx)
+    exchange = cv.cosine_exchange_mode(ver.ctx)
     stream = torch.cuda.current_stream(dev)
     wm = WEIGHTS[args.weights]
 
@@ -627,7 +631,8 @@ def run_vocab(args, c, dev, world, rank, local):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": WORKLOADS["c5"], "weights": args.weights, "global_batch": B, "k": k,
                        "drafters": N, "vocab": V,
-                       "shard_columns": W, "parallelism": f"vocab-sharded x{world}", "mean_accept_len": acc,
+                       "shard_columns": W, "parallelism": f"vocab-sharded x{world}",
+                       "exchange": exchange, "mean_accept_len": acc,
                        "request_errors": errs,
                        "l2": f"inputs {alg_rank / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -96,6 +96,8 @@ typedef struct {
                            /* cosine_nccl_unique_id(), identical on every rank (the caller    */
                            /* broadcasts it); the context owns the NCCL communicator          */
   int32_t cluster_size;    /* 0 = automatic; else 1, 2, 4 or 8 CTAs per (request, position)  */
+  int32_t exchange;        /* sharded contexts: 0 = in-kernel peer writes when every rank can  */
+                           /* map the others' memory, else NCCL; 1 = NCCL all-gathers only    */
 } cosine_config_t;
 
 /* Optional per-unit diagnostics of cosine_verify_batch (any member may be NULL). */
@@ -127,9 +129,13 @@ const char* cosine_last_error(cosine_ctx_t ctx);
  * cosine_verify_batch collectively (same B, k, N, draft_tokens, draft_len, request_ids, step,
  * modes, temperature) with ITS columns of every row (ld >= the shard width; token ids stay
  * global); the outputs are identical on every rank and equal to the unsharded call on the full
- * rows up to flagged near-ties.  Three NCCL all-gathers on `stream`: per-(request, position)
- * row statistics and candidate gathers (~N^2 + 4N + 8 words), the local masses of the final
- * draw (B doubles), the owner's token (B x 16 bytes).  ARGMAX selection only;
+ * rows up to flagged near-ties.  Three exchanges: per-(request, position) row statistics and
+ * candidate gathers (~N^2 + 4N + 8 words), the local masses of the final draw (B doubles), the
+ * owner's token (B x 16 bytes).  With <= 8 ranks whose GPUs can map each other's memory (CUDA
+ * IPC over NVLink, set up collectively at init) the producing kernels write them straight into
+ * every rank's gather buffer and count them on per-rank arrival counters that the consuming
+ * kernels wait on (no collective launches; a wait gives up after ~5 s instead of hanging);
+ * otherwise three NCCL all-gathers on `stream`.  ARGMAX selection only;
  * cosine_fuse_drafts / cosine_sample_residual / cosine_verify_tree return COSINE_ERR_UNSUPPORTED
  * on a sharded context.
  *
@@ -152,6 +158,9 @@ cosine_status_t cosine_nccl_unique_id(void* out, int64_t capacity);
  *   of every rank's send buffer into every rank's gather buffer in rank order.
  *   target_logits[g] / draft[g]: rank g's column shard ([B][k+1][ld_t] / [B][k][N][ld_q], one ld
  *   for all ranks); accept_len[g] / out_tokens[g] / status[g]: rank g's (replicated) outputs.
+ *   exchange: 0 = device copies between the phases (the layout of the NCCL all-gathers);
+ *   1 = the in-kernel peer-memory exchange of multi-GPU calls (G <= 8), the peers being the
+ *   other contexts' gather blocks.
  *   Errors as cosine_verify_batch; a vgroup context passed to cosine_verify_batch returns
  *   COSINE_ERR_UNSUPPORTED.
  */
@@ -162,7 +171,7 @@ cosine_status_t cosine_verify_batch_vgroup(const cosine_ctx_t* ctxs, int32_t G, 
                                            const int32_t* draft_tokens, const int32_t* draft_len,
                                            const uint64_t* request_ids, uint32_t step,
                                            cosine_weight_mode_t weight_mode, int32_t* const* accept_len,
-                                           int32_t* const* out_tokens, int32_t* const* status);
+                                           int32_t* const* out_tokens, int32_t* const* status, int32_t exchange);
 
 /*
  * cosine_fuse_drafts — Eq. 4 token fusion only (Alg. 1 TokenFusion P:376-381).
@@ -347,6 +356,9 @@ cosine_status_t cosine_verify_tree_lazy(cosine_ctx_t ctx, cosine_stream_t stream
 
 /* Number of kernels the last successful call on ctx enqueued (for launch accounting). */
 int32_t cosine_last_launch_count(cosine_ctx_t ctx);
+/* How a sharded context exchanges: 0 unsharded, 1 NCCL all-gathers, 2 in-kernel writes into the
+ * peers' memory (CUDA IPC over NVLink), 3 a virtual group (cosine_verify_init_vgroup). */
+int32_t cosine_exchange_mode(cosine_ctx_t ctx);
 
 /* Live timing of the dominant kernel (the streaming statistics kernel of cosine_verify_batch):
  * when enabled, every verify call brackets it with CUDA events on the caller's stream.

@@ -21,6 +21,7 @@ from ._lib import (  # noqa: F401
     cosine_verify_tree,
     cosine_verify_init_vgroup,
     cosine_verify_batch_vgroup,
+    cosine_exchange_mode,
 )
 
 __all__ = [

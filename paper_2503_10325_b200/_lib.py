@@ -41,7 +41,7 @@ class cosine_config_t(ctypes.Structure):
         ("max_batch", _i32), ("max_draft_len", _i32), ("max_drafters", _i32), ("max_tree_nodes", _i32),
         ("target_dtype", ctypes.c_int), ("draft_dtype", ctypes.c_int), ("draft_kind", ctypes.c_int),
         ("seed", _u64), ("nranks", _i32), ("rank", _i32), ("nccl_unique_id", _P),
-        ("cluster_size", _i32),
+        ("cluster_size", _i32), ("exchange", _i32),
     ]
 
 
@@ -58,6 +58,8 @@ _lib.cosine_last_error.argtypes = [_P]
 _lib.cosine_last_error.restype = ctypes.c_char_p
 _lib.cosine_last_launch_count.argtypes = [_P]
 _lib.cosine_last_launch_count.restype = _i32
+_lib.cosine_exchange_mode.argtypes = [_P]
+_lib.cosine_exchange_mode.restype = _i32
 _lib.cosine_fuse_drafts.argtypes = [_P, _P, _i32, _i32, _i32, _P, _i64, _P, _P, _u32, _f32,
                                     ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _i64, _P]
 _lib.cosine_fuse_drafts.restype = ctypes.c_int
@@ -89,7 +91,7 @@ _lib.cosine_verify_init_vgroup.argtypes = [ctypes.POINTER(cosine_config_t), _i32
 _lib.cosine_verify_init_vgroup.restype = ctypes.c_int
 _lib.cosine_verify_batch_vgroup.argtypes = [ctypes.POINTER(_P), _i32, _P, _i32, _i32, _i32, ctypes.POINTER(_P), _i64,
                                             _f32, ctypes.POINTER(_P), _i64, _P, _P, _P, _u32, ctypes.c_int,
-                                            ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)]
+                                            ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P), _i32]
 _lib.cosine_verify_batch_vgroup.restype = ctypes.c_int
 _lib.cosine_nccl_unique_id.argtypes = [_P, _i64]
 _lib.cosine_nccl_unique_id.restype = ctypes.c_int
@@ -104,7 +106,7 @@ EXPORTED_SYMBOLS = ("cosine_verify_init", "cosine_verify_destroy", "cosine_last_
                     "cosine_verify_tree", "cosine_nccl_unique_id", "cosine_verify_batch_lazy",
                     "cosine_verify_tree_lazy", "cosine_fuse_step",
                     "cosine_route_update", "cosine_tree_select", "cosine_verify_init_vgroup",
-                    "cosine_verify_batch_vgroup")
+                    "cosine_verify_batch_vgroup", "cosine_exchange_mode")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -160,7 +162,7 @@ def cosine_verify_init(vocab_size: int, *, device: int = 0, max_batch: int, max_
                        draft_kind: int = DRAFT_PROBS, seed: int = 0, cluster_size: int = 0,
                        max_tree_nodes: int = 0, nranks: int = 1, rank: int = 0,
                        vocab_begin: int = 0, vocab_end: int | None = None,
-                       nccl_unique_id: bytes | None = None):
+                       nccl_unique_id: bytes | None = None, exchange: int = 0):
     """Create a context on `device`; returns a Context.  nranks > 1: vocabulary-sharded over
     nranks GPUs, this rank holding columns [vocab_begin, vocab_end) (collective init)."""
     vocab_end = vocab_size if vocab_end is None else vocab_end
@@ -173,7 +175,7 @@ def cosine_verify_init(vocab_size: int, *, device: int = 0, max_batch: int, max_
                           target_dtype=_DT[target_dtype], draft_dtype=_DT[draft_dtype],
                           draft_kind=draft_kind, seed=seed, nranks=nranks, rank=rank,
                           nccl_unique_id=ctypes.cast(uid, _P) if uid is not None else None,
-                          cluster_size=cluster_size)
+                          cluster_size=cluster_size, exchange=exchange)
     h = _P()
     _check(_lib.cosine_verify_init(ctypes.byref(cfg), ctypes.byref(h)), None)
     return Context(h, cfg)
@@ -198,9 +200,11 @@ def cosine_verify_init_vgroup(vocab_size: int, shards, *, device: int = 0, max_b
 
 
 def cosine_verify_batch_vgroup(ctxs, targets, drafts, draft_tokens, request_ids, accept_lens, out_tokens, statuses,
-                               *, temperature=1.0, draft_len=None, step=0, weight_mode=W_CONF, stream=None):
+                               *, temperature=1.0, draft_len=None, step=0, weight_mode=W_CONF, stream=None,
+                               peer_exchange=False):
     """The collective sharded call of a virtual group: targets[g] [B][k+1][ld_t] / drafts[g]
-    [B][k][N][ld_q] are rank g's column shards; outputs per rank."""
+    [B][k][N][ld_q] are rank g's column shards; outputs per rank.  peer_exchange: the in-kernel
+    peer-memory exchange of multi-GPU calls instead of copies between the phases."""
     G = len(ctxs)
     B, kp1, ld_t = targets[0].shape
     N, ld_q = drafts[0].shape[2], drafts[0].shape[3]
@@ -209,7 +213,7 @@ def cosine_verify_batch_vgroup(ctxs, targets, drafts, draft_tokens, request_ids,
     rc = _lib.cosine_verify_batch_vgroup(hs, G, _stream(stream, targets[0].device), B, kp1 - 1, N, arr(targets),
                                          ld_t, temperature, arr(drafts), ld_q, _ptr(draft_tokens), _ptr(draft_len),
                                          _ptr(request_ids), step, weight_mode, arr(accept_lens), arr(out_tokens),
-                                         arr(statuses))
+                                         arr(statuses), 1 if peer_exchange else 0)
     _check(rc, ctxs[0])
 
 
@@ -219,6 +223,13 @@ def cosine_verify_destroy(ctx) -> None:
 
 def cosine_last_launch_count(ctx) -> int:
     return int(_lib.cosine_last_launch_count(ctx))
+
+
+EXCHANGE_MODES = {0: "none", 1: "nccl all-gathers", 2: "in-kernel nvlink peer writes", 3: "virtual group"}
+
+
+def cosine_exchange_mode(ctx) -> str:
+    return EXCHANGE_MODES.get(int(_lib.cosine_exchange_mode(ctx)), "?")
 
 
 def cosine_profile_enable(ctx, enable: bool = True) -> None:

@@ -93,6 +93,14 @@ struct cosine_ctx_s {
   YRec* ysend = nullptr;
   YRec* yall = nullptr;
   bool vgroup = false;  // a cosine_verify_init_vgroup context (device copies instead of NCCL)
+  // in-kernel exchange over NVLink peer memory: this rank's gather block [rec_all | zall | yall |
+  // arrival counters] (one allocation, shared with the peers through CUDA IPC) and the peers'
+  // blocks mapped into this process; p2p = false -> the NCCL all-gathers
+  bool p2p = false;
+  char* xblock = nullptr;
+  size_t xrec = 0, xz = 0, xy = 0;  // byte offsets of zall, yall and the counters in a block
+  char* peer_block[kMaxPeers] = {};
+  unsigned long long arrivals[3] = {0, 0, 0};  // cumulative arrival targets (same on every rank)
 };
 
 static thread_local std::string g_init_error;
@@ -281,11 +289,13 @@ cudaError_t shard_phase_a(cosine_ctx_t ctx, cudaStream_t s, const SplitParams& S
 }
 // Phase B: decisions from the gathered records, local masses of the final draw.
 cudaError_t shard_phase_b(cudaStream_t s, const SplitParams& S, const KernelSet& ks, bool logits, const char** stage) {
+  // p2p: the consumers wait on the arrival counters (their own rank's producer arrives too), so
+  // they are launched as programmatic dependents: their launch latency hides under the producer
   ShardLaunch L(s);
   const int64_t units = (int64_t)S.B * (S.k + 1);
   *stage = "decide";
   cudaError_t e = L(logits ? shard_decide_kernel<true> : shard_decide_kernel<false>,
-                    (unsigned)((units + kWarps - 1) / kWarps), false, S);
+                    (unsigned)((units + kWarps - 1) / kWarps), S.p2p != 0, S);
   if (e == cudaSuccess) {
     *stage = "resample";
     e = L(ks.resample, (unsigned)(S.B * S.spr), true, S);
@@ -295,12 +305,12 @@ cudaError_t shard_phase_b(cudaStream_t s, const SplitParams& S, const KernelSet&
 cudaError_t shard_phase_c(cudaStream_t s, const SplitParams& S, const KernelSet& ks, const char** stage) {
   ShardLaunch L(s);
   *stage = "sample";
-  return L(ks.shard_sample, (unsigned)S.B, false, S);
+  return L(ks.shard_sample, (unsigned)S.B, S.p2p != 0, S);
 }
 cudaError_t shard_phase_d(cudaStream_t s, const SplitParams& S, const char** stage) {
   ShardLaunch L(s);
   *stage = "finish";
-  return L(shard_finish_kernel, (unsigned)((S.B + kThreads - 1) / kThreads), false, S);
+  return L(shard_finish_kernel, (unsigned)((S.B + kThreads - 1) / kThreads), S.p2p != 0, S);
 }
 size_t shard_x_bytes(const SplitParams& S, int x) {  // bytes one rank contributes to exchange x
   if (x == 1) return (size_t)S.B * (S.k + 1) * S.rec_words * 4;
@@ -323,6 +333,75 @@ cosine_status_t shard_fail(cosine_ctx_t ctx, cudaStream_t s, cudaError_t e, nccl
   return fail(ctx, COSINE_ERR_NCCL, std::string("sharded verify all-gather: ") + ncclGetErrorString(r));
 }
 
+// Collective (init): share this rank's gather block with the other ranks through CUDA IPC (the
+// handles travel by one NCCL all-gather) and map theirs.  Any failure leaves p2p off: the call
+// then uses the NCCL all-gathers.
+void p2p_attach(cosine_ctx_t ctx) {
+  const int G = ctx->cfg.nranks, rank = ctx->cfg.rank;
+  cudaIpcMemHandle_t mine;
+  bool ok = cudaIpcGetMemHandle(&mine, ctx->xblock) == cudaSuccess;
+  void* dev = nullptr;
+  std::vector<cudaIpcMemHandle_t> all(G);
+  cudaStream_t s = nullptr;
+  ok = ok && cudaMalloc(&dev, sizeof(cudaIpcMemHandle_t) * (G + 1)) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess;
+  // every rank takes part in the all-gather (a rank whose handle failed sends zeros)
+  if (dev) {
+    cudaMemcpy((char*)dev + sizeof(mine) * G, &mine, sizeof(mine), cudaMemcpyHostToDevice);
+    const ncclResult_t r = ncclAllGather((char*)dev + sizeof(mine) * G, dev, sizeof(mine), ncclUint8, ctx->comm, s);
+    ok = ok && r == ncclSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+    ok = ok && cudaMemcpy(all.data(), dev, sizeof(mine) * G, cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  for (int g = 0; g < G && ok; ++g) {
+    if (g == rank) {
+      ctx->peer_block[g] = ctx->xblock;
+      continue;
+    }
+    void* p = nullptr;
+    ok = cudaIpcOpenMemHandle(&p, all[g], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    ctx->peer_block[g] = (char*)p;
+  }
+  // every rank must agree: p2p only if it is on everywhere
+  int flag = ok ? 1 : 0;
+  if (dev) {
+    cudaMemcpy(dev, &flag, sizeof(int), cudaMemcpyHostToDevice);
+    if (ncclAllReduce(dev, dev, 1, ncclInt32, ncclMin, ctx->comm, s) == ncclSuccess && cudaStreamSynchronize(s) == cudaSuccess)
+      cudaMemcpy(&flag, dev, sizeof(int), cudaMemcpyDeviceToHost);
+    else
+      flag = 0;
+  }
+  if (s) cudaStreamDestroy(s);
+  if (dev) cudaFree(dev);
+  cudaGetLastError();
+  ctx->p2p = flag != 0;
+  if (!ctx->p2p)
+    for (int g = 0; g < G; ++g) {
+      if (ctx->peer_block[g] && ctx->peer_block[g] != ctx->xblock) cudaIpcCloseMemHandle(ctx->peer_block[g]);
+      ctx->peer_block[g] = nullptr;
+    }
+}
+
+// The peer pointers and arrival targets of one sharded call (p2p): rank r's records go to
+// [r][units][words] of every peer's block, its masses to [r][B], its tokens to [r][B].
+void p2p_params(cosine_ctx_t ctx, SplitParams& S) {
+  S.p2p = 1;
+  const int G = S.G, r = S.rank;
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  for (int g = 0; g < G; ++g) {
+    char* blk = ctx->peer_block[g];
+    S.rec_peer[g] = (uint32_t*)blk + (int64_t)r * units * S.rec_words;
+    S.z_peer[g] = (double*)(blk + ctx->xz) + (int64_t)r * S.B;
+    S.y_peer[g] = (YRec*)(blk + ctx->xy) + (int64_t)r * S.B;
+    S.cnt_peer[g] = (unsigned long long*)(blk + ctx->xrec);
+  }
+  S.cnt_own = (unsigned long long*)(ctx->xblock + ctx->xrec);
+  const unsigned long long pack_ctas = (unsigned long long)((units + kWarps - 1) / kWarps);
+  ctx->arrivals[0] += (unsigned long long)G * pack_ctas;
+  ctx->arrivals[1] += (unsigned long long)G * (unsigned long long)S.B;
+  ctx->arrivals[2] += (unsigned long long)G * (unsigned long long)S.B;
+  for (int x = 0; x < 3; ++x) S.tgt[x] = ctx->arrivals[x];
+}
+
 // One rank's collective call (NCCL): the four phases on `stream` with an all-gather after each
 // of the first three.  (Request slices whose exchanges ran on a second stream under the next
 // slice's statistics were measured slower on 2 B200s: 1 / 2 / 4 / 8 slices -> 1024 / 1046 / 1097 /
@@ -337,12 +416,13 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
   const char* stage = "stats";
   ncclResult_t r = ncclSuccess;
+  if (ctx->p2p) p2p_params(ctx, F);  // in-kernel exchange: no all-gathers
   cudaError_t e = shard_phase_a(ctx, stream, F, ks, &stage);
-  if (e == cudaSuccess) r = shard_allgather(ctx, stream, F, 1);
+  if (e == cudaSuccess && !F.p2p) r = shard_allgather(ctx, stream, F, 1);
   if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_b(stream, F, ks, logits, &stage);
-  if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, stream, F, 2);
+  if (e == cudaSuccess && r == ncclSuccess && !F.p2p) r = shard_allgather(ctx, stream, F, 2);
   if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_c(stream, F, ks, &stage);
-  if (e == cudaSuccess && r == ncclSuccess) r = shard_allgather(ctx, stream, F, 3);
+  if (e == cudaSuccess && r == ncclSuccess && !F.p2p) r = shard_allgather(ctx, stream, F, 3);
   if (e == cudaSuccess && r == ncclSuccess) e = shard_phase_d(stream, F, &stage);
   if (e != cudaSuccess || r != ncclSuccess) return shard_fail(ctx, stream, e, r, stage);
   ctx->last_launches = 6;
@@ -354,7 +434,7 @@ cosine_status_t launch_shard(cosine_ctx_t ctx, cudaStream_t stream, SplitParams&
 // phase over all ranks, each exchange done by device copies into every rank's gather buffer in
 // rank order — the same kernels, slices and record layouts as launch_shard.
 cosine_status_t launch_shard_vgroup(const cosine_ctx_t* ctxs, int G, cudaStream_t stream, SplitParams* F,
-                                    cosine_dtype_t tt, cosine_dtype_t tq, bool logits) {
+                                    cosine_dtype_t tt, cosine_dtype_t tq, bool logits, bool p2p) {
   KernelSet ks;
   kernel_set(tt, tq, logits, F[0].N, &ks);
   for (int g = 0; g < G; ++g) {
@@ -364,7 +444,14 @@ cosine_status_t launch_shard_vgroup(const cosine_ctx_t* ctxs, int G, cudaStream_
   }
   const char* stage = "stats";
   cudaError_t e = cudaSuccess;
+  if (p2p) {  // the in-kernel exchange, peers = the other contexts' blocks on this device
+    for (int g = 0; g < G; ++g) {
+      for (int h = 0; h < G; ++h) ctxs[g]->peer_block[h] = ctxs[h]->xblock;
+      p2p_params(ctxs[g], F[g]);
+    }
+  }
   auto exchange = [&](int x) {
+    if (p2p) return;
     for (int g = 0; g < G && e == cudaSuccess; ++g) {
       const size_t n = shard_x_bytes(F[g], x);
       const void* src = x == 1 ? (const void*)F[g].rec_send
@@ -513,6 +600,8 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "an unsharded context covers [0, vocab_size)");
   if (cfg->nranks > 1 && !cfg->nccl_unique_id && !vgroup)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "nranks > 1 needs nccl_unique_id (cosine_nccl_unique_id on rank 0)");
+  if (cfg->exchange != 0 && cfg->exchange != 1)
+    return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "exchange must be 0 (automatic) or 1 (NCCL)");
   if (cfg->cluster_size != 0 && cfg->cluster_size != 1 && cfg->cluster_size != 2 &&
       cfg->cluster_size != 4 && cfg->cluster_size != 8 && cfg->cluster_size != 16)
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "cluster_size must be 0, 1, 2, 4, 8 or 16");
@@ -543,12 +632,21 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
   if (e == cudaSuccess && cfg->nranks > 1) {  // vocabulary-sharded: exchange buffers + communicator
     const size_t units = nb * (size_t)(cfg->max_draft_len + 1);
     const size_t rb = units * (size_t)shard_rec_words(cfg->max_drafters) * 4;
+    const size_t G = (size_t)cfg->nranks;
     e = cudaMalloc(&ctx->rec_send, rb);
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->rec_all, rb * (size_t)cfg->nranks);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->zsend, nb * sizeof(double));
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->zall, nb * sizeof(double) * (size_t)cfg->nranks);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->ysend, nb * sizeof(YRec));
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->yall, nb * sizeof(YRec) * (size_t)cfg->nranks);
+    // the gather buffers and the arrival counters in one block (the unit of IPC sharing)
+    ctx->xz = (rb * G + 255) / 256 * 256;
+    ctx->xy = ctx->xz + (nb * sizeof(double) * G + 255) / 256 * 256;
+    ctx->xrec = ctx->xy + (nb * sizeof(YRec) * G + 255) / 256 * 256;  // (counters)
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->xblock, ctx->xrec + 256);
+    if (e == cudaSuccess) e = cudaMemset(ctx->xblock + ctx->xrec, 0, 256);
+    if (e == cudaSuccess) {
+      ctx->rec_all = (uint32_t*)ctx->xblock;
+      ctx->zall = (double*)(ctx->xblock + ctx->xz);
+      ctx->yall = (YRec*)(ctx->xblock + ctx->xy);
+    }
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ncclResult_t nr = ncclSuccess;
@@ -557,16 +655,15 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
     memcpy(&uid, cfg->nccl_unique_id, sizeof(uid));
     nr = ncclCommInitRank(&ctx->comm, cfg->nranks, uid, cfg->rank);
     if (nr != ncclSuccess) ctx->comm = nullptr;
+    if (nr == ncclSuccess && cfg->nranks <= kMaxPeers && cfg->exchange == 0) p2p_attach(ctx);
   }
   if (e != cudaSuccess || nr != ncclSuccess) {
     std::string msg = (e != cudaSuccess) ? std::string("init: ") + cudaGetErrorString(e)
                                          : std::string("init: ncclCommInitRank: ") + ncclGetErrorString(nr);
     cudaFree(ctx->rec_send);
-    cudaFree(ctx->rec_all);
     cudaFree(ctx->zsend);
-    cudaFree(ctx->zall);
     cudaFree(ctx->ysend);
-    cudaFree(ctx->yall);
+    cudaFree(ctx->xblock);
     cudaFree(ctx->lz);
     cudaGetLastError();
     cudaFree(ctx->parts);
@@ -623,12 +720,12 @@ cosine_status_t cosine_verify_destroy(cosine_ctx_t ctx) {
   cudaFree(ctx->segsum);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   cudaFree(ctx->lz);
+  for (int g = 0; g < kMaxPeers; ++g)
+    if (ctx->peer_block[g] && ctx->peer_block[g] != ctx->xblock && !ctx->vgroup) cudaIpcCloseMemHandle(ctx->peer_block[g]);
   cudaFree(ctx->rec_send);
-  cudaFree(ctx->rec_all);
   cudaFree(ctx->zsend);
-  cudaFree(ctx->zall);
   cudaFree(ctx->ysend);
-  cudaFree(ctx->yall);
+  cudaFree(ctx->xblock);
   for (auto& pe : ctx->prof_ev) {
     cudaEventDestroy(pe.first);
     cudaEventDestroy(pe.second);
@@ -652,6 +749,11 @@ const char* cosine_last_error(cosine_ctx_t ctx) {
 }
 
 int32_t cosine_last_launch_count(cosine_ctx_t ctx) { return ctx ? ctx->last_launches : 0; }
+
+int32_t cosine_exchange_mode(cosine_ctx_t ctx) {
+  if (!ctx || ctx->cfg.nranks == 1) return 0;
+  return ctx->vgroup ? 3 : (ctx->p2p ? 2 : 1);
+}
 
 cosine_status_t cosine_profile_enable(cosine_ctx_t ctx, int32_t enable) {
   if (!ctx) return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "NULL context");
@@ -833,8 +935,9 @@ cosine_status_t cosine_verify_batch_vgroup(const cosine_ctx_t* ctxs, int32_t G, 
                                            const int32_t* draft_tokens, const int32_t* draft_len,
                                            const uint64_t* request_ids, uint32_t step,
                                            cosine_weight_mode_t weight_mode, int32_t* const* accept_len,
-                                           int32_t* const* out_tokens, int32_t* const* status) {
-  if (!ctxs || G < 2 || !target_logits || !draft || !accept_len || !out_tokens || !status)
+                                           int32_t* const* out_tokens, int32_t* const* status, int32_t exchange) {
+  if (!ctxs || G < 2 || !target_logits || !draft || !accept_len || !out_tokens || !status || exchange < 0 ||
+      exchange > 1 || (exchange == 1 && G > kMaxPeers))
     return fail(nullptr, COSINE_ERR_INVALID_ARGUMENT, "vgroup: NULL argument or G < 2");
   for (int g = 0; g < G; ++g) {
     if (!ctxs[g] || !ctxs[g]->vgroup || ctxs[g]->cfg.nranks != G || ctxs[g]->cfg.rank != g)
@@ -855,7 +958,7 @@ cosine_status_t cosine_verify_batch_vgroup(const cosine_ctx_t* ctxs, int32_t G, 
                       request_ids, step, weight_mode, accept_len[g], out_tokens[g], status[g], nullptr);
   const cosine_config_t& c = ctxs[0]->cfg;
   return launch_shard_vgroup(ctxs, G, (cudaStream_t)stream, S.data(), c.target_dtype, c.draft_dtype,
-                             c.draft_kind == COSINE_DRAFT_LOGITS);
+                             c.draft_kind == COSINE_DRAFT_LOGITS, exchange == 1);
 }
 
 cosine_status_t cosine_verify_batch_lazy(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,

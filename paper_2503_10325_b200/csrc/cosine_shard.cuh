@@ -39,16 +39,42 @@ struct RecOff {
       : sig(8), dmax(8 + 2 * N), tx(8 + 3 * N), dx(8 + 4 * N) {}
 };
 
+constexpr int kMaxPeers = 8;  // ranks of an in-kernel (NVLink peer memory) exchange
+
+// One thread: wait until this rank's arrival counter x reaches the call's target (every rank's
+// contribution to exchange x is in this rank's gather buffer).  Gives up after ~5 s (a rank that
+// never arrives must not hang the GPU: the outputs are then wrong, not stuck).
+__device__ __forceinline__ void p2p_wait(const SplitParams& P, int x) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long n;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(n) : "l"(P.cnt_own + x) : "memory");
+    if (n >= P.tgt[x]) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 5000000000ull) break;
+    __nanosleep(64);
+  }
+}
+// One thread: this thread's writes into the peers' buffers before one arrival on each of them.
+__device__ __forceinline__ void p2p_arrive(const SplitParams& P, int x) {
+  __threadfence_system();
+  for (int g = 0; g < P.G; ++g) atomicAdd_system(P.cnt_peer[g] + x, 1ull);
+}
+__device__ __forceinline__ void shard_put_y(const SplitParams& P, int b, const YRec& y) {
+  if (!P.p2p) {
+    P.ysend[b] = y;
+    return;
+  }
+  for (int g = 0; g < P.G; ++g) P.y_peer[g][b] = y;
+  p2p_arrive(P, 2);
+}
+
 // ---------------- 1. the local record of a unit (one warp per unit) ----------------
 template <typename TT, typename TQ, bool kLogits>
-__global__ void __launch_bounds__(kThreads) shard_pack_kernel(const SplitParams P) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // stats_kernel's partial records (PDL)
-  if (unit >= (int64_t)P.B * (P.k + 1)) return;
-  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
-  const int g = P.draft_len ? P.draft_len[b] : P.k;
-  if (g < 1 || g > P.k || i > g) return;
+__device__ __forceinline__ void shard_pack_unit(const SplitParams& P, int64_t unit, int b, int i, int g) {
+  const int lane = threadIdx.x & 31;
   const bool has_d = i < g;
   const int N = P.N, C = P.C;
   const double k2 = (double)P.k2f;
@@ -117,6 +143,28 @@ __global__ void __launch_bounds__(kThreads) shard_pack_kernel(const SplitParams 
     if (!has_d)
       for (int n = 0; n < N; ++n) recf[ro.tx + n] = 0.f;
   }
+  if (P.p2p) {  // the record into every rank's gather buffer (rank-major, as the all-gather's)
+    __syncwarp();
+    for (int gg = 0; gg < P.G; ++gg) {
+      uint32_t* dst = P.rec_peer[gg] + unit * P.rec_words;
+      for (int w = lane; w < P.rec_words; w += 32) dst[w] = rec[w];
+    }
+  }
+}
+
+template <typename TT, typename TQ, bool kLogits>
+__global__ void __launch_bounds__(kThreads) shard_pack_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // stats_kernel's partial records (PDL)
+  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  const bool valid = unit < (int64_t)P.B * (P.k + 1);
+  const int g = valid ? (P.draft_len ? P.draft_len[b] : P.k) : 0;
+  if (valid && g >= 1 && g <= P.k && i <= g) shard_pack_unit<TT, TQ, kLogits>(P, unit, b, i, g);
+  if (P.p2p) {  // every rank's copy of this CTA's records, then one arrival per CTA on every rank
+    __syncthreads();
+    if (threadIdx.x == 0) p2p_arrive(P, 0);
+  }
 }
 
 // ---------------- 2. global decisions from the G records (one warp per unit) ----------------
@@ -126,6 +174,10 @@ __global__ void __launch_bounds__(kThreads) shard_decide_kernel(const SplitParam
   const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
   __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
   __shared__ int32_t s_tok[kWarps][kMaxN];
+  if (P.p2p) {  // every rank's records have arrived
+    if (tid == 0) p2p_wait(P, 0);
+    __syncthreads();
+  }
   const int64_t units = (int64_t)P.B * (P.k + 1);
   if (unit >= units) return;
   const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
@@ -230,9 +282,13 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
   yr.margin = INFINITY;
   yr.deg = 0;
   yr.z = 0.f;
+  if (P.p2p) {  // every rank's local masses have arrived
+    if (tid == 0) p2p_wait(P, 1);
+    __syncthreads();
+  }
   const int g = P.draft_len ? P.draft_len[b] : P.k;
   if (g < 1 || g > P.k) {
-    if (tid == 0) P.ysend[b] = yr;
+    if (tid == 0) shard_put_y(P, b, yr);
     return;
   }
   {
@@ -250,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
   __syncthreads();
   const ReqView v = s_v;
   if (!v.sample) {
-    if (tid == 0) P.ysend[b] = yr;
+    if (tid == 0) shard_put_y(P, b, yr);
     return;
   }
   const Decision d = s_d;
@@ -334,10 +390,11 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
       yr.margin = (y >= 0) ? s_margin : 0.f;
     }
   }
+  __syncthreads();  // (p2p: every read of this rank's gather buffers precedes the last arrival)
   if (tid == 0) {
     yr.deg = s_deg;
     yr.z = (float)s_Z;
-    P.ysend[b] = yr;
+    shard_put_y(P, b, yr);
   }
 }
 
@@ -345,6 +402,10 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
 
 // ---------------- 5. the replicated outputs (one thread per request) ----------------
 __global__ void __launch_bounds__(kThreads) shard_finish_kernel(const SplitParams P) {
+  if (P.p2p) {  // every rank's token has arrived
+    if (threadIdx.x == 0) p2p_wait(P, 2);
+    __syncthreads();
+  }
   const int b = blockIdx.x * kThreads + threadIdx.x;
   if (b >= P.B) return;
   const int g = P.draft_len ? P.draft_len[b] : P.k;

@@ -105,6 +105,18 @@ struct SplitParams {
   const double* zall;        // [G][B]
   struct YRec* ysend;        // [B] the owner's token (-1 elsewhere)
   const struct YRec* yall;   // [G][B]
+  // in-kernel exchange over NVLink peer memory (p2p = 1, replaces the three NCCL all-gathers):
+  // the kernel that produces a record / mass / token writes it straight into every rank's
+  // gather buffer (peer pointers of this call, rank-major layout as the all-gather's) and counts
+  // it on every rank's arrival counter [3] (rec, z, y); the consumer waits until its own counter
+  // reaches the call's cumulative target tgt[x]
+  int p2p;
+  uint32_t* rec_peer[8];
+  double* z_peer[8];
+  struct YRec* y_peer[8];
+  unsigned long long* cnt_peer[8];
+  unsigned long long* cnt_own;
+  unsigned long long tgt[3];
 };
 
 
@@ -1253,6 +1265,19 @@ __device__ __forceinline__ double warp_tile_crossing(const double* seg, int64_t 
   return Z;
 }
 
+// The local mass of request b's final draw in vocabulary-sharded mode: into this rank's send
+// slot (NCCL all-gather) or straight into every rank's gather buffer + one arrival on each
+// (p2p; cosine_shard.cuh).  One thread.
+__device__ __forceinline__ void shard_z_out(const SplitParams& P, int b, double z) {
+  if (!P.p2p) {
+    P.zsend[b] = z;
+    return;
+  }
+  for (int g = 0; g < P.G; ++g) P.z_peer[g][b] = z;
+  __threadfence_system();
+  for (int g = 0; g < P.G; ++g) atomicAdd_system(P.cnt_peer[g] + 1, 1ull);
+}
+
 // The final draw of a request, split in parts of kSegTilesPerCta 2048-entry tiles:
 //  1. the request's position decisions give the first rejection L (request_view);
 //  2. each part streams its tiles of the (1+N) rows at L (or the bonus row) — same group
@@ -1381,7 +1406,7 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
     if (lane == 0) {
       P.counters[b] = 0;  // ready for the next call
       if (P.shard) {      // vocabulary-sharded: this rank's mass; shard_sample_kernel goes on
-        P.zsend[b] = Z;
+        shard_z_out(P, b, Z);
       } else {
         int kind = kind0, dg = 0;
         if (!(Z > 0.0) && (kind == kWResidual || kind == kWPoint)) {
@@ -1470,7 +1495,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
   }
   if (g < 1 || g > P.k) {
     if (part == 0 && threadIdx.x == 0) {
-      if (P.shard) P.zsend[b] = 0.0;  // the outputs come from shard_finish_kernel
+      if (P.shard) shard_z_out(P, b, 0.0);  // the outputs come from shard_finish_kernel
       else write_bad_len(P, b);
     }
     return;
@@ -1485,7 +1510,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     }
     if (part == 0) {
       if (P.shard) {
-        if (threadIdx.x == 0) P.zsend[b] = 0.0;
+        if (threadIdx.x == 0) shard_z_out(P, b, 0.0);
       } else {
         write_plain_outputs(P, b, s);
       }

@@ -21,7 +21,7 @@ import shard_check  # noqa: E402  (the case list and the column-shard helper)
 pytestmark = pytest.mark.gpu
 
 
-def _vgroup_verify(inp, shards, *, T=1.0, wm=0, draft_kind="probs", seed=7, dev=None):
+def _vgroup_verify(inp, shards, *, T=1.0, wm=0, draft_kind="probs", seed=7, dev=None, peer=False):
     """Run the virtual group over the column shards of `inp`; returns one output dict per rank."""
     import paper_2503_10325_b200 as cv
     dev = dev or torch.device("cuda", 0)
@@ -31,6 +31,7 @@ def _vgroup_verify(inp, shards, *, T=1.0, wm=0, draft_kind="probs", seed=7, dev=
     dk = cv.DRAFT_LOGITS if draft_kind == "logits" else cv.DRAFT_PROBS
     ctxs = cv.cosine_verify_init_vgroup(V, shards, max_batch=B, max_draft_len=k, max_drafters=N, target_dtype=dt,
                                         draft_dtype=qt, draft_kind=dk, seed=seed)
+    reps = 2 if peer else 1  # (peer: a second call checks that the arrival targets advance)
     width = max(e - b for b, e in shards)
     ld = (width + 7) // 8 * 8
     tg, dr = [], []
@@ -46,8 +47,9 @@ def _vgroup_verify(inp, shards, *, T=1.0, wm=0, draft_kind="probs", seed=7, dev=
     ot = [torch.empty(B, kp1, dtype=torch.int32, device=dev) for _ in range(G)]
     st = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(G)]
     dl = inp["draft_len"].to(dev) if inp["draft_len"] is not None else None
-    cv.cosine_verify_batch_vgroup(ctxs, tg, dr, inp["draft_tokens"].to(dev), inp["request_ids"].to(dev), al, ot, st,
-                                  temperature=T, draft_len=dl, weight_mode=wm)
+    for _ in range(reps):
+        cv.cosine_verify_batch_vgroup(ctxs, tg, dr, inp["draft_tokens"].to(dev), inp["request_ids"].to(dev), al, ot,
+                                      st, temperature=T, draft_len=dl, weight_mode=wm, peer_exchange=peer)
     torch.cuda.synchronize()
     launches = cv.cosine_last_launch_count(ctxs[0])
     for c in ctxs:
@@ -70,9 +72,10 @@ def _check(name, inp, outs, *, T=1.0, wm=0, draft_kind="probs", oracle_slices=No
     assert not (diff & ~flagged).any(), f"{name}: sharded != unsharded at {np.nonzero(diff & ~flagged)[0][:5]}"
 
 
+@pytest.mark.parametrize("peer", [False, True], ids=["copies", "peer"])
 @pytest.mark.parametrize("G", [2, 3, 4])
 @pytest.mark.parametrize("case", shard_check.CASES, ids=[c[0] for c in shard_check.CASES])
-def test_vgroup_cases(cuda_ok, case, G):
+def test_vgroup_cases(cuda_ok, case, G, peer):
     name, B, k, N, V, dtype, kw = case
     inp = shard_check.make_inputs(B, k, N, V, dtype, kw, 1000 + sum(map(ord, name)))
     if kw.get("split") == "odd":
@@ -81,11 +84,12 @@ def test_vgroup_cases(cuda_ok, case, G):
     else:
         shards = [vocab_shard(V, G, r) for r in range(G)]
     T, wm, dk = kw.get("T", 1.0), kw.get("wm", 0), kw.get("draft_kind", "probs")
-    outs = _vgroup_verify(inp, shards, T=T, wm=wm, draft_kind=dk)
-    _check(f"vgroup {name} G={G}", inp, outs, T=T, wm=wm, draft_kind=dk)
+    outs = _vgroup_verify(inp, shards, T=T, wm=wm, draft_kind=dk, peer=peer)
+    _check(f"vgroup {name} G={G}{' peer' if peer else ''}", inp, outs, T=T, wm=wm, draft_kind=dk)
 
 
-def test_vgroup_c5_full_size(cuda_ok):
+@pytest.mark.parametrize("peer", [False, True], ids=["copies", "peer"])
+def test_vgroup_c5_full_size(cuda_ok, peer):
     # BASELINE config c5: B = 1024, k = 8, N = 4, V = 128256 split over G = 8 shards of 16032
     # columns — the sharded kernels at their real shape (9216 units per record exchange), every
     # request checked against the oracle and the unsharded call.
@@ -100,6 +104,6 @@ def test_vgroup_c5_full_size(cuda_ok):
     del parts
     shards = [vocab_shard(V, G, r) for r in range(G)]
     assert all(e - b == 16032 for b, e in shards)
-    outs = _vgroup_verify(inp, shards)
+    outs = _vgroup_verify(inp, shards, peer=peer)
     assert outs[0]["launches"] == 6
-    _check("vgroup c5 G=8", inp, outs)
+    _check(f"vgroup c5 G=8{' peer' if peer else ''}", inp, outs)

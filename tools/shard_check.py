@@ -101,13 +101,15 @@ def run_case(name, B, k, N, V, dtype, kw, world, rank, dev):
              status=s.cpu().numpy().copy(), launches=cv.cosine_last_launch_count(ver.ctx))
     for n, t in ver.debug.items():
         g[n] = t[:B].cpu().numpy().copy()
+    exchange = cv.cosine_exchange_mode(ctx)
     ver.close()
     # every rank must hold the same outputs
     mine = torch.tensor(np.concatenate([g["accept_len"], g["out_tokens"].ravel(), g["status"]]), dtype=torch.int64)
     allv = [torch.zeros_like(mine) for _ in range(world)]
     dist.all_gather(allv, mine)
     replicated = all(bool((x == allv[0]).all()) for x in allv)
-    res = dict(case=name, shard=[b, e], replicated=replicated, launches=g["launches"])
+    res = dict(case=name, shard=[b, e], replicated=replicated, launches=g["launches"],
+               exchange=exchange)
     if rank != 0:
         return res
     import parity
