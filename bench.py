@@ -174,21 +174,22 @@ def cpu_threads(args):
 
 # --------------------------------------------------------------------------------------
 def cpu_oracle_rate(host_inputs, k, V, budget_s, seed, threads, wm=0, sm=0):
-    """The CPU oracle as it stands, on `threads` host threads (one request slice each, GIL
-    released in the C code), on rounds of `threads` whole requests of the workload until
-    ~budget_s seconds; returns (tokens/s, requests, seconds)."""
+    """The CPU oracle as it stands, on `threads` host threads (one request per thread at a time,
+    GIL released in the C code), over rounds of `threads` whole requests of the workload — the
+    sample cycled — until ~budget_s seconds; returns (tokens/s, requests, seconds)."""
     import oracle
     B = host_inputs["target"].shape[0]
-    done_req, spent = 0, 0.0
-    while spent < budget_s and done_req < B:
-        b0, b1 = done_req, min(B, done_req + threads)
+    done_req, spent, b0 = 0, 0.0, 0
+    while spent < budget_s:
+        b1 = min(B, b0 + threads)
         t0 = time.perf_counter()
         oracle.verify_batch_parallel(host_inputs["target"][b0:b1], host_inputs["draft"][b0:b1],
                                      host_inputs["draft_tokens"][b0:b1], host_inputs["request_ids"][b0:b1],
                                      threads=threads, temperature=1.0, seed=seed, vocab=V, weight_mode=wm,
                                      select_mode=sm)
         spent += time.perf_counter() - t0
-        done_req = b1
+        done_req += b1 - b0
+        b0 = 0 if b1 >= B else b1
     return done_req * k / spent, done_req, spent
 
 
@@ -404,10 +405,11 @@ def run_ours(args):
         threads = cpu_threads(args)
         host_inp = {n: inp[n][: min(B, 4 * threads)].cpu() for n in ("target", "draft", "draft_tokens", "request_ids")}
         rate, nreq, spent = cpu_oracle_rate(host_inp, k, V, args.cpu_seconds, args.seed, threads, wm, sm)
-        rate1, nreq1, spent1 = cpu_oracle_rate(host_inp, k, V, args.cpu_seconds / 4, args.seed, 1, wm, sm)
+        rate1, nreq1, spent1 = cpu_oracle_rate(host_inp, k, V, args.cpu_seconds / 3, args.seed, 1, wm, sm)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"{nreq} requests of {args.config} ({nreq * k} verified tokens), fp64 C oracle, "
-                         f"{threads} threads (one request slice each), {spent:.1f} s",
+               "sample": f"{nreq} requests of {args.config} ({nreq * k} verified tokens; the first "
+                         f"{host_inp['target'].shape[0]} of the batch, cycled), fp64 C oracle, {threads} threads "
+                         f"(one request per thread at a time), {spent:.1f} s",
                "single_thread": {"value": rate1, "cores": 1, "sample": f"{nreq1} requests, {spent1:.1f} s"}}
     ver.close()
     del inp
