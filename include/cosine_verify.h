@@ -202,6 +202,10 @@ cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int
  * Outputs: accept_len [B] = L_b (-1 on a per-request error); out_tokens [B][k+1] = x*_0 ..
  *   x*_{L-1}, y, then -1; status [B].  debug may be NULL.
  * Rows after gamma_b are never read.  All rows 0..gamma_b are read and validated.
+ * One GPU: three launches on `stream` — the row statistics (every input byte read once), the
+ * decisions (ARGMAX: a warp per position; SAMPLE: a CTA per position that draws x* ~ q from the
+ * crossing chunk found in the statistics' chunk records, reading #26) and the final draws (the
+ * rows at L re-read once) — the latter two as programmatic dependents waiting on device counters.
  */
 cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
                                     int32_t N, const void* target_logits, int64_t ld_t,

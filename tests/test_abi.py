@@ -58,6 +58,19 @@ def test_null_and_invalid_arguments_return_status_codes():
     assert b"vocabulary" in L.cosine_last_error(None)
     cfg.vocab_size, cfg.vocab_end, cfg.max_drafters = 100, 100, 9
     assert L.cosine_verify_init(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    cfg.max_drafters, cfg.exchange = 1, 7  # exchange must be 0 (automatic) or 1 (NCCL)
+    assert L.cosine_verify_init(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    assert b"exchange" in L.cosine_last_error(None)
+    # virtual groups: G >= 2, cfgs[g] must be rank g of G with tiling shards
+    cfg.exchange = 0
+    cfgs = (_lib.cosine_config_t * 2)(cfg, cfg)
+    hs = (ctypes.c_void_p * 2)()
+    assert L.cosine_verify_init_vgroup(cfgs, 1, hs) == 1
+    assert L.cosine_verify_init_vgroup(cfgs, 2, hs) == 1  # nranks / rank / shards not set
+    assert b"vgroup" in L.cosine_last_error(None)
+    assert L.cosine_verify_batch_vgroup(None, 2, None, 1, 1, 1, None, 8, 1.0, None, 8, None, None, None, 0, 0,
+                                        None, None, None, 0) == 1
+    assert L.cosine_exchange_mode(None) == 0
 
 
 def test_init_without_gpu_fails_cleanly():
