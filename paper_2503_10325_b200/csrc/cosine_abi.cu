@@ -75,6 +75,8 @@ struct cosine_ctx_s {
   ChildPQ* cpq = nullptr;
   double* segsum = nullptr;
   size_t segsum_cap = 0;
+  float* slices = nullptr;  // SAMPLE selection: 64-group slice sums of the drafter rows
+  size_t slices_cap = 0;    // floats
   // optional live timing of the dominant kernel (stats_kernel) with CUDA events on the stream
   int prof_on = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
@@ -180,6 +182,13 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
   if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
   S.fused = 1;
+  // SAMPLE over probability drafts: the statistics pass keeps 64-group slice sums and the draw
+  // runs a warp per unit (sample_decide_w_kernel); otherwise a CTA per unit scans the chunk
+  S.nsl = (S.cg + kSliceGroups - 1) / kSliceGroups;
+  const bool sliced = sample && !S.greedy && ks.stats_slices && ctx->slices && !S.lazy && !S.tree &&
+                      (size_t)units * S.C * S.nsl * S.N <= ctx->slices_cap;
+  S.slices = sliced ? ctx->slices : nullptr;
+  const bool warp_b1 = !sample || sliced;
   cudaLaunchConfig_t lc;
   memset(&lc, 0, sizeof(lc));
   lc.blockDim = dim3(kThreads, 1, 1);
@@ -190,14 +199,15 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
   const auto pe = prof_events(ctx);
   if (pe.first) cudaEventRecord(pe.first, stream);
   lc.gridDim = dim3((unsigned)(units * S.C), 1, 1);
-  cudaError_t e = cudaLaunchKernelEx(&lc, ks.stats, S);
+  cudaError_t e = cudaLaunchKernelEx(&lc, sliced ? ks.stats_slices : ks.stats, S);
   if (pe.second) cudaEventRecord(pe.second, stream);
   if (e == cudaSuccess) {
-    // ARGMAX: a warp per unit; SAMPLE: a CTA per unit (the draw scans one chunk block-wide)
-    lc.gridDim = dim3((unsigned)(sample ? units : (units + kWarps - 1) / kWarps), 1, 1);
+    // ARGMAX and sliced SAMPLE: a warp per unit; SAMPLE otherwise: a CTA per unit (the draw
+    // scans one chunk block-wide)
+    lc.gridDim = dim3((unsigned)(warp_b1 ? (units + kWarps - 1) / kWarps : units), 1, 1);
     lc.attrs = pe.second ? nullptr : at;  // (an event record between the two breaks PDL)
     lc.numAttrs = pe.second ? 0 : 1;
-    e = cudaLaunchKernelEx(&lc, sample ? ks.sample_decide : ks.decide, S);
+    e = cudaLaunchKernelEx(&lc, !sample ? ks.decide : (sliced ? ks.sample_decide_w : ks.sample_decide), S);
   }
   if (e == cudaSuccess) {
     lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
@@ -629,6 +639,14 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
   if (e == cudaSuccess) e = cudaMemset(ctx->counters, 0, ncnt * sizeof(int32_t));
   ctx->segsum_cap = nb * (size_t)((ctx->V + (int64_t)kTileElems - 1) / kTileElems);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->segsum, ctx->segsum_cap * sizeof(double));
+  if (e == cudaSuccess && cfg->nranks == 1 && cfg->draft_kind == COSINE_DRAFT_PROBS) {
+    // slice sums for SAMPLE selection: per unit and drafter <= ceil(groups / kSliceGroups) +
+    // kMaxC floats (chunks round up), i.e. ~1/256 of a bf16 drafter row
+    const size_t units = nb * (size_t)(cfg->max_draft_len + 1);
+    const size_t per = (size_t)((ctx->V + kGroup * kSliceGroups - 1) / (kGroup * kSliceGroups)) + kMaxC;
+    ctx->slices_cap = units * per * (size_t)cfg->max_drafters;
+    e = cudaMalloc(&ctx->slices, ctx->slices_cap * sizeof(float));
+  }
   if (e == cudaSuccess && cfg->nranks > 1) {  // vocabulary-sharded: exchange buffers + communicator
     const size_t units = nb * (size_t)(cfg->max_draft_len + 1);
     const size_t rb = units * (size_t)shard_rec_words(cfg->max_drafters) * 4;
@@ -672,6 +690,8 @@ static cosine_status_t init_impl(const cosine_config_t* cfg, cosine_ctx_t* out, 
     cudaFree(ctx->ndec);
     cudaFree(ctx->cpq);
     cudaFree(ctx->segsum);
+  cudaFree(ctx->slices);
+    cudaFree(ctx->slices);
     delete ctx;
     if (e == cudaSuccess) return fail(nullptr, COSINE_ERR_NCCL, msg);
     return fail(nullptr, e == cudaErrorMemoryAllocation ? COSINE_ERR_OUT_OF_MEMORY : COSINE_ERR_CUDA, msg);

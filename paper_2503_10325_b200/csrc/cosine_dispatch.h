@@ -16,6 +16,8 @@ struct KernelSet {
   SplitFn lazy_decide;   // lazy round decisions (NEXT-1)
   SplitFn decide;        // split path decisions (stats -> decide -> resample)
   SplitFn sample_decide; // the same with SAMPLE selection (x* ~ fused q)
+  SplitFn stats_slices;  // SAMPLE over probability drafts: stats_kernel + 64-group slice sums
+  SplitFn sample_decide_w;  // ... and its warp-per-unit draw from the slices (nullptr: logits)
   SplitFn fuse_decide;   // cosine_fuse_drafts: Eq. 4 fusion per unit
   SplitFn fuse_write_q;  // cosine_fuse_drafts: the fused distribution rows
   SplitFn sample_prep;   // cosine_sample_residual: the request records

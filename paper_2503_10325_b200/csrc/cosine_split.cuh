@@ -88,6 +88,11 @@ struct SplitParams {
   int32_t* lz;
   double* segsum;  // [B][nseg] residual / bonus mass per 256-group segment
   int64_t nseg;
+  // SAMPLE selection over probability drafts: the statistics pass also writes the drafter row
+  // sums of every kSliceGroups-group slice of its chunk, slices[((unit * C + chunk) * nsl + s) * N + n]
+  // (fp32 warp sums), so that the draw x* ~ q locates its slice without re-reading the chunk
+  float* slices;
+  int64_t nsl;     // slices per chunk (ceil(cg / kSliceGroups))
   int spr;         // B2a CTAs per request
   int tpc;         // tiles per B2 CTA (<= kSegTilesPerCta)
   int b_off, nb;   // this launch covers requests [b_off, b_off + nb) (batch pipelining)
@@ -186,6 +191,34 @@ __device__ __forceinline__ int64_t warp_scan_range(const PP& P, const Decision& 
 }
 
 // ============================== kernel A ==============================
+constexpr int kSliceGroups = 32;  // groups per slice of the SAMPLE slice sums (stats_kernel<..., kSlices>)
+
+// K per-lane values -> their K warp sums in K - 1 + 5 - log2(K) shuffles instead of 5 K (a
+// transposed reduction: each level halves the values a lane holds); lane l returns the sum of
+// value l / (32 / K).
+template <int K>
+__device__ __forceinline__ float warp_sums_scatter(const float (&v)[K]) {
+  static_assert(K >= 1 && K <= 32 && (K & (K - 1)) == 0, "K: a power of two <= 32");
+  const int lane = threadIdx.x & 31;
+  float cur[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) cur[j] = v[j];
+  int o = 16;
+#pragma unroll
+  for (int w = K; w > 1; w >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < w / 2; ++j) {
+      const float send = up ? cur[j] : cur[j + w / 2];
+      const float keep = up ? cur[j + w / 2] : cur[j];
+      cur[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) cur[0] += __shfl_xor_sync(0xffffffffu, cur[0], o);
+  return cur[0];
+}
+
 // Resident CTAs per SM of the streaming kernels: register-lean (40 registers) for bf16 with
 // N <= 4, so that 48 warps of 128-bit loads are in flight per SM.
 template <typename TT, typename TQ, int NMAX>
@@ -197,8 +230,9 @@ constexpr int stats_occupancy() {
 // once; writes the chunk's partial record.  Returns the unit's record index, or -1 when the CTA
 // has no rows (position past gamma_b, bad gamma_b, or a stopped lazy request).  Ends with the
 // record written by warp 0 (no trailing barrier).
-template <typename TT, typename TQ, bool kLogits, int NMAX>
+template <typename TT, typename TQ, bool kLogits, int NMAX, bool kSlices = false>
 __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit, int rank) {
+  static_assert(!(kSlices && kLogits), "slice sums are kept for probability drafts only");
   const int C = P.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int N = P.N;
@@ -251,7 +285,7 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
   __shared__ double s_wd[kWarps][1 + kMaxN];
   __shared__ int32_t s_wbad[kWarps];
 
-  const bool greedy = P.greedy != 0;
+  const bool greedy = !kSlices && P.greedy != 0;  // (the slice variant runs at T > 0 only)
   const float k2 = P.k2f;
   float tmx = kNegBig, tmk = kNegBig, ts = 0.f;  // running max, fl(max * k2), sum 2^(l k2 - tmk)
   float tb = -INFINITY;
@@ -260,6 +294,7 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
   float dm[NMAX], dmk[NMAX], ds[NMAX];
 #pragma unroll
   for (int n = 0; n < NMAX; ++n) { dm[n] = kNegBig; dmk[n] = kNegBig; ds[n] = 0.f; }
+  float dacc = 0.f;  // kSlices: this lane's drafter's running slice total (see below)
   const int64_t gb = (int64_t)rank * P.cg;
   const int64_t ge = min(P.ngroups, gb + P.cg);
   const int64_t gfe = min(ge, P.gfull);  // full groups of the chunk
@@ -303,25 +338,69 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
     }
   };
 
-  for (int64_t gi = gb + tid; gi < gfe; gi += kThreads) {
-    Group<TT> tv;
-    Group<TQ> dv[NMAX];
-    tv.load(trow, gi);
+  if constexpr (kSlices) {
+    // the same stream in warp-contiguous slices: warp w covers slices s = w, w + 8, ... of
+    // kSliceGroups consecutive groups (two coalesced 32-group steps each), whose drafter sums it
+    // writes (a transposed warp reduction: one shuffle tree for all N sums)
+    float* sl = P.slices + (gu * C + rank) * P.nsl * N;
+    // (the chunk's drafter sums are the sums of its slices: lane l accumulates the slice totals
+    // of drafter l / (32 / NMAX), so no per-thread drafter sums stay live across the loop)
+    for (int64_t s0 = gb + (int64_t)kSliceGroups * warp; s0 < gfe; s0 += (int64_t)kSliceGroups * kWarps) {
+      float sn[NMAX];
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n)
-      if (n < Nd) dv[n].load(drow + (int64_t)n * P.ld_q, gi);
-    float f[8];
-    tv.unpack(f);
-    t_step(f, gi);
+      for (int n = 0; n < NMAX; ++n) sn[n] = 0.f;
 #pragma unroll
-    for (int n = 0; n < NMAX; ++n) {
-      if (n < Nd) {
-        dv[n].unpack(f);
-        if (!kLogits && dv[n].any_sign()) {
+      for (int h = 0; h < kSliceGroups; h += 32) {
+        const int64_t gi = s0 + h + lane;
+        if (gi < gfe) {
+          Group<TT> tv;
+          Group<TQ> dv[NMAX];
+          tv.load(trow, gi);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) dneg |= (f[e] < 0.f);
+          for (int n = 0; n < NMAX; ++n)
+            if (n < Nd) dv[n].load(drow + (int64_t)n * P.ld_q, gi);
+          float f[8];
+          tv.unpack(f);
+          t_step(f, gi);
+#pragma unroll
+          for (int n = 0; n < NMAX; ++n) {
+            if (n < Nd) {
+              dv[n].unpack(f);
+              if (dv[n].any_sign()) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) dneg |= (f[e] < 0.f);
+              }
+              sn[n] += sum8(f);
+            }
+          }
         }
-        d_step(n, f);
+      }
+      const float tot = warp_sums_scatter<NMAX>(sn);
+      dacc += tot;
+      const int idx = lane / (32 / NMAX);
+      if (lane % (32 / NMAX) == 0 && idx < Nd) sl[((s0 - gb) / kSliceGroups) * N + idx] = tot;
+    }
+  } else {
+    for (int64_t gi = gb + tid; gi < gfe; gi += kThreads) {
+      Group<TT> tv;
+      Group<TQ> dv[NMAX];
+      tv.load(trow, gi);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n)
+        if (n < Nd) dv[n].load(drow + (int64_t)n * P.ld_q, gi);
+      float f[8];
+      tv.unpack(f);
+      t_step(f, gi);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n < Nd) {
+          dv[n].unpack(f);
+          if (!kLogits && dv[n].any_sign()) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dneg |= (f[e] < 0.f);
+          }
+          d_step(n, f);
+        }
       }
     }
   }
@@ -376,10 +455,12 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) dMc = fmaxf(dMc, s_wf[w][1 + n]);
         if (ds[n] != 0.f) dsd[n] = (double)ds[n] * exp2((double)dmk[n] - (double)dMc * (double)k2);
+        dsd[n] = warp_sum(dsd[n]);
+      } else if (kSlices) {  // the warp's slice totals (+ the partial group's thread sum)
+        dsd[n] = (double)__shfl_sync(0xffffffffu, dacc, n * (32 / NMAX)) + warp_sum((double)ds[n]);
       } else {
-        dsd[n] = (double)ds[n];
+        dsd[n] = warp_sum((double)ds[n]);
       }
-      dsd[n] = warp_sum(dsd[n]);
     }
   }
   const int bad = (__any_sync(0xffffffffu, tbad) ? 1 : 0) | (__any_sync(0xffffffffu, dneg) ? 2 : 0);
@@ -424,13 +505,14 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
   return gu;
 }
 
-template <typename TT, typename TQ, bool kLogits, int NMAX>
+template <typename TT, typename TQ, bool kLogits, int NMAX, bool kSlices = false>
 __global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX>()))
     stats_kernel(const SplitParams P) {
   // every CTA of this grid is resident or done once all passed this point: kernel B (launched
   // as a programmatic dependent) may then be scheduled into the tail wave (it waits per unit)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int64_t gu = stats_body<TT, TQ, kLogits, NMAX>(P, blockIdx.x / P.C, (int)(blockIdx.x % P.C));
+  const int64_t gu =
+      stats_body<TT, TQ, kLogits, NMAX, kSlices>(P, blockIdx.x / P.C, (int)(blockIdx.x % P.C));
   if (P.fused && gu >= 0) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -853,6 +935,134 @@ __global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitPara
   if (tid == 0) {
     P.pdec[gu] = s_pd;
     write_pos_debug(P, b, i, has_d, s_pd);
+    P.ucnt[gu] = 0;   // ready for the next call
+    __threadfence();  // the decision before its count (release)
+    atomicAdd(&P.dcnt[b], 1);
+  }
+}
+
+// Kernel B1 for SAMPLE selection over probability drafts: one WARP per unit.  Steps 1-2 as
+// sample_decide_kernel; the crossing chunk's 64-group slice sums, written by the statistics pass
+// (stats_kernel<..., kSlices>), locate the slice of t in one more warp prefix (slice masses
+// sum_n (w_n / sigma_n) slice_{n,s}), and a 32-lane scan of that slice (two steps, reading #10)
+// finds x*.  Re-reads 64 groups of the N drafter rows per unit instead of half a chunk.  A t that falls in
+// no slice (the row's partial last group, or rounding at the chunk end) scans the whole chunk.
+template <typename TT, typename TQ, int NMAX>
+__global__ void __launch_bounds__(kThreads) sample_decide_w_kernel(const SplitParams P) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float s_gx[kWarps][(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kWarps][kMaxN];
+  __shared__ PosDec s_pd[kWarps];
+  __shared__ Decision s_d[kWarps];
+  __shared__ double s_w[kWarps][kMaxN], s_sig[kWarps][kMaxN];
+  __shared__ float s_dmax[kWarps][kMaxN];
+  __shared__ int64_t s_g0[kWarps], s_g1[kWarps];
+  __shared__ double s_tc[kWarps], s_Q[kWarps];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
+  if (unit >= (int64_t)P.B * (P.k + 1)) return;
+  const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  if (g < 1 || g > P.k || i > g) return;
+  const int64_t gu = (int64_t)b * (P.k + 1) + i;
+  const int N = P.N, C = P.C;
+  const bool has_d = i < g;
+  const double k2 = (double)P.k2f;
+  const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.k + i) * N * P.ld_q;
+  const TT* trow = (const TT*)P.target + gu * P.ld_t;
+  if (lane == 0) {  // this unit's C chunk records
+    uint32_t n;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.ucnt + gu) : "memory");
+      if ((int)n >= C) break;
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+  PosDec pd;
+  double sig[kMaxN];
+  float dmax[kMaxN];
+  const UnitFlags f = warp_combine<TT, TQ, false>(P, b, i, has_d, true, s_gx[warp], s_tok[warp], pd, sig, dmax);
+  int go = 0;
+  if (lane == 0) {
+    decide_lane0<false>(P, b, i, has_d, f.tok_bad, f.t_nf || f.d_nf, f.t_empty || f.d_empty, s_gx[warp],
+                        s_tok[warp], sig, dmax, pd, s_w[warp]);
+    go = (has_d && pd.status == 0) ? 1 : 0;
+    for (int n = 0; n < N; ++n) { s_sig[warp][n] = sig[n]; s_dmax[warp][n] = dmax[n]; }
+    s_pd[warp] = pd;
+  }
+  go = __shfl_sync(0xffffffffu, go, 0);
+  __syncwarp();
+  if (go) {
+    chunk_crossing_warp<false>(P, gu, (uint32_t)(i + 1), P.rids[b], s_w[warp], s_sig[warp], s_dmax[warp],
+                               &s_d[warp], &s_g0[warp], &s_g1[warp], &s_tc[warp], &s_Q[warp]);
+    __syncwarp();
+    const Decision d = s_d[warp];
+    const int64_t g0 = s_g0[warp], g1 = s_g1[warp];
+    const double tc = s_tc[warp], Q = s_Q[warp];
+    // ---- the slice of t within the chunk ----
+    const int64_t r = g0 / P.cg;
+    const int64_t gfe = min(g1, P.gfull);
+    const int nsl = gfe > g0 ? (int)((gfe - g0 + kSliceGroups - 1) / kSliceGroups) : 0;
+    const float* sl = P.slices + (gu * C + r) * P.nsl * N;
+    double a[kMaxN];
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n) a[n] = (n < N) ? s_w[warp][n] / s_sig[warp][n] : 0.0;
+    int hs = -1;
+    double tcs = 0.0, base = 0.0;
+    for (int s0 = 0; s0 < nsl && hs < 0; s0 += 32) {
+      const int s = s0 + lane;
+      double m = 0.0;
+      if (s < nsl)
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+          if (n < N) m += a[n] * (double)__ldcg(&sl[(int64_t)s * N + n]);
+      double incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double nb = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nb;
+      }
+      const double excl = base + incl - m;
+      const unsigned hit = __ballot_sync(0xffffffffu, s < nsl && m > 0.0 && excl <= tc && tc < excl + m);
+      if (hit) {
+        const int src = __ffs(hit) - 1;
+        hs = s0 + src;
+        tcs = tc - __shfl_sync(0xffffffffu, excl, src);
+      }
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    float margin = 0.f;
+    int64_t y;
+    if (hs >= 0) {
+      const int64_t sb = g0 + (int64_t)kSliceGroups * hs;
+      y = warp_scan_range<TT, TQ, false, NMAX>(P, d, kWFuseQ, trow, drow, N, sb, min(gfe, sb + kSliceGroups), tcs, Q,
+                                               &margin);
+    } else {
+      y = warp_scan_range<TT, TQ, false, NMAX>(P, d, kWFuseQ, trow, drow, N, g0, g1, tc, Q, &margin);
+    }
+    if (lane == 0) {
+      PosDec& p = s_pd[warp];
+      p.xstar = (int32_t)y;
+      if (y >= 0) {
+        double q = 0.0;
+        for (int m = 0; m < N; ++m)
+          q += s_w[warp][m] * ((double)load_one(drow + (int64_t)m * P.ld_q, y) / s_sig[warp][m]);
+        p.qx = q;
+        p.u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
+        // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
+        p.px = exp2((double)load_one(trow, y) * k2 - (double)p.M * k2) / p.S;
+        p.accept = (p.u * p.qx < p.px);
+        p.m_fa = fmin_(fmin_(p.m_fa, margin), (float)fabs(p.u - p.px / p.qx));
+      } else {
+        p.status = COSINE_REQ_EMPTY_ROW;  // unreachable: q has mass (every w_n, sigma_n > 0)
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    P.pdec[gu] = s_pd[warp];
+    write_pos_debug(P, b, i, has_d, s_pd[warp]);
     P.ucnt[gu] = 0;   // ready for the next call
     __threadfence();  // the decision before its count (release)
     atomicAdd(&P.dcnt[b], 1);

@@ -164,6 +164,24 @@ def test_sample_select_chunking(cuda_ok, cs):
     _run(inp, sm=1, cluster_size=cs, name=f"SAMPLE C={cs}")
 
 
+@pytest.mark.parametrize("V,dtype", [(5, torch.float32), (1003, torch.float32), (2051, torch.bfloat16),
+                                     (40003, torch.bfloat16)])
+def test_sample_select_ragged_tail_mass(cuda_ok, V, dtype):
+    # SAMPLE draws over probability drafts locate their 32-group slice from the statistics pass;
+    # the row's partial last group is in no slice.  Half of every drafter row's mass is moved
+    # into the last V % 8 entries so that many draws land there (and in the last full slices)
+    inp = synth.linear_inputs(32, 5, 3, V, dtype=dtype, seed=V + 7, draft_len="random")
+    d = inp["draft"]
+    tail = V % 8
+    if V > tail:
+        body = d[..., : V - tail].float()
+        d[..., : V - tail] = (body / body.sum(-1, keepdim=True) * 0.5).to(dtype)
+        d[..., V - tail:V] = 0.5 / tail
+    else:
+        d[..., :V] = 1.0 / V
+    _run(inp, sm=1, name=f"SAMPLE tail V={V}")
+
+
 @pytest.mark.slow
 def test_gpu_output_distribution_chi_square(cuda_ok):
     # SAMPLE fusion is distribution exact (reading #3): the first emitted token ~ o_0
