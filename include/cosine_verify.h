@@ -26,8 +26,11 @@
  *     synchronously and enqueue nothing.
  *   - Device-detected data errors are reported per request in status[b]; that request's
  *     accept_len is -1 and its out_tokens row is all -1; other requests are unaffected.
- *   - The context owns scratch memory (sized at init from the max_* fields).  One context
- *     may be used by one host thread / one stream at a time.
+ *   - The context owns scratch memory (sized at init from the max_* fields: per (request,
+ *     position) unit 16 partial records of 128 B, the decision, the tile masses, and for an
+ *     unsharded context over probability drafts the SAMPLE slice sums, max_drafters floats
+ *     per 256 vocabulary entries).  One context may be used by one host thread / one stream
+ *     at a time.
  *   - Randomness: U(rid, node, tag) = (Philox4x32-10(ctr = {rid_lo, rid_hi, node,
  *     (step << 4) | tag}, key = {seed_lo, seed_hi}).x0 >> 8) * 2^-24 (readings #8, #9).
  *     Tags: ACCEPT = 0, SAMPLE = 1, FUSE = 2.  Results depend only on global request ids,

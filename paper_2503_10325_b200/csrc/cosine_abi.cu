@@ -75,6 +75,7 @@ struct cosine_ctx_s {
   ChildPQ* cpq = nullptr;
   double* segsum = nullptr;
   size_t segsum_cap = 0;
+  int tiny_cap[2] = {-1, -1};  // co-resident tiny_kernel CTAs (NMAX 4 / 8), -1 = not queried
   float* slices = nullptr;  // SAMPLE selection: 64-group slice sums of the drafter rows
   size_t slices_cap = 0;    // floats
   // optional live timing of the dominant kernel (stats_kernel) with CUDA events on the stream
@@ -175,9 +176,94 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_events(cosine_ctx_t ctx) {
 // The split path: stats_kernel -> decide_kernel -> resample_kernel, the latter two programmatic
 // dependents waiting per unit / per request on device counters (scheduled into the previous
 // grid's tail wave; the waits always end because every CTA they wait for is resident or done).
+#ifdef COSINE_TRACE
+// instrumentation build: one device buffer of phase timestamps, read by cosine_trace_read
+static unsigned long long* g_trace = nullptr;
+static size_t g_trace_n = 0;
+unsigned long long* cosine_trace_buffer(size_t n) {
+  if (n > g_trace_n) {
+    cudaFree(g_trace);
+    cudaMalloc(&g_trace, n * sizeof(unsigned long long));
+    g_trace_n = n;
+  }
+  cudaMemset(g_trace, 0, g_trace_n * sizeof(unsigned long long));
+  return g_trace;
+}
+size_t cosine_trace_copy(unsigned long long* host, size_t n) {
+  cudaDeviceSynchronize();
+  n = std::min(n, g_trace_n);
+  if (n) cudaMemcpy(host, g_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return n;
+}
+#endif
+
+// Small batches (ARGMAX): the whole call as one cooperative launch of tiny_kernel when its
+// (unit, chunk) grid is co-resident and the request's CTAs cover its final draw's tiles.
+// Returns false (nothing enqueued) when the batch does not qualify.
+bool launch_tiny(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, const KernelSet& ks, cosine_status_t* st) {
+  const int64_t units = (int64_t)S.B * (S.k + 1);
+  const int slot = S.N <= 4 ? 0 : 1;
+  if (ctx->tiny_cap[slot] < 0) {
+    int occ = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.tiny, kThreads, 0) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 0;
+    }
+    ctx->tiny_cap[slot] = occ * sms;
+  }
+  const int64_t cap = ctx->tiny_cap[slot];
+  if (ctx->cfg.cluster_size > 0 || units > cap) return false;
+  int C = stats_chunks(ctx, units, S.ngroups);
+  while (C < kMaxC && units * 2 * C <= cap && S.ngroups >= (int64_t)C * kThreads) C *= 2;
+  while (C > 1 && units * C > cap) C /= 2;
+  fill_scratch(ctx, S, C);
+  const int64_t per_req = (int64_t)(S.k + 1) * C;
+  S.tpc = (int)((S.nseg + per_req - 1) / per_req);
+  if (S.tpc > kSegTilesPerCta) return false;
+  S.spr = (int)((S.nseg + S.tpc - 1) / S.tpc);
+  if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap) return false;
+  S.fused = 1;
+#ifdef COSINE_TRACE
+  S.trace = cosine_trace_buffer((size_t)units * C * 16);
+#endif
+  cudaLaunchConfig_t lc;
+  memset(&lc, 0, sizeof(lc));
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.gridDim = dim3((unsigned)(units * C), 1, 1);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // co-residency: the parts wait on other CTAs
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const auto pe = prof_events(ctx);
+  if (pe.first) cudaEventRecord(pe.first, stream);
+  const cudaError_t e = cudaLaunchKernelEx(&lc, ks.tiny, S);
+  if (pe.second) cudaEventRecord(pe.second, stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {  // (not expected: the grid fits the query)
+    cudaGetLastError();
+    return false;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ctx->last_launches = 0;
+    *st = fail(ctx, COSINE_ERR_CUDA, std::string("verify kernel (one launch): ") + cudaGetErrorString(e));
+    return true;
+  }
+  ctx->last_launches = 1;
+  ctx->last_cluster = C;
+  *st = COSINE_OK;
+  return true;
+}
+
 cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, const KernelSet& ks,
                               bool sample) {
   const int64_t units = (int64_t)S.B * (S.k + 1);
+  if (!sample && !S.lazy && !S.tree && S.mode == kSplitVerify && ks.tiny) {
+    cosine_status_t st = COSINE_OK;
+    if (launch_tiny(ctx, stream, S, ks, &st)) return st;
+  }
   fill_scratch(ctx, S, stats_chunks(ctx, units, S.ngroups));
   if ((size_t)S.B * (size_t)S.nseg > ctx->segsum_cap)
     return fail(ctx, COSINE_ERR_INVALID_ARGUMENT, "segment scratch too small");
@@ -1344,3 +1430,7 @@ cosine_status_t cosine_sample_residual(cosine_ctx_t ctx, cosine_stream_t stream,
 }
 
 }  // extern "C"
+
+#ifdef COSINE_TRACE
+extern "C" size_t cosine_trace_read(unsigned long long* host, size_t n) { return cosine_trace_copy(host, n); }
+#endif

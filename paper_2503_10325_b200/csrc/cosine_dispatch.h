@@ -22,6 +22,7 @@ struct KernelSet {
   SplitFn fuse_write_q;  // cosine_fuse_drafts: the fused distribution rows
   SplitFn sample_prep;   // cosine_sample_residual: the request records
   SplitFn resample;      // final draws
+  SplitFn tiny;          // small batches: the three steps in one cooperative launch
   SplitFn shard_pack;    // vocabulary-sharded records
   SplitFn shard_sample;  // vocabulary-sharded owner scan
   TreeFn tree_decide;

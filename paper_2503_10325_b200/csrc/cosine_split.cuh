@@ -36,6 +36,21 @@ constexpr int kLazySpan = 2;  // positions per lazy round (NEXT-1)
 
 enum SplitMode : int { kSplitVerify = 0, kSplitFuse = 1, kSplitSample = 2 };
 
+// Phase timestamps for latency studies (tools/tiny_trace.py builds the library with
+// -DCOSINE_TRACE; in the product build the macro is empty).
+#ifdef COSINE_TRACE
+#define COSINE_TRACE_AT(P, slot)                                                      \
+  do {                                                                                \
+    if ((P).trace && threadIdx.x == 0) {                                              \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      (P).trace[(size_t)blockIdx.x * 16 + (slot)] = t_;                                \
+    }                                                                                 \
+  } while (0)
+#else
+#define COSINE_TRACE_AT(P, slot) ((void)0)
+#endif
+
 struct SplitParams {
   int mode;  // kSplitVerify (cosine_verify_batch / _lazy / _tree), kSplitFuse, kSplitSample
   // cosine_fuse_drafts outputs
@@ -93,6 +108,7 @@ struct SplitParams {
   // (fp32 warp sums), so that the draw x* ~ q locates its slice without re-reading the chunk
   float* slices;
   int64_t nsl;     // slices per chunk (ceil(cg / kSliceGroups))
+  unsigned long long* trace;  // instrumentation builds only (-DCOSINE_TRACE): [grid][16] timestamps
   int spr;         // B2a CTAs per request
   int tpc;         // tiles per B2 CTA (<= kSegTilesPerCta)
   int b_off, nb;   // this launch covers requests [b_off, b_off + nb) (batch pipelining)
@@ -728,23 +744,192 @@ __device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, i
   return f;
 }
 
-// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131); lane 0
-// writes the decision to *out (and the diagnostics if asked).
+// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131) and
+// writes the decision to *out (and the diagnostics if asked), lane-parallel: lane n holds
+// drafter n's normaliser sigma_n and confidence c_n, the fusion argmax / second best / weight
+// sums are shuffle reductions, lane n writes drafter n's fields.  (The same decision as
+// decide_lane0 up to the order of the fp64 sums over drafters; a lane-0 sequential version
+// keeps its arrays in local memory and costs ~7 us of latency per position, which dominates
+// small batches.)  Ends with __syncwarp().
 template <typename TT, typename TQ, bool kLogits>
 __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
-                                            int32_t* s_tokw, PosDec* out, bool write_debug,
-                                            PosDec* out2 = nullptr) {
+                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
+  const int lane = threadIdx.x & 31;
   const bool has_d = i < g;
-  PosDec pd;
-  double sig[kMaxN];
-  float dmax[kMaxN];
-  const UnitFlags f = warp_combine<TT, TQ, kLogits>(P, b, i, has_d, false, s_gxw, s_tokw, pd, sig, dmax);
-  if ((threadIdx.x & 31) != 0) return;
-  decide_lane0<kLogits>(P, b, i, has_d, f.tok_bad, f.t_nf || f.d_nf, f.t_empty || f.d_empty, s_gxw, s_tokw, sig,
-                        dmax, pd);
-  *out = pd;
-  if (out2) *out2 = pd;
-  if (write_debug) write_pos_debug(P, b, i, has_d, pd);
+  const int N = P.N, C = P.C;
+  const int64_t unit = (int64_t)b * (P.k + 1) + i;
+  const bool greedy = P.greedy != 0;
+  const double k2 = (double)P.k2f;
+  // ---- gathers: lane m * N + n loads d_m(X_n) (m < N) or l(X_n) (m == N) ----
+  const int ng = has_d ? N * (N + 1) : 0;
+  if (lane < ng) {
+    const int n = lane % N, m = lane / N;
+    const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
+    float v = 0.f;
+    if (tk >= 0 && (int64_t)tk < P.V) {
+      if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
+      else v = load_one((const TT*)P.target + unit * P.ld_t, tk);
+    }
+    s_gxw[m * kMaxN + n] = v;
+    if (m == 0) s_tokw[n] = tk;
+  }
+  COSINE_TRACE_AT(P, 8);
+  // ---- the unit's C chunk records (chunk r in lane r) ----
+  const PartRec* parts = P.parts + unit * C;
+  const bool own = lane < C;
+  const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
+  float M;
+  double S = 0.0;
+  int64_t amax = -1;
+  bool t_nf, t_empty;
+  if (greedy) {
+    float bv = own ? tmax : -INFINITY;
+    int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
+    warp_argmax(bv, bi);
+    t_nf = (bad & 1) != 0;
+    t_empty = (bi < 0);
+    amax = bi;
+    M = bv;
+  } else {
+    M = warp_max(tmax);
+    const double tsum = own ? __ldcg(&parts[lane].tsum) : 0.0;
+    S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
+    t_nf = !isfinite(S) || !isfinite(M);
+    t_empty = !t_nf && !(S > 0.0);
+  }
+  // ---- drafter normalisers: sigma_n, (LOGITS) the row max, in lane n ----
+  double sig_l = NAN;
+  float dmx_l = kNegBig;
+  bool d_nf = false, d_empty = false;
+  if (has_d) {
+    d_nf = (bad & 2) != 0;
+    for (int n = 0; n < N; ++n) {
+      double sv;
+      float mx = kNegBig;
+      const double ds = own ? __ldcg(&parts[lane].dsum[n]) : 0.0;
+      if (kLogits) {
+        const float dmr = own ? __ldcg(&parts[lane].dmax[n]) : kNegBig;
+        mx = warp_max(dmr);
+        sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
+        if (!isfinite(mx)) d_nf = true;
+      } else {
+        sv = warp_sum(ds);
+      }
+      if (lane == n) { sig_l = sv; dmx_l = mx; }
+      if (!isfinite(sv)) d_nf = true;
+      else if (!(sv > 0.0)) d_empty = true;
+    }
+  }
+  __syncwarp();
+  COSINE_TRACE_AT(P, 9);
+  const bool dl = lane < N;  // this lane holds a drafter
+  bool tok_bad = false;
+  if (has_d) {
+    const int32_t t = dl ? s_tokw[lane] : 0;
+    tok_bad = __any_sync(0xffffffffu, dl && (t < 0 || (int64_t)t >= P.V));
+  }
+  int stc = tok_bad ? COSINE_REQ_TOKEN_OUT_OF_RANGE
+                    : ((t_nf || d_nf) ? COSINE_REQ_NONFINITE_INPUT : ((t_empty || d_empty) ? COSINE_REQ_EMPTY_ROW : 0));
+  // q_n(x) of a gathered drafter value (PROBS: d / sigma; LOGITS: softmax at the same k2), lane n
+  auto qval = [&](double dv) {
+    return kLogits ? exp2(dv * k2 - (double)dmx_l * k2) / sig_l : dv / sig_l;
+  };
+  double c_l = 0.0;  // c_{n,i} = q_{n,i}(X_{n,i})
+  if (!stc && has_d) {
+    if (dl) c_l = qval((double)s_gxw[lane * kMaxN + lane]);
+    if (__any_sync(0xffffffffu, dl && c_l == 0.0)) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+  }
+  const bool filled = !stc && has_d;
+  COSINE_TRACE_AT(P, 10);
+  int accept = 1, xstar = -1;
+  float m_fa = INFINITY;
+  double px = NAN, qx = NAN, u = NAN, w_l = NAN;
+  if (filled) {
+    // Eq. 4: n* = argmax_n c_n, ties -> lowest n; fused weights (reading #2)
+    double bc = dl ? c_l : -1.0;
+    int bn = dl ? lane : 1 << 30;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const int on = __shfl_xor_sync(0xffffffffu, bn, o);
+      if (oc > bc || (oc == bc && on < bn)) { bc = oc; bn = on; }
+    }
+    const int ns = bn;
+    double second = (dl && lane != ns) ? c_l : -1.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) second = fmax(second, __shfl_xor_sync(0xffffffffu, second, o));
+    m_fa = (N > 1) ? (float)((bc - second) / bc) : INFINITY;
+    if (P.weight_mode == COSINE_W_CONF) {
+      const double sc = warp_sum(dl ? c_l : 0.0);
+      w_l = dl ? c_l / sc : 0.0;
+    } else if (P.weight_mode == COSINE_W_UNIFORM) {
+      w_l = dl ? 1.0 / (double)N : 0.0;
+    } else {
+      w_l = (lane == ns) ? 1.0 : 0.0;
+    }
+    xstar = s_tokw[ns];
+    if (P.weight_mode == COSINE_W_POINT) {
+      qx = 1.0;
+    } else {
+      qx = warp_sum(dl ? w_l * qval((double)s_gxw[lane * kMaxN + ns]) : 0.0);
+    }
+    COSINE_TRACE_AT(P, 11);
+    u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
+    COSINE_TRACE_AT(P, 12);
+    if (greedy) {
+      accept = ((int64_t)xstar == amax);
+    } else {
+      // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
+      px = exp2((double)s_gxw[N * kMaxN + ns] * k2 - (double)M * k2) / S;
+      accept = (u * qx < px);
+      m_fa = fmin_(m_fa, (float)fabs(u - px / qx));
+    }
+  }
+  COSINE_TRACE_AT(P, 13);
+  // ---- the decision record: lane n < kMaxN writes drafter n's fields, lane 0 the scalars ----
+  if (lane < kMaxN) {
+    const bool mine = filled && dl;
+    out->a[lane] = mine ? (float)(w_l / sig_l) : 0.f;
+    out->dm[lane] = mine ? dmx_l : 0.f;
+    out->sig[lane] = mine ? (float)sig_l : NAN;
+    out->c[lane] = mine ? (float)c_l : NAN;
+    out->w[lane] = mine ? (float)w_l : NAN;
+  }
+  if (lane == 0) {
+    out->status = stc;
+    out->accept = accept;
+    out->xstar = xstar;
+    out->amax = amax;
+    out->m_fa = m_fa;
+    out->M = M;
+    out->S = S;
+    out->px = px;
+    out->qx = qx;
+    out->u = u;
+  }
+  if (write_debug) {
+    const cosine_debug_t& D = P.dbg;
+    const int64_t o1 = (int64_t)b * P.k + i;
+    if (lane == 0) {
+      if (D.row_max) D.row_max[unit] = M;
+      if (D.row_sumexp) D.row_sumexp[unit] = greedy ? 0.f : (float)S;
+      if (has_d) {
+        if (D.p_x) D.p_x[o1] = (float)px;
+        if (D.q_x) D.q_x[o1] = (float)qx;
+        if (D.accept_u) D.accept_u[o1] = (float)u;
+        if (D.fused_tokens) D.fused_tokens[o1] = xstar;
+      }
+    }
+    if (has_d && dl) {
+      const bool mine = filled;
+      if (D.draft_norm) D.draft_norm[o1 * N + lane] = mine ? (float)sig_l : NAN;
+      if (D.conf) D.conf[o1 * N + lane] = mine ? (float)c_l : NAN;
+      if (D.weights) D.weights[o1 * N + lane] = mine ? (float)w_l : NAN;
+    }
+  }
+  __syncwarp();
+  COSINE_TRACE_AT(P, 14);
 }
 
 // Kernel B1 (split path): one warp per (request, position) -> PosDec in global memory (+
@@ -1600,6 +1785,7 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
     if (s.last && P.fused) P.dcnt[b] = 0;  // every part of the request has passed its wait
   }
   __syncthreads();
+  COSINE_TRACE_AT(P, 5);
   if (!s.last) return;
   // ---------------- the last part of the request: crossing tile, scan, outputs ----------------
   __threadfence();
@@ -1653,6 +1839,7 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
                                           s.wi, &s.found, &s.margin);
     margin = s.margin;
   } else if (s.tstar >= 0) {
+    COSINE_TRACE_AT(P, 6);
     const int64_t sb = s.tstar * kTileGroups;
     y = scan_range<TT, TQ, kLogits, NMAX>(P, d, kind, trow, drow, Nd, sb, min(P.ngroups, sb + kTileGroups),
                                           s.tc, Z, s.scan, s.wi, &s.found, &s.margin);
@@ -1728,6 +1915,81 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     return;
   }
   resample_tiles<TT, TQ, kLogits, NMAX>(P, b, part, s);
+}
+
+// ============================== small batches: one launch ==============================
+// The three kernels' work in ONE cooperative launch for a batch whose (unit, chunk) grid is
+// co-resident (c1, c2: latency-bound — the split path pays three dependent launches and a
+// device round trip per hand-off).  CTA (unit u = (b, i), chunk r), p = i C + r its index among
+// request b's (k + 1) C CTAs:
+//  1. the chunk's statistics (stats_body) and its count on ucnt[u]; the unit's LAST chunk CTA
+//     (the one whose count completes the unit, so no wait) decides the unit with one warp
+//     (Eq. 4 fusion and acceptance, warp_decide) and counts the decision on dcnt[b];
+//  2. CTAs p < spr are the parts of the request's final draw: wait for the request's g + 1
+//     decisions (every CTA they wait for is resident: cooperative launch), then the tile
+//     masses of row L and, in the last part, the crossing tile and its scan (resample_tiles).
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, 4) tiny_kernel(const SplitParams P) {
+  __shared__ __align__(16) ResampleSmem s;
+  __shared__ float s_gx[(kMaxN + 1) * kMaxN];
+  __shared__ int32_t s_tok[kMaxN];
+  __shared__ int s_decide;
+  const int C = P.C;
+  const int64_t u = blockIdx.x / C;
+  const int r = (int)(blockIdx.x % C);
+  const int b = (int)(u / (P.k + 1)), i = (int)(u % (P.k + 1));
+  const int p = i * C + r;
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  COSINE_TRACE_AT(P, 0);
+  const int64_t gu = stats_body<TT, TQ, kLogits, NMAX>(P, u, r);
+  __syncthreads();
+  COSINE_TRACE_AT(P, 1);
+  if (threadIdx.x == 0) {
+    int last = 0;
+    if (gu >= 0) {
+      __threadfence();  // the record before the count (release)
+      last = atomicAdd(&P.ucnt[gu], 1) == C - 1;
+      if (last) __threadfence();  // (acquire: the unit's other records)
+    }
+    s_decide = last;
+  }
+  __syncthreads();
+  if (s_decide && threadIdx.x < 32) {
+    warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx, s_tok, &P.pdec[gu], true);
+    if (threadIdx.x == 0) {
+      P.ucnt[gu] = 0;   // ready for the next call
+      __threadfence();  // the decision before its count (release)
+      atomicAdd(&P.dcnt[b], 1);
+    }
+    COSINE_TRACE_AT(P, 2);
+  }
+  if (p >= P.spr) return;
+  if (g < 1 || g > P.k) {
+    if (p == 0 && threadIdx.x == 0) write_bad_len(P, b);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t n;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.dcnt + b) : "memory");
+      if ((int)n >= g + 1) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  COSINE_TRACE_AT(P, 3);
+  load_request(P, b, g, s);
+  COSINE_TRACE_AT(P, 4);
+  if (!s.v.sample) {
+    if (threadIdx.x == 0 && atomicAdd(&P.counters[b], 1) == P.spr - 1) {  // the last part resets
+      P.counters[b] = 0;
+      P.dcnt[b] = 0;
+    }
+    if (p == 0) write_plain_outputs(P, b, s);
+    return;
+  }
+  resample_tiles<TT, TQ, kLogits, NMAX>(P, b, p, s);
+  COSINE_TRACE_AT(P, 7);
 }
 
 }  // namespace cosine

@@ -1,0 +1,93 @@
+"""Latency study: phase timestamps (%globaltimer) of the one-launch small-batch kernel.
+
+`python tools/tiny_trace.py build` (here, CPU) compiles an instrumentation copy of the library
+with -DCOSINE_TRACE into tools/_trace/pkg/ (the product build has no instrumentation);
+`python tools/tiny_trace.py run [c1|c2]` (GPU) imports that copy, runs calls with L2 flushed
+before each, and prints per phase the min / median / max over CTAs of the time since the
+earliest CTA start (µs).  Slots: 0 start, 1 stats done, 2 unit decided (deciding CTAs),
+3 request's decisions seen (parts), 4 request loaded, 5 part's tile masses done, 6 crossing
+tile found (last part), 7 part end; inside the decision (deciding CTAs): 8 start, 9 gathers and
+records combined, 10 confidences, 11 fusion and q(x*), 12 Philox, 13 acceptance, 14 written.
+"""
+import ctypes
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TR = os.path.join(ROOT, "tools", "_trace")
+PKGDST = os.path.join(TR, "pkg", "paper_2503_10325_b200")
+
+
+def build():
+    sys.path.insert(0, os.path.join(ROOT, "paper_2503_10325_b200"))
+    import build as B
+    os.makedirs(os.path.join(TR, "obj"), exist_ok=True)
+    os.makedirs(PKGDST, exist_ok=True)
+    objs = []
+    procs = []
+    for src in B.SOURCES:
+        o = os.path.join(TR, "obj", os.path.basename(src)[:-3] + ".o")
+        objs.append(o)
+        procs.append(subprocess.Popen([B.nvcc(), *B.NVCC_FLAGS, "-DCOSINE_TRACE", "-I", B.INCLUDE, "-I", B.CSRC,
+                                       "-c", "-o", o, src], stdout=subprocess.PIPE, stderr=subprocess.PIPE))
+    for p in procs:
+        out, err = p.communicate()
+        if p.returncode:
+            sys.stderr.write(err.decode())
+            raise SystemExit("nvcc failed")
+    for f in os.listdir(os.path.join(ROOT, "paper_2503_10325_b200")):
+        if f.endswith(".py"):
+            shutil.copy(os.path.join(ROOT, "paper_2503_10325_b200", f), PKGDST)
+    subprocess.check_call([B.nvcc(), *B.ARCH, "-shared", "-o", os.path.join(PKGDST, "libcosine_verify.so"),
+                           *objs, "-lnccl"])
+    print("built", PKGDST)
+
+
+def run(cfg, flush=True):
+    sys.path.insert(0, os.path.join(TR, "pkg"))
+    sys.path.insert(1, ROOT)
+    import numpy as np
+    import torch
+    import paper_2503_10325_b200 as cv
+    import synth
+    assert cv.__file__.startswith(TR), cv.__file__
+    lib = ctypes.CDLL(os.path.join(PKGDST, "libcosine_verify.so"))
+    lib.cosine_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    lib.cosine_trace_read.restype = ctypes.c_size_t
+    c = synth.CONFIGS[cfg]
+    inp = synth.linear_inputs(c["B"], c["k"], c["N"], c["V"], dtype=c["dtype"], seed=3, device="cuda")
+    ver = cv.Verifier(c["V"], max_batch=c["B"], k=c["k"], N=c["N"], device=0, target_dtype=c["dtype"],
+                      draft_dtype=c["dtype"], seed=1)
+    scratch = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+    rows = []
+    for it in range(12):
+        if flush:
+            scratch.sum()
+        ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"], temperature=1.0)
+        torch.cuda.synchronize()
+        grid = cv.cosine_last_launch_count(ver.ctx)
+        buf = np.zeros(1 << 20, dtype=np.uint64)
+        n = lib.cosine_trace_read(buf.ctypes.data, buf.size)
+        t = buf[:n].reshape(-1, 16).astype(np.int64)
+        if it >= 2:
+            rows.append(t)
+    print(f"{cfg} (L2 {'flushed' if flush else 'warm'}): {rows[0].shape[0]} CTAs, last launch count {grid}")
+    for slot in range(16):
+        vals = []
+        for t in rows:
+            t0 = t[:, 0][t[:, 0] > 0].min()
+            v = t[:, slot][t[:, slot] > 0] - t0
+            if v.size:
+                vals.append((v.min(), np.median(v), v.max()))
+        if vals:
+            a = np.array(vals, dtype=np.float64).mean(0) / 1e3
+            print(f"  slot {slot}: min {a[0]:7.2f}  median {a[1]:7.2f}  max {a[2]:7.2f} us")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        run(sys.argv[2] if len(sys.argv) > 2 else "c1", flush="noflush" not in sys.argv)
