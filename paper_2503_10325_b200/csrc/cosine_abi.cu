@@ -236,7 +236,11 @@ bool launch_tiny(cosine_ctx_t ctx, cudaStream_t stream, SplitParams& S, const Ke
   at[0].id = cudaLaunchAttributeCooperative;  // co-residency: the parts wait on other CTAs
   at[0].val.cooperative = 1;
   lc.attrs = at;
+#ifdef COSINE_TRACE_NONCOOP  // (latency study only)
+  lc.numAttrs = 0;
+#else
   lc.numAttrs = 1;
+#endif
   const auto pe = prof_events(ctx);
   if (pe.first) cudaEventRecord(pe.first, stream);
   const cudaError_t e = cudaLaunchKernelEx(&lc, ks.tiny, S);

@@ -160,6 +160,21 @@ __device__ __forceinline__ void warp_argmax(float& v, int64_t& idx) {
 }
 
 // ---------------------------------------------------------------------------
+// Device counters between CTAs: release arrivals (the CTA's writes, ordered before by a barrier,
+// become visible before the count: the red/atom's release is cumulative) and acquire waits
+// (ld.acquire).  A plain __threadfence (fence.sc + L1 invalidate) + atomicAdd costs the
+// arriving CTA ~1 us more before it can retire.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_release_add(int32_t* p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t atom_acq_rel_add(int32_t* p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// ---------------------------------------------------------------------------
 // Cluster barrier halves and mbarriers (PTX ISA: barrier.cluster, mbarrier, mapa)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

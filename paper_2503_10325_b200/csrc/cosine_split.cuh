@@ -531,10 +531,7 @@ __global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX>()))
       stats_body<TT, TQ, kLogits, NMAX, kSlices>(P, blockIdx.x / P.C, (int)(blockIdx.x % P.C));
   if (P.fused && gu >= 0) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();  // the record before the count (release)
-      atomicAdd(&P.ucnt[gu], 1);
-    }
+    if (threadIdx.x == 0) red_release_add(&P.ucnt[gu], 1);  // the record before the count
   }
 }
 
@@ -958,9 +955,8 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   __syncwarp();
   warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[gu], true);
   if ((threadIdx.x & 31) == 0) {
-    P.ucnt[gu] = 0;   // ready for the next call
-    __threadfence();  // the decision before its count (release)
-    atomicAdd(&P.dcnt[b], 1);
+    P.ucnt[gu] = 0;                 // ready for the next call
+    red_release_add(&P.dcnt[b], 1);  // the decision before its count
   }
 }
 
@@ -1120,9 +1116,8 @@ __global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitPara
   if (tid == 0) {
     P.pdec[gu] = s_pd;
     write_pos_debug(P, b, i, has_d, s_pd);
-    P.ucnt[gu] = 0;   // ready for the next call
-    __threadfence();  // the decision before its count (release)
-    atomicAdd(&P.dcnt[b], 1);
+    P.ucnt[gu] = 0;                 // ready for the next call
+    red_release_add(&P.dcnt[b], 1);  // the decision before its count
   }
 }
 
@@ -1248,9 +1243,8 @@ __global__ void __launch_bounds__(kThreads) sample_decide_w_kernel(const SplitPa
   if (lane == 0) {
     P.pdec[gu] = s_pd[warp];
     write_pos_debug(P, b, i, has_d, s_pd[warp]);
-    P.ucnt[gu] = 0;   // ready for the next call
-    __threadfence();  // the decision before its count (release)
-    atomicAdd(&P.dcnt[b], 1);
+    P.ucnt[gu] = 0;                 // ready for the next call
+    red_release_add(&P.dcnt[b], 1);  // the decision before its count
   }
 }
 
@@ -1778,9 +1772,8 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
     P.segsum[(int64_t)b * P.nseg + tile0 + tid] = z;
   }
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const int old = atomicAdd(&P.counters[b], 1);
+  if (tid == 0) {  // the masses before the count; the last part acquires the others'
+    const int old = atom_acq_rel_add(&P.counters[b], 1);
     s.last = (old == P.spr - 1);
     if (s.last && P.fused) P.dcnt[b] = 0;  // every part of the request has passed its wait
   }
@@ -1788,7 +1781,6 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
   COSINE_TRACE_AT(P, 5);
   if (!s.last) return;
   // ---------------- the last part of the request: crossing tile, scan, outputs ----------------
-  __threadfence();
   const double* ss = P.segsum + (int64_t)b * P.nseg;
   const bool in_smem = P.nseg <= kMaxSeg;
   if (in_smem)
@@ -1946,20 +1938,16 @@ __global__ void __launch_bounds__(kThreads, 4) tiny_kernel(const SplitParams P) 
   COSINE_TRACE_AT(P, 1);
   if (threadIdx.x == 0) {
     int last = 0;
-    if (gu >= 0) {
-      __threadfence();  // the record before the count (release)
-      last = atomicAdd(&P.ucnt[gu], 1) == C - 1;
-      if (last) __threadfence();  // (acquire: the unit's other records)
-    }
+    if (gu >= 0)  // the record before the count; the unit's last chunk acquires the others'
+      last = atom_acq_rel_add(&P.ucnt[gu], 1) == C - 1;
     s_decide = last;
   }
   __syncthreads();
   if (s_decide && threadIdx.x < 32) {
     warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx, s_tok, &P.pdec[gu], true);
     if (threadIdx.x == 0) {
-      P.ucnt[gu] = 0;   // ready for the next call
-      __threadfence();  // the decision before its count (release)
-      atomicAdd(&P.dcnt[b], 1);
+      P.ucnt[gu] = 0;                 // ready for the next call
+      red_release_add(&P.dcnt[b], 1);  // the decision before its count
     }
     COSINE_TRACE_AT(P, 2);
   }

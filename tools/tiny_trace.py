@@ -16,7 +16,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-TR = os.path.join(ROOT, "tools", "_trace")
+VARIANT = os.environ.get("TRACE_VARIANT", "")  # "noncoop": the one-launch kernel without the cooperative attribute
+TR = os.path.join(ROOT, "tools", "_trace" + VARIANT)
 PKGDST = os.path.join(TR, "pkg", "paper_2503_10325_b200")
 
 
@@ -30,7 +31,7 @@ def build():
     for src in B.SOURCES:
         o = os.path.join(TR, "obj", os.path.basename(src)[:-3] + ".o")
         objs.append(o)
-        procs.append(subprocess.Popen([B.nvcc(), *B.NVCC_FLAGS, "-DCOSINE_TRACE", "-I", B.INCLUDE, "-I", B.CSRC,
+        procs.append(subprocess.Popen([B.nvcc(), *B.NVCC_FLAGS, "-DCOSINE_TRACE", *(["-DCOSINE_TRACE_NONCOOP"] if VARIANT == "noncoop" else []), "-I", B.INCLUDE, "-I", B.CSRC,
                                        "-c", "-o", o, src], stdout=subprocess.PIPE, stderr=subprocess.PIPE))
     for p in procs:
         out, err = p.communicate()
@@ -62,18 +63,25 @@ def run(cfg, flush=True):
                       draft_dtype=c["dtype"], seed=1)
     scratch = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
     rows = []
+    ev_us = []
     for it in range(12):
         if flush:
             scratch.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"], temperature=1.0)
+        e1.record()
         torch.cuda.synchronize()
+        if it >= 2:
+            ev_us.append(e0.elapsed_time(e1) * 1e3)
         grid = cv.cosine_last_launch_count(ver.ctx)
         buf = np.zeros(1 << 20, dtype=np.uint64)
         n = lib.cosine_trace_read(buf.ctypes.data, buf.size)
         t = buf[:n].reshape(-1, 16).astype(np.int64)
         if it >= 2:
             rows.append(t)
-    print(f"{cfg} (L2 {'flushed' if flush else 'warm'}): {rows[0].shape[0]} CTAs, last launch count {grid}")
+    print(f"{cfg} (L2 {'flushed' if flush else 'warm'}{', ' + VARIANT if VARIANT else ''}): {rows[0].shape[0]} CTAs, "
+          f"last launch count {grid}, call (events) median {np.median(ev_us):.2f} us")
     for slot in range(16):
         vals = []
         for t in rows:
