@@ -287,9 +287,20 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   const auto pe = prof_events(ctx);
+#ifdef COSINE_TRACE  // [stats grid | decide grid | resample grid] x 16 slots
+  const size_t n_st = (size_t)units * S.C, n_de = (size_t)units, n_rs = (size_t)S.B * S.spr;
+  unsigned long long* tb = cosine_trace_buffer(16 + (n_st + n_de + n_rs) * 16);
+  const unsigned long long hdr[3] = {n_st, n_de, n_rs};  // header: the three grids' sizes
+  cudaMemcpy(tb, hdr, sizeof(hdr), cudaMemcpyHostToDevice);
+  tb += 16;
+  S.trace = tb;
+#endif
   if (pe.first) cudaEventRecord(pe.first, stream);
   lc.gridDim = dim3((unsigned)(units * S.C), 1, 1);
   cudaError_t e = cudaLaunchKernelEx(&lc, sliced ? ks.stats_slices : ks.stats, S);
+#ifdef COSINE_TRACE
+  S.trace = tb + n_st * 16;
+#endif
   if (pe.second) cudaEventRecord(pe.second, stream);
   if (e == cudaSuccess) {
     // ARGMAX and sliced SAMPLE: a warp per unit; SAMPLE otherwise: a CTA per unit (the draw
@@ -300,6 +311,9 @@ cosine_status_t launch_split3(cosine_ctx_t ctx, cudaStream_t stream, SplitParams
     e = cudaLaunchKernelEx(&lc, !sample ? ks.decide : (sliced ? ks.sample_decide_w : ks.sample_decide), S);
   }
   if (e == cudaSuccess) {
+#ifdef COSINE_TRACE
+    S.trace = tb + (n_st + n_de) * 16;
+#endif
     lc.gridDim = dim3((unsigned)(S.B * S.spr), 1, 1);
     lc.attrs = at;
     lc.numAttrs = 1;

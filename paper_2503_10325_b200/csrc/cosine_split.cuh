@@ -527,10 +527,12 @@ __global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX>()))
   // every CTA of this grid is resident or done once all passed this point: kernel B (launched
   // as a programmatic dependent) may then be scheduled into the tail wave (it waits per unit)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  COSINE_TRACE_AT(P, 0);
   const int64_t gu =
       stats_body<TT, TQ, kLogits, NMAX, kSlices>(P, blockIdx.x / P.C, (int)(blockIdx.x % P.C));
   if (P.fused && gu >= 0) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
     __syncthreads();
+    COSINE_TRACE_AT(P, 1);
     if (threadIdx.x == 0) red_release_add(&P.ucnt[gu], 1);  // the record before the count
   }
 }
@@ -943,6 +945,7 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
   const int g = P.draft_len ? P.draft_len[b] : P.k;
   if (g < 1 || g > P.k || i > g) return;
   const int64_t gu = (int64_t)b * (P.k + 1) + i;
+  COSINE_TRACE_AT(P, 0);
   // this unit's C chunk records (every stats CTA is resident or done once this CTA runs)
   if ((threadIdx.x & 31) == 0) {
     uint32_t n;
@@ -953,7 +956,9 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(const SplitParams P) {
     }
   }
   __syncwarp();
+  COSINE_TRACE_AT(P, 1);
   warp_decide<TT, TQ, kLogits>(P, b, i, g, s_gx[warp], s_tok[warp], &P.pdec[gu], true);
+  COSINE_TRACE_AT(P, 2);
   if ((threadIdx.x & 31) == 0) {
     P.ucnt[gu] = 0;                 // ready for the next call
     red_release_add(&P.dcnt[b], 1);  // the decision before its count
@@ -1857,31 +1862,9 @@ __device__ __forceinline__ void resample_tiles(const SplitParams& P, int b, int 
   }
 }
 
-// Kernel B2 (lazy and vocabulary-sharded paths): CTA (request b, part), a programmatic
-// dependent of the kernel that wrote the decisions.
+// One item of kernel B2: part `part` of request b's final draw (the decisions are complete).
 template <typename TT, typename TQ, bool kLogits, int NMAX>
-__global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams P) {
-  __shared__ __align__(16) ResampleSmem s;
-  const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
-  const int part = blockIdx.x % P.spr;
-  const int g = P.draft_len ? P.draft_len[b] : P.k;
-  if (P.fused) {
-    // split path: wait for this request's g + 1 decisions only (every decide_kernel CTA is
-    // resident or done once this CTA runs, so the wait always ends), not for the whole grid
-    if (g >= 1 && g <= P.k) {
-      if (threadIdx.x == 0) {
-        uint32_t n;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.dcnt + b) : "memory");
-          if ((int)n >= g + 1) break;
-          __nanosleep(200);
-        }
-      }
-      __syncthreads();
-    }
-  } else {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the decisions (PDL)
-  }
+__device__ __forceinline__ void resample_item(const SplitParams& P, int b, int part, int g, ResampleSmem& s) {
   if (g < 1 || g > P.k) {
     if (part == 0 && threadIdx.x == 0) {
       if (P.shard) shard_z_out(P, b, 0.0);  // the outputs come from shard_finish_kernel
@@ -1889,6 +1872,7 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     }
     return;
   }
+  COSINE_TRACE_AT(P, 1);
   load_request(P, b, g, s);
   if (!s.v.sample) {
     if (P.fused && threadIdx.x == 0) {  // the request's last part resets the counters
@@ -1907,6 +1891,38 @@ __global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams
     return;
   }
   resample_tiles<TT, TQ, kLogits, NMAX>(P, b, part, s);
+}
+
+// Kernel B2: CTA (request b, part), a programmatic dependent of the kernel that wrote the
+// decisions.  Split path (P.fused): waits for its request's g + 1 decisions only (every
+// decide_kernel CTA is resident or done once this CTA runs, so the wait always ends), not for
+// the whole grid.  (Measured slower on c3 and not kept: a persistent one-wave grid taking the
+// parts from a device counter, 462 vs 454 us; two tiles per thread in flight at 4 CTAs / SM,
+// 465 us.)
+template <typename TT, typename TQ, bool kLogits, int NMAX>
+__global__ void __launch_bounds__(kThreads, 5) resample_kernel(const SplitParams P) {
+  __shared__ __align__(16) ResampleSmem s;
+  const int b = P.b_off + blockIdx.x / P.spr;  // spr = CTAs per request
+  const int part = blockIdx.x % P.spr;
+  const int g = P.draft_len ? P.draft_len[b] : P.k;
+  COSINE_TRACE_AT(P, 0);
+  if (P.fused) {
+    if (g >= 1 && g <= P.k) {
+      if (threadIdx.x == 0) {
+        uint32_t n;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.dcnt + b) : "memory");
+          if ((int)n >= g + 1) break;
+          __nanosleep(200);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the decisions (PDL)
+  }
+  resample_item<TT, TQ, kLogits, NMAX>(P, b, part, g, s);
+  COSINE_TRACE_AT(P, 7);
 }
 
 // ============================== small batches: one launch ==============================

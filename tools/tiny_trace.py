@@ -94,7 +94,52 @@ def run(cfg, flush=True):
             print(f"  slot {slot}: min {a[0]:7.2f}  median {a[1]:7.2f}  max {a[2]:7.2f} us")
 
 
+def run_split(cfg, select=0):
+    """c3-size split path: per-kernel phase timestamps relative to the first stats CTA."""
+    sys.path.insert(0, os.path.join(TR, "pkg"))
+    sys.path.insert(1, ROOT)
+    import numpy as np
+    import torch
+    import paper_2503_10325_b200 as cv
+    import synth
+    lib = ctypes.CDLL(os.path.join(PKGDST, "libcosine_verify.so"))
+    lib.cosine_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    lib.cosine_trace_read.restype = ctypes.c_size_t
+    c = synth.CONFIGS[cfg]
+    inp = synth.linear_inputs(c["B"], c["k"], c["N"], c["V"], dtype=c["dtype"], seed=3, device="cuda")
+    ver = cv.Verifier(c["V"], max_batch=c["B"], k=c["k"], N=c["N"], device=0, target_dtype=c["dtype"],
+                      draft_dtype=c["dtype"], seed=1)
+    res = []
+    for it in range(6):
+        ver.verify(inp["target"], inp["draft"], inp["draft_tokens"], inp["request_ids"], temperature=1.0,
+                   select_mode=select)
+        torch.cuda.synchronize()
+        buf = np.zeros(1 << 23, dtype=np.uint64)
+        n = lib.cosine_trace_read(buf.ctypes.data, buf.size)
+        n_st, n_de, n_rs = (int(x) for x in buf[:3])
+        t = buf[16:16 + 16 * (n_st + n_de + n_rs)].reshape(-1, 16).astype(np.int64)
+        if it >= 2:
+            res.append((t[:n_st], t[n_st:n_st + n_de], t[n_st + n_de:]))
+    names = {"stats": {0: "start", 1: "done"}, "decide": {0: "start", 1: "unit ready", 2: "decided"},
+             "resample": {0: "start", 1: "decisions seen", 5: "tile masses", 6: "crossing (last)", 7: "end"}}
+    print(f"{cfg} split path (select {select}): grids {n_st} / {n_de} / {n_rs} CTAs")
+    for gi, gname in enumerate(["stats", "decide", "resample"]):
+        for slot, sname in names[gname].items():
+            vals = []
+            for r in res:
+                t0 = r[0][:, 0][r[0][:, 0] > 0].min()
+                v = r[gi][:, slot][r[gi][:, slot] > 0] - t0
+                if v.size:
+                    vals.append(np.percentile(v, [0, 10, 50, 90, 100]))
+            if vals:
+                a = np.array(vals).mean(0) / 1e3
+                print(f"  {gname:8s} {sname:15s} " + "  ".join(f"{x:7.1f}" for x in a) + "   (min p10 p50 p90 max, us)")
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "split":
+        run_split(sys.argv[2] if len(sys.argv) > 2 else "c3", int(sys.argv[3]) if len(sys.argv) > 3 else 0)
+        raise SystemExit
     if sys.argv[1] == "build":
         build()
     else:
