@@ -192,31 +192,32 @@ __global__ void __launch_bounds__(kThreads) shard_decide_kernel(const SplitParam
   const float* recf = reinterpret_cast<const float*>(rec);
   const uint32_t flags = own ? rec[1] : 0u;
   const int bad = (int)__reduce_or_sync(0xffffffffu, flags & 3u);
-  PosDec pd;
-  init_posdec(pd);
-  bool t_nf = false, t_empty = false, d_nf = false, d_empty = false, tok_bad = false;
+  UnitStats st;
+  st.M = 0.f;
+  st.S = 0.0;
+  st.amax = -1;
+  st.t_nf = st.t_empty = st.d_nf = st.d_empty = st.tok_bad = false;
+  st.sig = NAN;
+  st.dmx = kNegBig;
   if (P.greedy) {
     float bv = own ? recf[3] : -INFINITY;
     int64_t bi = own ? (int64_t)(int32_t)rec[2] : -1;
     warp_argmax(bv, bi);  // best value, lowest global index on ties (reading #5 / #7)
-    t_nf = (bad & 1) != 0;
-    t_empty = bi < 0;
-    pd.amax = bi;
-    pd.M = bv;
+    st.t_nf = (bad & 1) != 0;
+    st.t_empty = bi < 0;
+    st.amax = bi;
+    st.M = bv;
   } else {
     const float Mr = own ? recf[0] : kNegBig;
-    const float M = warp_max(Mr);
+    st.M = warp_max(Mr);
     const double Sr = own ? *reinterpret_cast<const double*>(rec + 4) : 0.0;
-    const double S = warp_sum(Sr != 0.0 ? Sr * exp2((double)Mr * k2 - (double)M * k2) : 0.0);
-    pd.M = M;
-    pd.S = S;
-    t_nf = !isfinite(S) || !isfinite(M);
-    t_empty = !t_nf && !(S > 0.0);
+    st.S = warp_sum(Sr != 0.0 ? Sr * exp2((double)Mr * k2 - (double)st.M * k2) : 0.0);
+    st.t_nf = !isfinite(st.S) || !isfinite(st.M);
+    st.t_empty = !st.t_nf && !(st.S > 0.0);
   }
-  double sig[kMaxN];
-  float dmax[kMaxN];
+  bool tok_bad = false;
   if (has_d) {
-    if (bad & 2) d_nf = true;
+    if (bad & 2) st.d_nf = true;
     const double* sg = reinterpret_cast<const double*>(rec + ro.sig);
     for (int n = 0; n < N; ++n) {
       const double ds = own ? sg[n] : 0.0;
@@ -226,22 +227,22 @@ __global__ void __launch_bounds__(kThreads) shard_decide_kernel(const SplitParam
         const float dmr = own ? recf[ro.dmax + n] : kNegBig;
         mx = warp_max(dmr);
         sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
-        if (!isfinite(mx)) d_nf = true;
+        if (!isfinite(mx)) st.d_nf = true;
       } else {
         sv = warp_sum(ds);
       }
-      sig[n] = sv;
-      dmax[n] = mx;
-      if (!isfinite(sv)) d_nf = true;
-      else if (!(sv > 0.0)) d_empty = true;
+      if (lane == n) { st.sig = sv; st.dmx = mx; }
+      if (!isfinite(sv)) st.d_nf = true;
+      else if (!(sv > 0.0)) st.d_empty = true;
     }
-    // the candidate gathers come from the rank that owns each token
+    // the candidate gathers come from the rank that owns each token (lane n: candidate n)
     for (int n = 0; n < N; ++n) {
       const unsigned owners = __ballot_sync(0xffffffffu, own && ((flags >> (8 + n)) & 1u));
       const int src = owners ? __ffs(owners) - 1 : -1;
-      if (lane == 0) {
-        s_tok[warp][n] = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
-        if (src < 0) {
+      if (lane == n) {
+        const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
+        s_tok[warp][n] = tk;
+        if (src < 0 || tk < 0 || (int64_t)tk >= P.Vg) {
           tok_bad = true;
         } else {
           const float* rs = reinterpret_cast<const float*>(P.rec_all + ((int64_t)src * units + unit) * P.rec_words);
@@ -251,15 +252,9 @@ __global__ void __launch_bounds__(kThreads) shard_decide_kernel(const SplitParam
       }
     }
   }
+  st.tok_bad = __any_sync(0xffffffffu, tok_bad);
   __syncwarp();
-  if (lane != 0) return;
-  if (has_d)
-    for (int n = 0; n < N; ++n)
-      if (s_tok[warp][n] < 0 || (int64_t)s_tok[warp][n] >= P.Vg) tok_bad = true;
-  decide_lane0<kLogits>(P, b, i, has_d, tok_bad, t_nf || d_nf, t_empty || d_empty, s_gx[warp], s_tok[warp], sig,
-                        dmax, pd);
-  P.pdec[unit] = pd;
-  write_pos_debug(P, b, i, has_d, pd);
+  warp_decide_core<kLogits>(P, b, i, has_d, st, s_gx[warp], s_tok[warp], &P.pdec[unit], true);
 }
 
 // ---------------- 4. the owner of t scans its crossing tile (one CTA per request) ----------------

@@ -572,109 +572,27 @@ __device__ __forceinline__ void write_pos_debug(const SplitParams& P, int b, int
   }
 }
 
-// Lane 0 of a decision warp: the position's decision from the combined row statistics (pd.M,
-// pd.S / pd.amax already set), the drafter normalisers sig / dmax and the gathered values
-// gx[m * kMaxN + n] = d_m(X_n) (m < N) and l(X_n) (m == N) (Eq. 4 fusion P:406-411, acceptance
-// P:130-131).  Shared by the single-GPU and the vocabulary-sharded decision kernels.
-template <bool kLogits>
-__device__ __forceinline__ void decide_lane0(const SplitParams& P, int b, int i, bool has_d, bool tok_bad,
-                                             bool nonfinite, bool empty, const float* gx, const int32_t* tok,
-                                             const double* sig, const float* dmax, PosDec& pd,
-                                             double* w_sample = nullptr) {
-  const int N = P.N;
-  const bool greedy = P.greedy != 0;
-  const double k2 = (double)P.k2f;
-  bool zero = false;
-  int stc = 0;
-  if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
-  else if (nonfinite) stc = COSINE_REQ_NONFINITE_INPUT;
-  else if (empty) stc = COSINE_REQ_EMPTY_ROW;
-  // q_n(x) of a gathered drafter value (PROBS: d / sigma; LOGITS: softmax at the same k2)
-  auto qval = [&](int m, double dv) {
-    return kLogits ? exp2(dv * k2 - (double)dmax[m] * k2) / sig[m] : dv / sig[m];
-  };
-  double c[kMaxN], w[kMaxN];
-  if (!stc && has_d) {
-    for (int n = 0; n < N; ++n) {
-      c[n] = qval(n, (double)gx[n * kMaxN + n]);  // c_{n,i} = q_{n,i}(X_{n,i})
-      if (c[n] == 0.0) zero = true;
-    }
-    if (zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
-  }
-  pd.status = stc;
-  if (!stc && has_d) {
-    // Eq. 4: n* = argmax_n c_n, ties -> lowest n; fused weights (reading #2)
-    int ns = 0;
-    for (int n = 1; n < N; ++n)
-      if (c[n] > c[ns]) ns = n;
-    double second = -1.0;
-    for (int n = 0; n < N; ++n)
-      if (n != ns && c[n] > second) second = c[n];
-    pd.m_fa = (N > 1) ? (float)((c[ns] - second) / c[ns]) : INFINITY;
-    if (P.weight_mode == COSINE_W_CONF) {
-      double sc = 0.0;
-      for (int n = 0; n < N; ++n) sc += c[n];
-      for (int n = 0; n < N; ++n) w[n] = c[n] / sc;
-    } else if (P.weight_mode == COSINE_W_UNIFORM) {
-      for (int n = 0; n < N; ++n) w[n] = 1.0 / (double)N;
-    } else {
-      for (int n = 0; n < N; ++n) w[n] = (n == ns) ? 1.0 : 0.0;
-    }
-    if (w_sample) {  // x* is the caller's (SAMPLE: a draw from q; cosine_fuse_drafts)
-      pd.xstar = tok[ns];
-      // n* matters for the ARGMAX token and for WINNER weights only
-      if (P.weight_mode != COSINE_W_WINNER && P.select != COSINE_SEL_ARGMAX) pd.m_fa = INFINITY;
-      for (int n = 0; n < N; ++n) {
-        w_sample[n] = w[n];
-        pd.a[n] = (float)(w[n] / sig[n]);
-        pd.dm[n] = dmax[n];
-        pd.sig[n] = (float)sig[n];
-        pd.c[n] = (float)c[n];
-        pd.w[n] = (float)w[n];
-      }
-      return;
-    }
-    pd.xstar = tok[ns];
-    if (P.weight_mode == COSINE_W_POINT) {
-      pd.qx = 1.0;
-    } else {
-      double q = 0.0;
-      for (int m = 0; m < N; ++m) q += w[m] * qval(m, (double)gx[m * kMaxN + ns]);
-      pd.qx = q;
-    }
-    pd.u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
-    if (greedy) {
-      pd.accept = ((int64_t)pd.xstar == pd.amax);
-    } else {
-      // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
-      pd.px = exp2((double)gx[N * kMaxN + ns] * k2 - (double)pd.M * k2) / pd.S;
-      pd.accept = (pd.u * pd.qx < pd.px);
-      pd.m_fa = fmin_(pd.m_fa, (float)fabs(pd.u - pd.px / pd.qx));
-    }
-    for (int n = 0; n < N; ++n) {
-      pd.a[n] = (float)(w[n] / sig[n]);
-      pd.dm[n] = dmax[n];
-      pd.sig[n] = (float)sig[n];
-      pd.c[n] = (float)c[n];
-      pd.w[n] = (float)w[n];
-    }
-  }
-}
-
-// One warp: the gathers of the drafters' own tokens (lane m * N + n: d_m(X_n), m == N: l(X_n);
-// `diag_only`: d_n(X_n) only) and the combination of unit's C chunk records (chunk r in lane r,
-// fixed-order shuffle reductions, fp64).  Results in lane 0 (pd.M / pd.S / pd.amax, sig, dmax,
-// the error flags).
-struct UnitFlags {
+// A unit's combined row statistics, in every lane of a decision warp; drafter n's values in
+// lane n (no per-drafter arrays: a lane-0 sequential decision with local arrays costs ~7 us of
+// latency per position, which dominates small batches and the decision kernels' tails).
+struct UnitStats {
+  float M;       // T > 0: row max; greedy: the best value
+  double S;      // sum 2^((l - M) k2) (0 when greedy)
+  int64_t amax;  // greedy argmax, -1 otherwise
   bool t_nf, t_empty, d_nf, d_empty, tok_bad;
+  double sig;    // lane n < N: sigma_n (PROBS: the row sum; LOGITS: sum-exp at its max)
+  float dmx;     // lane n < N: LOGITS row max (kNegBig for PROBS)
 };
+
+// One warp: the gathers of the drafters' own tokens into s_gxw / s_tokw (lane m * N + n:
+// d_m(X_n), m == N: l(X_n); `diag_only`: d_n(X_n) only) and the combination of the unit's C
+// chunk records (chunk r in lane r, fixed-order shuffle reductions, fp64).  `has_t` = false:
+// cosine_fuse_drafts units (b * k + i, no target row).
 template <typename TT, typename TQ, bool kLogits>
-__device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, int i, bool has_d, bool diag_only,
-                                                  float* s_gxw, int32_t* s_tokw, PosDec& pd, double* sig,
-                                                  float* dmax, bool has_t = true) {
+__device__ __forceinline__ UnitStats warp_combine(const SplitParams& P, int b, int i, bool has_d, bool diag_only,
+                                                  float* s_gxw, int32_t* s_tokw, bool has_t = true) {
   const int lane = threadIdx.x & 31;
   const int N = P.N, C = P.C;
-  // the unit's record index (cosine_fuse_drafts units have no target row: b * k + i)
   const int64_t unit = has_t ? (int64_t)b * (P.k + 1) + i : (int64_t)b * P.k + i;
   const bool greedy = P.greedy != 0;
   const double k2 = (double)P.k2f;
@@ -690,34 +608,37 @@ __device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, i
     s_gxw[m * kMaxN + n] = v;
     if (m == 0) s_tokw[n] = tk;
   }
-  // ---- combine the partial records (chunk r in lane r) ----
-  const PartRec* parts = P.parts + unit * C;  // L2 reads (written by other CTAs, maybe this kernel)
+  COSINE_TRACE_AT(P, 8);
+  const PartRec* parts = P.parts + unit * C;  // L2 reads (written by other CTAs)
   const bool own = lane < C;
   const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
   const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
-  init_posdec(pd);
-  UnitFlags f = {false, false, false, false, false};
+  UnitStats st;
+  st.M = 0.f;
+  st.S = 0.0;
+  st.amax = -1;
+  st.t_nf = st.t_empty = st.d_nf = st.d_empty = st.tok_bad = false;
+  st.sig = NAN;
+  st.dmx = kNegBig;
   if (!has_t) {
     // no target row (its record fields are ignored)
   } else if (greedy) {
     float bv = own ? tmax : -INFINITY;
     int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
     warp_argmax(bv, bi);
-    f.t_nf = (bad & 1) != 0;
-    f.t_empty = (bi < 0);
-    pd.amax = bi;
-    pd.M = bv;
+    st.t_nf = (bad & 1) != 0;
+    st.t_empty = (bi < 0);
+    st.amax = bi;
+    st.M = bv;
   } else {
-    const float M = warp_max(tmax);
+    st.M = warp_max(tmax);
     const double tsum = own ? __ldcg(&parts[lane].tsum) : 0.0;
-    const double S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
-    pd.M = M;
-    pd.S = S;
-    f.t_nf = !isfinite(S) || !isfinite(M);
-    f.t_empty = !f.t_nf && !(S > 0.0);
+    st.S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)st.M * k2) : 0.0);
+    st.t_nf = !isfinite(st.S) || !isfinite(st.M);
+    st.t_empty = !st.t_nf && !(st.S > 0.0);
   }
   if (has_d) {
-    if (bad & 2) f.d_nf = true;
+    st.d_nf = (bad & 2) != 0;
     for (int n = 0; n < N; ++n) {
       double sv;
       float mx = kNegBig;
@@ -726,110 +647,50 @@ __device__ __forceinline__ UnitFlags warp_combine(const SplitParams& P, int b, i
         const float dmr = own ? __ldcg(&parts[lane].dmax[n]) : kNegBig;
         mx = warp_max(dmr);
         sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
-        if (!isfinite(mx)) f.d_nf = true;
+        if (!isfinite(mx)) st.d_nf = true;
       } else {
         sv = warp_sum(ds);
       }
-      sig[n] = sv;
-      dmax[n] = mx;
-      if (!isfinite(sv)) f.d_nf = true;
-      else if (!(sv > 0.0)) f.d_empty = true;
+      if (lane == n) { st.sig = sv; st.dmx = mx; }
+      if (!isfinite(sv)) st.d_nf = true;
+      else if (!(sv > 0.0)) st.d_empty = true;
     }
   }
   __syncwarp();
-  if (lane == 0 && has_d)
-    for (int n = 0; n < N; ++n)
-      if (s_tokw[n] < 0 || (int64_t)s_tokw[n] >= P.V) f.tok_bad = true;
-  return f;
+  if (has_d) {
+    const int32_t t = lane < N ? s_tokw[lane] : 0;
+    st.tok_bad = __any_sync(0xffffffffu, lane < N && (t < 0 || (int64_t)t >= P.V));
+  }
+  COSINE_TRACE_AT(P, 9);
+  return st;
 }
 
-// One warp decides position i of request b (Eq. 4 fusion P:406-411, acceptance P:130-131) and
-// writes the decision to *out (and the diagnostics if asked), lane-parallel: lane n holds
-// drafter n's normaliser sigma_n and confidence c_n, the fusion argmax / second best / weight
-// sums are shuffle reductions, lane n writes drafter n's fields.  (The same decision as
-// decide_lane0 up to the order of the fp64 sums over drafters; a lane-0 sequential version
-// keeps its arrays in local memory and costs ~7 us of latency per position, which dominates
-// small batches.)  Ends with __syncwarp().
-template <typename TT, typename TQ, bool kLogits>
-__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
-                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
+// One warp decides position i of request b from its combined statistics (Eq. 4 fusion
+// P:406-411, acceptance P:130-131), lane-parallel: lane n holds drafter n's sigma_n and
+// confidence c_n, the fusion argmax / second best / weight sum are shuffle reductions, lane n
+// writes drafter n's fields of *out (lane 0 the scalars) and of the diagnostics.
+// `w_sample` (SAMPLE selection, cosine_fuse_drafts): stop after the weights — x* is the
+// caller's draw — and leave w_n in w_sample[n] (and sigma_n, the LOGITS row max in sig_out /
+// dmax_out).  s_gxw / s_tokw / st as warp_combine leaves them (or the sharded records).  Ends
+// with __syncwarp().
+template <bool kLogits>
+__device__ __forceinline__ void warp_decide_core(const SplitParams& P, int b, int i, bool has_d, const UnitStats& st,
+                                                 const float* s_gxw, const int32_t* s_tokw, PosDec* out,
+                                                 bool write_debug, double* w_sample = nullptr,
+                                                 double* sig_out = nullptr, float* dmax_out = nullptr) {
   const int lane = threadIdx.x & 31;
-  const bool has_d = i < g;
-  const int N = P.N, C = P.C;
+  const int N = P.N;
   const int64_t unit = (int64_t)b * (P.k + 1) + i;
   const bool greedy = P.greedy != 0;
   const double k2 = (double)P.k2f;
-  // ---- gathers: lane m * N + n loads d_m(X_n) (m < N) or l(X_n) (m == N) ----
-  const int ng = has_d ? N * (N + 1) : 0;
-  if (lane < ng) {
-    const int n = lane % N, m = lane / N;
-    const int32_t tk = P.draft_tokens[((int64_t)b * P.k + i) * N + n];
-    float v = 0.f;
-    if (tk >= 0 && (int64_t)tk < P.V) {
-      if (m < N) v = load_one((const TQ*)P.draft + (((int64_t)b * P.k + i) * N + m) * P.ld_q, tk);
-      else v = load_one((const TT*)P.target + unit * P.ld_t, tk);
-    }
-    s_gxw[m * kMaxN + n] = v;
-    if (m == 0) s_tokw[n] = tk;
-  }
-  COSINE_TRACE_AT(P, 8);
-  // ---- the unit's C chunk records (chunk r in lane r) ----
-  const PartRec* parts = P.parts + unit * C;
-  const bool own = lane < C;
-  const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
-  const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
-  float M;
-  double S = 0.0;
-  int64_t amax = -1;
-  bool t_nf, t_empty;
-  if (greedy) {
-    float bv = own ? tmax : -INFINITY;
-    int64_t bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
-    warp_argmax(bv, bi);
-    t_nf = (bad & 1) != 0;
-    t_empty = (bi < 0);
-    amax = bi;
-    M = bv;
-  } else {
-    M = warp_max(tmax);
-    const double tsum = own ? __ldcg(&parts[lane].tsum) : 0.0;
-    S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
-    t_nf = !isfinite(S) || !isfinite(M);
-    t_empty = !t_nf && !(S > 0.0);
-  }
-  // ---- drafter normalisers: sigma_n, (LOGITS) the row max, in lane n ----
-  double sig_l = NAN;
-  float dmx_l = kNegBig;
-  bool d_nf = false, d_empty = false;
-  if (has_d) {
-    d_nf = (bad & 2) != 0;
-    for (int n = 0; n < N; ++n) {
-      double sv;
-      float mx = kNegBig;
-      const double ds = own ? __ldcg(&parts[lane].dsum[n]) : 0.0;
-      if (kLogits) {
-        const float dmr = own ? __ldcg(&parts[lane].dmax[n]) : kNegBig;
-        mx = warp_max(dmr);
-        sv = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)mx * k2) : 0.0);
-        if (!isfinite(mx)) d_nf = true;
-      } else {
-        sv = warp_sum(ds);
-      }
-      if (lane == n) { sig_l = sv; dmx_l = mx; }
-      if (!isfinite(sv)) d_nf = true;
-      else if (!(sv > 0.0)) d_empty = true;
-    }
-  }
-  __syncwarp();
-  COSINE_TRACE_AT(P, 9);
   const bool dl = lane < N;  // this lane holds a drafter
-  bool tok_bad = false;
-  if (has_d) {
-    const int32_t t = dl ? s_tokw[lane] : 0;
-    tok_bad = __any_sync(0xffffffffu, dl && (t < 0 || (int64_t)t >= P.V));
-  }
-  int stc = tok_bad ? COSINE_REQ_TOKEN_OUT_OF_RANGE
-                    : ((t_nf || d_nf) ? COSINE_REQ_NONFINITE_INPUT : ((t_empty || d_empty) ? COSINE_REQ_EMPTY_ROW : 0));
+  const double sig_l = st.sig;
+  const float dmx_l = st.dmx;
+  if (dl && sig_out) sig_out[lane] = sig_l;
+  if (dl && dmax_out) dmax_out[lane] = dmx_l;
+  int stc = st.tok_bad ? COSINE_REQ_TOKEN_OUT_OF_RANGE
+                       : ((st.t_nf || st.d_nf) ? COSINE_REQ_NONFINITE_INPUT
+                                                : ((st.t_empty || st.d_empty) ? COSINE_REQ_EMPTY_ROW : 0));
   // q_n(x) of a gathered drafter value (PROBS: d / sigma; LOGITS: softmax at the same k2), lane n
   auto qval = [&](double dv) {
     return kLogits ? exp2(dv * k2 - (double)dmx_l * k2) / sig_l : dv / sig_l;
@@ -868,21 +729,27 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
       w_l = (lane == ns) ? 1.0 : 0.0;
     }
     xstar = s_tokw[ns];
-    if (P.weight_mode == COSINE_W_POINT) {
-      qx = 1.0;
+    if (w_sample) {  // x* is the caller's (SAMPLE: a draw from q; cosine_fuse_drafts)
+      // n* matters for the ARGMAX token and for WINNER weights only
+      if (P.weight_mode != COSINE_W_WINNER && P.select != COSINE_SEL_ARGMAX) m_fa = INFINITY;
+      if (dl) w_sample[lane] = w_l;
     } else {
-      qx = warp_sum(dl ? w_l * qval((double)s_gxw[lane * kMaxN + ns]) : 0.0);
-    }
-    COSINE_TRACE_AT(P, 11);
-    u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
-    COSINE_TRACE_AT(P, 12);
-    if (greedy) {
-      accept = ((int64_t)xstar == amax);
-    } else {
-      // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
-      px = exp2((double)s_gxw[N * kMaxN + ns] * k2 - (double)M * k2) / S;
-      accept = (u * qx < px);
-      m_fa = fmin_(m_fa, (float)fabs(u - px / qx));
+      if (P.weight_mode == COSINE_W_POINT) {
+        qx = 1.0;
+      } else {
+        qx = warp_sum(dl ? w_l * qval((double)s_gxw[lane * kMaxN + ns]) : 0.0);
+      }
+      COSINE_TRACE_AT(P, 11);
+      u = philox_u24(P.seed, P.rids[b], (uint32_t)(i + 1), P.step, kTagAccept);
+      COSINE_TRACE_AT(P, 12);
+      if (greedy) {
+        accept = ((int64_t)xstar == st.amax);
+      } else {
+        // acceptance u * q(x*) < o(x*), i.e. u < min(1, o/q)
+        px = exp2((double)s_gxw[N * kMaxN + ns] * k2 - (double)st.M * k2) / st.S;
+        accept = (u * qx < px);
+        m_fa = fmin_(m_fa, (float)fabs(u - px / qx));
+      }
     }
   }
   COSINE_TRACE_AT(P, 13);
@@ -899,10 +766,10 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     out->status = stc;
     out->accept = accept;
     out->xstar = xstar;
-    out->amax = amax;
+    out->amax = st.amax;
     out->m_fa = m_fa;
-    out->M = M;
-    out->S = S;
+    out->M = st.M;
+    out->S = st.S;
     out->px = px;
     out->qx = qx;
     out->u = u;
@@ -911,8 +778,8 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
     const cosine_debug_t& D = P.dbg;
     const int64_t o1 = (int64_t)b * P.k + i;
     if (lane == 0) {
-      if (D.row_max) D.row_max[unit] = M;
-      if (D.row_sumexp) D.row_sumexp[unit] = greedy ? 0.f : (float)S;
+      if (D.row_max) D.row_max[unit] = st.M;
+      if (D.row_sumexp) D.row_sumexp[unit] = greedy ? 0.f : (float)st.S;
       if (has_d) {
         if (D.p_x) D.p_x[o1] = (float)px;
         if (D.q_x) D.q_x[o1] = (float)qx;
@@ -921,14 +788,22 @@ __device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, 
       }
     }
     if (has_d && dl) {
-      const bool mine = filled;
-      if (D.draft_norm) D.draft_norm[o1 * N + lane] = mine ? (float)sig_l : NAN;
-      if (D.conf) D.conf[o1 * N + lane] = mine ? (float)c_l : NAN;
-      if (D.weights) D.weights[o1 * N + lane] = mine ? (float)w_l : NAN;
+      if (D.draft_norm) D.draft_norm[o1 * N + lane] = filled ? (float)sig_l : NAN;
+      if (D.conf) D.conf[o1 * N + lane] = filled ? (float)c_l : NAN;
+      if (D.weights) D.weights[o1 * N + lane] = filled ? (float)w_l : NAN;
     }
   }
   __syncwarp();
   COSINE_TRACE_AT(P, 14);
+}
+
+// One warp decides position i of request b (split path): warp_combine + warp_decide_core.
+template <typename TT, typename TQ, bool kLogits>
+__device__ __forceinline__ void warp_decide(const SplitParams& P, int b, int i, int g, float* s_gxw,
+                                            int32_t* s_tokw, PosDec* out, bool write_debug) {
+  const bool has_d = i < g;
+  const UnitStats st = warp_combine<TT, TQ, kLogits>(P, b, i, has_d, false, s_gxw, s_tokw);
+  warp_decide_core<kLogits>(P, b, i, has_d, st, s_gxw, s_tokw, out, write_debug);
 }
 
 // Kernel B1 (split path): one warp per (request, position) -> PosDec in global memory (+
@@ -1035,7 +910,7 @@ __device__ __forceinline__ void chunk_crossing_warp(const SplitParams& P, int64_
 // fusion; "direct ensemble sampling"): one CTA per unit, a programmatic dependent
 // of stats_kernel that waits for its unit's C chunk records.
 //  1. warp 0 combines the records (M, S, sigma) and the own-token gathers: confidences and the
-//     fusion weights w (Eq. 4 weights; decide_lane0 stopped before x*);
+//     fusion weights w (Eq. 4 weights; warp_decide_core stopped before x*);
 //  2. the chunk masses of q come free from the statistics pass: chunk r holds
 //     sum_n (w_n / sigma_n) dsum_{n,r} (rescaled to the row max for LOGITS drafts); the crossing
 //     chunk of t = u Q, u = U(rid, i+1, FUSE), is found in one warp prefix over the C chunks;
@@ -1079,17 +954,9 @@ __global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitPara
   }
   __syncthreads();
   if (tid < 32) {
-    PosDec pd;
-    double sig[kMaxN];
-    float dmax[kMaxN];
-    const UnitFlags f = warp_combine<TT, TQ, kLogits>(P, b, i, has_d, true, s_gx, s_tok, pd, sig, dmax);
-    if (lane == 0) {
-      decide_lane0<kLogits>(P, b, i, has_d, f.tok_bad, f.t_nf || f.d_nf, f.t_empty || f.d_empty, s_gx, s_tok, sig,
-                            dmax, pd, s_w);
-      s_go = (has_d && pd.status == 0) ? 1 : 0;
-      for (int n = 0; n < N; ++n) { s_sig[n] = sig[n]; s_dmax[n] = dmax[n]; }
-      s_pd = pd;
-    }
+    const UnitStats st = warp_combine<TT, TQ, kLogits>(P, b, i, has_d, true, s_gx, s_tok);
+    warp_decide_core<kLogits>(P, b, i, has_d, st, s_gx, s_tok, &s_pd, false, s_w, s_sig, s_dmax);
+    if (lane == 0) s_go = (has_d && s_pd.status == 0) ? 1 : 0;
     __syncwarp();
     if (s_go) chunk_crossing_warp<kLogits>(P, gu, (uint32_t)(i + 1), P.rids[b], s_w, s_sig, s_dmax, &s_d, &s_g0, &s_g1,
                                            &s_tc, &s_Q);
@@ -1127,10 +994,10 @@ __global__ void __launch_bounds__(kThreads) sample_decide_kernel(const SplitPara
 }
 
 // Kernel B1 for SAMPLE selection over probability drafts: one WARP per unit.  Steps 1-2 as
-// sample_decide_kernel; the crossing chunk's 64-group slice sums, written by the statistics pass
+// sample_decide_kernel; the crossing chunk's 32-group slice sums, written by the statistics pass
 // (stats_kernel<..., kSlices>), locate the slice of t in one more warp prefix (slice masses
-// sum_n (w_n / sigma_n) slice_{n,s}), and a 32-lane scan of that slice (two steps, reading #10)
-// finds x*.  Re-reads 64 groups of the N drafter rows per unit instead of half a chunk.  A t that falls in
+// sum_n (w_n / sigma_n) slice_{n,s}), and one 32-lane scan of that slice (reading #10) finds x*.
+// Re-reads 32 groups of the N drafter rows per unit instead of half a chunk.  A t that falls in
 // no slice (the row's partial last group, or rounding at the chunk end) scans the whole chunk.
 template <typename TT, typename TQ, int NMAX>
 __global__ void __launch_bounds__(kThreads) sample_decide_w_kernel(const SplitParams P) {
@@ -1164,20 +1031,10 @@ __global__ void __launch_bounds__(kThreads) sample_decide_w_kernel(const SplitPa
     }
   }
   __syncwarp();
-  PosDec pd;
-  double sig[kMaxN];
-  float dmax[kMaxN];
-  const UnitFlags f = warp_combine<TT, TQ, false>(P, b, i, has_d, true, s_gx[warp], s_tok[warp], pd, sig, dmax);
-  int go = 0;
-  if (lane == 0) {
-    decide_lane0<false>(P, b, i, has_d, f.tok_bad, f.t_nf || f.d_nf, f.t_empty || f.d_empty, s_gx[warp],
-                        s_tok[warp], sig, dmax, pd, s_w[warp]);
-    go = (has_d && pd.status == 0) ? 1 : 0;
-    for (int n = 0; n < N; ++n) { s_sig[warp][n] = sig[n]; s_dmax[warp][n] = dmax[n]; }
-    s_pd[warp] = pd;
-  }
-  go = __shfl_sync(0xffffffffu, go, 0);
-  __syncwarp();
+  const UnitStats st = warp_combine<TT, TQ, false>(P, b, i, has_d, true, s_gx[warp], s_tok[warp]);
+  warp_decide_core<false>(P, b, i, has_d, st, s_gx[warp], s_tok[warp], &s_pd[warp], false, s_w[warp], s_sig[warp],
+                          s_dmax[warp]);
+  const int go = (has_d && s_pd[warp].status == 0) ? 1 : 0;
   if (go) {
     chunk_crossing_warp<false>(P, gu, (uint32_t)(i + 1), P.rids[b], s_w[warp], s_sig[warp], s_dmax[warp],
                                &s_d[warp], &s_g0[warp], &s_g1[warp], &s_tc[warp], &s_Q[warp]);
@@ -1281,16 +1138,9 @@ __global__ void __launch_bounds__(kThreads) fuse_decide_kernel(const SplitParams
   const int N = P.N;
   const TQ* drow = (const TQ*)P.draft + unit * N * P.ld_q;
   if (tid < 32) {
-    PosDec pd;
-    double sig[kMaxN];
-    float dmax[kMaxN];
-    const UnitFlags f = warp_combine<TT, TQ, kLogits>(P, b, i, true, true, s_gx, s_tok, pd, sig, dmax, false);
-    if (lane == 0) {
-      decide_lane0<kLogits>(P, b, i, true, f.tok_bad, f.d_nf, f.d_empty, s_gx, s_tok, sig, dmax, pd, s_w);
-      s_go = (pd.status == 0 && P.select == COSINE_SEL_SAMPLE) ? 1 : 0;
-      for (int n = 0; n < N; ++n) { s_sig[n] = sig[n]; s_dmax[n] = dmax[n]; }
-      s_pd = pd;
-    }
+    const UnitStats st = warp_combine<TT, TQ, kLogits>(P, b, i, true, true, s_gx, s_tok, false);
+    warp_decide_core<kLogits>(P, b, i, true, st, s_gx, s_tok, &s_pd, false, s_w, s_sig, s_dmax);
+    if (lane == 0) s_go = (s_pd.status == 0 && P.select == COSINE_SEL_SAMPLE) ? 1 : 0;
     __syncwarp();
     if (s_go) chunk_crossing_warp<kLogits>(P, unit, (uint32_t)(i + 1), P.rids[b], s_w, s_sig, s_dmax, &s_d, &s_g0,
                                            &s_g1, &s_tc, &s_Q);
