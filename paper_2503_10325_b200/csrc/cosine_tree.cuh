@@ -38,19 +38,22 @@ struct TreeParams {
 };
 
 // ---------------- node decisions (one warp) ----------------
-// The statistics of node j's rows, combined over the whole vocabulary (valid in every lane).
+// The statistics of node j's rows, combined over the whole vocabulary (valid in every lane;
+// drafter n's sigma_n and LOGITS row max in lane n).
 struct NodeStats {
   float M;
   double S;
-  double sig[kMaxN];
-  float dmax[kMaxN];
+  double sig;  // lane n < N
+  float dmx;   // lane n < N
   bool t_nf, t_empty, d_nf, d_empty;
 };
 
 // One warp decides node j of request b from its row statistics: Eq. 4 fusion at the node
-// (reading #2) and o_j(x_c), q_j(x_c) of every child c (lane-parallel).  Lane 0 writes
-// the node record *nd_out; the child values go to gcpq[c] (global) or scp[c] / scq[c] (shared).
-// s_*: per-warp shared scratch.  Shared by tree_decide_kernel and the lazy walk.
+// (reading #2) and o_j(x_c), q_j(x_c) of every child c, lane-parallel (lane n holds
+// drafter n's sigma_n and confidence; lanes over the children).  Writes the node record *nd_out
+// (lane n: drafter n's fields, lane 0 the scalars); the child values go to gcpq[c] (global) or
+// scp[c] / scq[c] (shared).  s_*: per-warp shared scratch.  Shared by tree_decide_kernel and the
+// lazy walk.  Ends with __syncwarp().
 template <typename TT, typename TQ, bool kLogits>
 __device__ __forceinline__ void node_decide_warp(const TreeParams& T, int b, int j, int ir, bool has_d,
                                                  const TT* trow, const TQ* drow, const NodeStats& ns,
@@ -71,60 +74,55 @@ __device__ __forceinline__ void node_decide_warp(const TreeParams& T, int b, int
     if (m == 0) s_tok[n] = tk;
   }
   __syncwarp();
-  NodeDec nd;
-  nd.M = ns.M;
-  nd.S = ns.S;
-  nd.gap = INFINITY;
-  for (int n = 0; n < kMaxN; ++n) { nd.a[n] = 0.f; nd.dm[n] = 0.f; }
-  int stc = 0;
-  bool ok_for_children = false;
-  if (lane == 0) {
-    bool tok_bad = false, zero = false;
-    if (has_d)
-      for (int n = 0; n < N; ++n)
-        if (s_tok[n] < 0 || (int64_t)s_tok[n] >= P.V) tok_bad = true;
-    if (tok_bad) stc = COSINE_REQ_TOKEN_OUT_OF_RANGE;
-    else if (ns.t_nf || ns.d_nf) stc = COSINE_REQ_NONFINITE_INPUT;
-    else if (ns.t_empty || ns.d_empty) stc = COSINE_REQ_EMPTY_ROW;
-    auto qval = [&](int m, double dv) {
-      return kLogits ? exp2(dv * k2 - (double)ns.dmax[m] * k2) / ns.sig[m] : dv / ns.sig[m];
-    };
-    double c[kMaxN], w[kMaxN];
-    if (!stc && has_d) {
-      for (int n = 0; n < N; ++n) {
-        c[n] = qval(n, (double)s_gx[n * kMaxN + n]);  // c_n = q_n(X_n) at this node
-        if (c[n] == 0.0) zero = true;
-      }
-      if (zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+  const bool dl = lane < N;  // this lane holds a drafter
+  const double sig_l = ns.sig;
+  const float dmx_l = ns.dmx;
+  bool tok_bad = false;
+  if (has_d) {
+    const int32_t t = dl ? s_tok[lane] : 0;
+    tok_bad = __any_sync(0xffffffffu, dl && (t < 0 || (int64_t)t >= P.V));
+  }
+  int stc = tok_bad ? COSINE_REQ_TOKEN_OUT_OF_RANGE
+                    : ((ns.t_nf || ns.d_nf) ? COSINE_REQ_NONFINITE_INPUT
+                                            : ((ns.t_empty || ns.d_empty) ? COSINE_REQ_EMPTY_ROW : 0));
+  double c_l = 0.0;  // c_n = q_n(X_n) at this node
+  if (!stc && has_d) {
+    if (dl) {
+      const double dv = (double)s_gx[lane * kMaxN + lane];
+      c_l = kLogits ? exp2(dv * k2 - (double)dmx_l * k2) / sig_l : dv / sig_l;
     }
-    if (!stc && has_d) {  // Eq. 4 fusion weights at the node (reading #2)
-      int nsel = 0;
-      for (int n = 1; n < N; ++n)
-        if (c[n] > c[nsel]) nsel = n;
-      double second = -1.0;
-      for (int n = 0; n < N; ++n)
-        if (n != nsel && c[n] > second) second = c[n];
-      nd.gap = (N > 1) ? (float)((c[nsel] - second) / c[nsel]) : INFINITY;
-      if (P.weight_mode == COSINE_W_CONF) {
-        double sc = 0.0;
-        for (int n = 0; n < N; ++n) sc += c[n];
-        for (int n = 0; n < N; ++n) w[n] = c[n] / sc;
-      } else if (P.weight_mode == COSINE_W_UNIFORM) {
-        for (int n = 0; n < N; ++n) w[n] = 1.0 / (double)N;
-      } else {
-        for (int n = 0; n < N; ++n) w[n] = (n == nsel) ? 1.0 : 0.0;
-      }
-      for (int n = 0; n < N; ++n) {
-        nd.a[n] = (float)(w[n] / ns.sig[n]);
-        nd.dm[n] = ns.dmax[n];
-        s_w[n] = w[n];
-        s_sig[n] = ns.sig[n];
-        s_dmax[n] = ns.dmax[n];
-      }
-      ok_for_children = true;
+    if (__any_sync(0xffffffffu, dl && c_l == 0.0)) stc = COSINE_REQ_ZERO_PROB_DRAFT;
+  }
+  const bool ok_for_children = !stc && has_d;
+  float gap = INFINITY;
+  double w_l = 0.0;
+  if (ok_for_children) {  // Eq. 4 fusion weights at the node (reading #2)
+    double bc = dl ? c_l : -1.0;
+    int bn = dl ? lane : 1 << 30;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const int on = __shfl_xor_sync(0xffffffffu, bn, o);
+      if (oc > bc || (oc == bc && on < bn)) { bc = oc; bn = on; }
+    }
+    double second = (dl && lane != bn) ? c_l : -1.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) second = fmax(second, __shfl_xor_sync(0xffffffffu, second, o));
+    gap = (N > 1) ? (float)((bc - second) / bc) : INFINITY;
+    if (P.weight_mode == COSINE_W_CONF) {
+      const double sc = warp_sum(dl ? c_l : 0.0);
+      w_l = dl ? c_l / sc : 0.0;
+    } else if (P.weight_mode == COSINE_W_UNIFORM) {
+      w_l = dl ? 1.0 / (double)N : 0.0;
+    } else {
+      w_l = (lane == bn) ? 1.0 : 0.0;
+    }
+    if (dl) {
+      s_w[lane] = w_l;
+      s_sig[lane] = sig_l;
+      s_dmax[lane] = dmx_l;
     }
   }
-  ok_for_children = __shfl_sync(0xffffffffu, ok_for_children, 0);
   __syncwarp();
   // o_j(x_c), q_j(x_c) of every child c of j (lane-parallel over candidate node ids)
   for (int c = j + 1 + lane; c < nn; c += 32) {
@@ -151,11 +149,19 @@ __device__ __forceinline__ void node_decide_warp(const TreeParams& T, int b, int
     }
   }
   __syncwarp();
+  if (lane < kMaxN) {
+    const bool mine = ok_for_children && dl;
+    nd_out->a[lane] = mine ? (float)(w_l / sig_l) : 0.f;
+    nd_out->dm[lane] = mine ? dmx_l : 0.f;
+  }
   if (lane == 0) {
     if (!stc && *s_zero) stc = COSINE_REQ_ZERO_PROB_DRAFT;
-    nd.status = stc;
-    *nd_out = nd;
+    nd_out->status = stc;
+    nd_out->M = ns.M;
+    nd_out->S = ns.S;
+    nd_out->gap = gap;
   }
+  __syncwarp();
 }
 
 // ---------------- kernel T1: one warp per node ----------------
@@ -184,6 +190,8 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
   const float tmax = own ? parts[lane].tmax : kNegBig;
   const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
   NodeStats ns;
+  ns.sig = NAN;
+  ns.dmx = kNegBig;
   ns.M = warp_max(tmax);
   const double tsum = own ? parts[lane].tsum : 0.0;
   ns.S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)ns.M * k2) : 0.0);
@@ -205,8 +213,7 @@ __global__ void __launch_bounds__(kThreads) tree_decide_kernel(const TreeParams 
       } else {
         sv = warp_sum(ds);
       }
-      ns.sig[n] = sv;
-      ns.dmax[n] = mx;
+      if (lane == n) { ns.sig = sv; ns.dmx = mx; }
       if (!isfinite(sv)) ns.d_nf = true;
       else if (!(sv > 0.0)) ns.d_empty = true;
     }
@@ -459,6 +466,8 @@ __device__ __forceinline__ void tree_node_stats(
   __syncthreads();
   if (warp == 0) {
     NodeStats ns;
+    ns.sig = NAN;
+    ns.dmx = kNegBig;
     float M = kNegBig;
     double S = 0.0;
     int bad = 0;
@@ -485,8 +494,7 @@ __device__ __forceinline__ void tree_node_stats(
         if (!isfinite(sv)) ns.d_nf = true;
         else if (!(sv > 0.0)) ns.d_empty = true;
       }
-      ns.sig[n] = sv;
-      ns.dmax[n] = mx;
+      if (lane == n) { ns.sig = sv; ns.dmx = mx; }
     }
     node_decide_warp<TT, TQ, kLogits>(T, b, j, ir, Nd > 0, trow, drow, ns, s_ngx, s_ntok, s_nw, s_nsig, s_ndmax,
                                       s_nzero, s_nd, nullptr, s_cp, s_cq);
