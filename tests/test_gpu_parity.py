@@ -196,3 +196,18 @@ def test_gpu_output_distribution_chi_square(cuda_ok):
     p = torch.softmax(base["target"][0, 0, :V].double(), -1).numpy()
     counts = np.bincount(g["out_tokens"][:, 0], minlength=V)
     assert scipy.stats.chisquare(counts, p * n).pvalue > 1e-4
+
+
+@pytest.mark.parametrize("B,k,N,V,dtype", [(1, 4, 2, 32000, torch.float32), (64, 8, 3, 32000, torch.bfloat16),
+                                           (7, 5, 4, 20011, torch.bfloat16)])
+def test_one_launch_small_batch_path(cuda_ok, B, k, N, V, dtype):
+    # small batches run as ONE cooperative launch (tiny_kernel); a fixed chunk count forces the
+    # three-launch split path.  Both against the oracle; identical outputs where nothing is flagged
+    inp = synth.linear_inputs(B, k, N, V, dtype=dtype, seed=B * 31 + k, draft_len="random")
+    g1, r, _ = _run(inp, name=f"one-launch B={B}")
+    assert g1["launches"] == 1
+    g3 = parity.gpu_verify(inp, cluster_size=4)
+    assert g3["launches"] == 3
+    ok = r["tie_margin"] >= parity.TIE
+    np.testing.assert_array_equal(g1["accept_len"][ok], g3["accept_len"][ok])
+    np.testing.assert_array_equal(g1["out_tokens"][ok], g3["out_tokens"][ok])
