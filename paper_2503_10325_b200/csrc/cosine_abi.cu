@@ -1208,6 +1208,9 @@ static cosine_status_t verify_tree_impl(bool lazy, cosine_ctx_t ctx, cosine_stre
     }
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(ks.tree_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.dynamicSmemBytes);
+#ifdef COSINE_TRACE
+    T.S.trace = cosine_trace_buffer((size_t)B * 16);
+#endif
     if (e == cudaSuccess) e = cudaLaunchKernelEx(&lc, ks.tree_walk, T);
   }
   if (e != cudaSuccess) {

@@ -235,10 +235,15 @@ constexpr int kTreeThreads = kTreeWarps * 32;       // consumer threads
 constexpr int kTreeBlock = kTreeThreads + 32;       // + the producer warp
 constexpr int kTreeMaxRej = 64;
 constexpr int kTreeMaxNodes = 1024;  // nodes per tree (the walk stages the tree in shared memory)
-constexpr int kTreeStages = 4;
+// Ring geometry (measured on c4 with the latency trace, tools/tiny_trace.py walk): a pass is
+// bound by the per-tile hand-over (consumer ~0.7 us per tile whatever its size) and the TMA
+// turnaround under load (~2.9 us), so few large stages win: 2 x 80 KB tiles 27 us per pass
+// (c4 1.405 ms, lazy 0.320 ms) vs 4 x 40 KB 29.5 us (1.423 / 0.350 ms), 8 x 20 KB 46 us,
+// 3 x 60 KB (1.405 / 0.350 ms).
+constexpr int kTreeStages = 2;
 
 // Tile geometry: one tile = kTG groups of every row of the node; a row's slice is <= kRowB bytes.
-__host__ __device__ constexpr int tree_row_bytes(int nmax) { return nmax <= 4 ? 8192 : 4096; }
+__host__ __device__ constexpr int tree_row_bytes(int nmax) { return nmax <= 4 ? 16384 : 8192; }
 __host__ __device__ constexpr int tree_tile_groups(int nmax, int esize_max) {
   return tree_row_bytes(nmax) / (kGroup * esize_max);
 }
@@ -601,7 +606,32 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
   }
   const int64_t ntile = (P.ngroups + kTG - 1) / kTG;
   uint32_t it = 0;  // tiles consumed so far (ring position and mbarrier phase), uniform
+#ifdef COSINE_TRACE  // thread 0: time in the walk logic and in each kind of block step
+  unsigned long long tr_prev = 0, tr_acc[5] = {0, 0, 0, 0, 0}, tr_cnt[5] = {0, 0, 0, 0, 0};
+  int tr_act = -1;
+  auto tr_now = []() { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); return t_; };
+  if (tid == 0) {
+    tr_prev = tr_now();
+    if (P.trace) P.trace[(size_t)blockIdx.x * 16 + 0] = tr_prev;
+  }
+  auto tr_flush = [&]() {
+    if (tid == 0 && P.trace) {
+      const unsigned long long t = tr_now();
+      if (tr_act >= 0) tr_acc[tr_act] += t - tr_prev;
+      unsigned long long* o = P.trace + (size_t)blockIdx.x * 16;
+      o[1] = t;
+      for (int q = 0; q < 5; ++q) { o[2 + q] = tr_acc[q]; o[7 + q] = tr_cnt[q]; }
+    }
+  };
+#endif
   for (;;) {
+#ifdef COSINE_TRACE
+    if (tid == 0) {  // the previous step's block work ends here
+      const unsigned long long t = tr_now();
+      if (tr_act >= 0) tr_acc[tr_act] += t - tr_prev;
+      tr_prev = t;
+    }
+#endif
     if (tid == 0) {
       // advance the walk until the block is needed for a pass (act 1) or the final draw (act 2)
       int act = -1;
@@ -655,6 +685,15 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
         st.qsc[st.r] = (qv < 1.0) ? (float)(1.0 / (1.0 - qv)) : 1.f;
         act = 1;
       }
+#ifdef COSINE_TRACE
+      {
+        const unsigned long long t = tr_now();
+        tr_acc[0] += t - tr_prev;  // slot 0 of the sums: the walk logic
+        tr_prev = t;
+        tr_act = act;
+        tr_cnt[act]++;
+      }
+#endif
       s_act = act;
       s_node = j;
       s_err = err;
@@ -666,6 +705,9 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
     const TT* trow = (const TT*)P.target + ((int64_t)b * nn + jn) * P.ld_t;
     const TQ* drow = (const TQ*)P.draft + ((int64_t)b * P.I + (Nd ? irw[jn] : 0)) * N * P.ld_q;
     if (act == 4) {  // lazy: a visited node's data error (reading #23)
+#ifdef COSINE_TRACE
+      tr_flush();
+#endif
       for (int c = tid; c < nn; c += kTreeBlock) { out[c] = -1; acc[c] = -1; }
       if (tid == 0) { P.accept_len[b] = -1; P.status[b] = s_err; }
       return;
@@ -771,7 +813,8 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
     if (s_tstar >= 0 && producer) {
       if (lane == 0) ring.fill(it, s_tstar, P, trow, drow, Nd);
       ++it;
-    } else if (s_tstar >= 0) {  // the crossing tile, one group per thread: block scan of group masses
+    } else if (s_tstar >= 0) {  // the crossing tile: thread t holds kGPT consecutive groups; block scan
+      constexpr int kGPT = (kTG + kTreeThreads - 1) / kTreeThreads;
       const int stg = (int)(it % kTreeStages);
       mbar_wait_parity(&s_full[stg], (it / kTreeStages) & 1u);
       ++it;
@@ -779,16 +822,20 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
       const int64_t g0 = s_tstar * kTG;
       const int tg = (int)min((int64_t)kTG, P.ngroups - g0);
       const double tc = s_tc;
-      float w[8];
       double s = 0.0;
-      const bool have = tid < tg;
-      const int vb = (int)((g0 + tid) * kGroup);
-      if (have) {
-        tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, tid, vb, (int)P.V, w);
-        s = (double)sum8(w);
-      } else {
+      int last = -1;  // the last positive entry of this thread's groups (rounding fallback)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) w[e] = 0.f;
+      for (int q = 0; q < kGPT; ++q) {
+        const int gl = tid * kGPT + q;
+        if (gl < tg) {
+          float w[8];
+          const int vb = (int)((g0 + gl) * kGroup);
+          tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, gl, vb, (int)P.V, w);
+          s += (double)sum8(w);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (w[e] > 0.f) last = vb + e;
+        }
       }
       double incl = s;
 #pragma unroll
@@ -797,10 +844,6 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
         if (lane >= o) incl += nb;
       }
       if (lane == 31) s_ws[warp] = incl;
-      int last = -1;  // the last positive entry of this thread's group (rounding fallback)
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (w[e] > 0.f) last = vb + e;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
       if (lane == 0) s_last[warp] = last;
@@ -809,19 +852,25 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
       for (int w2 = 0; w2 < warp; ++w2) base += s_ws[w2];
       const double excl_w = __shfl_up_sync(0xffffffffu, incl, 1);
       const double lo = base + (lane == 0 ? 0.0 : excl_w), hi = base + incl;
-      if (have && s > 0.0 && lo <= tc && tc < hi) {
+      if (s > 0.0 && lo <= tc && tc < hi) {  // this thread's groups hold t: walk them in order
         double cum = lo;
-        int ef = -1;
+        int y = -1, lastpos = -1;
         float mg = 0.f;
-        for (int e = 0; e < 8; ++e) {
-          const double prev = cum;
-          cum += (double)w[e];
-          if (cum > tc) { ef = e; mg = (float)(fmin(tc - prev, cum - tc) / s_Z); break; }
+        for (int q = 0; q < kGPT && y < 0; ++q) {
+          const int gl = tid * kGPT + q;
+          if (gl >= tg) break;
+          float w[8];
+          const int vb = (int)((g0 + gl) * kGroup);
+          tree_weights_s<TT, TQ, kLogits, NMAX>(st, mode, rr, sb, Nd, gl, vb, (int)P.V, w);
+          for (int e = 0; e < 8; ++e) {
+            const double prev = cum;
+            cum += (double)w[e];
+            if (w[e] > 0.f) lastpos = vb + e;
+            if (cum > tc) { y = vb + e; mg = (float)(fmin(tc - prev, cum - tc) / s_Z); break; }
+          }
         }
-        if (ef < 0)
-          for (int e = 7; e >= 0; --e)
-            if (w[e] > 0.f) { ef = e; break; }
-        s_y = vb + ef;
+        if (y < 0) { y = lastpos; mg = 0.f; }
+        s_y = y;
         s_margin = mg;
       }
       consumer_sync();
@@ -843,6 +892,9 @@ __global__ void __launch_bounds__(kTreeBlock, 1) tree_walk_kernel(const TreePara
                     (s_y < 0 ? 0xff : 0);
       if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
     }
+#ifdef COSINE_TRACE
+    tr_flush();
+#endif
     return;
   }
 }

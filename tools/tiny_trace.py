@@ -136,7 +136,55 @@ def run_split(cfg, select=0):
                 print(f"  {gname:8s} {sname:15s} " + "  ".join(f"{x:7.1f}" for x in a) + "   (min p10 p50 p90 max, us)")
 
 
+def run_walk(cfg="c4", lazy=False):
+    """The tree walk: per request CTA, time in the walk logic and in each kind of block step."""
+    sys.path.insert(0, os.path.join(TR, "pkg"))
+    sys.path.insert(1, ROOT)
+    import numpy as np
+    import torch
+    import paper_2503_10325_b200 as cv
+    import synth
+    lib = ctypes.CDLL(os.path.join(PKGDST, "libcosine_verify.so"))
+    lib.cosine_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    lib.cosine_trace_read.restype = ctypes.c_size_t
+    c = synth.CONFIGS[cfg]
+    B, N, V, dt = c["B"], c["N"], c["V"], c["dtype"]
+    t = synth.tree_inputs(B, N, V, dtype=dt, seed=3, device="cuda")
+    nn = t["J"] + 1
+    ctx = cv.cosine_verify_init(V, device=0, max_batch=B, max_draft_len=1, max_drafters=N, seed=1,
+                                target_dtype=dt, draft_dtype=dt, max_tree_nodes=nn)
+    al = torch.empty(B, dtype=torch.int32, device="cuda")
+    an = torch.empty(B, nn, dtype=torch.int32, device="cuda")
+    ot = torch.empty(B, nn, dtype=torch.int32, device="cuda")
+    st = torch.empty(B, dtype=torch.int32, device="cuda")
+    res = []
+    for it in range(5):
+        cv.cosine_verify_tree(ctx, t["parent"], t["node_token"], t["internal_row"], t["target"], t["draft"],
+                              t["node_draft_tokens"], t["request_ids"], al, an, ot, st, temperature=1.0, lazy=lazy)
+        torch.cuda.synchronize()
+        buf = np.zeros(B * 16, dtype=np.uint64)
+        lib.cosine_trace_read(buf.ctypes.data, buf.size)
+        if it >= 2:
+            res.append(buf.reshape(B, 16).astype(np.int64))
+    r = res[-1]
+    t0 = r[:, 0].min()
+    span = (r[:, 1] - r[:, 0]) / 1e3
+    names = ["logic", "pass", "final", "stats", "error"]
+    print(f"{cfg} walk ({'lazy' if lazy else 'all nodes'}): {B} CTAs; start spread {(r[:, 0].max() - t0) / 1e3:.1f} us; "
+          f"end max {(r[:, 1].max() - t0) / 1e3:.1f} us")
+    print(f"  per CTA span: median {np.median(span):.1f} max {span.max():.1f} us")
+    order = np.argsort(-span)
+    for q, nm in enumerate(names):
+        acc = r[:, 2 + q] / 1e3
+        cnt = r[:, 7 + q]
+        print(f"  {nm:6s}: median {np.median(acc):7.1f} us  (slowest CTA {acc[order[0]]:7.1f} us, "
+              f"count median {np.median(cnt):.0f}, slowest {cnt[order[0]]})")
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "walk":
+        run_walk(sys.argv[2] if len(sys.argv) > 2 else "c4", "lazy" in sys.argv)
+        raise SystemExit
     if sys.argv[1] == "split":
         run_split(sys.argv[2] if len(sys.argv) > 2 else "c3", int(sys.argv[3]) if len(sys.argv) > 3 else 0)
         raise SystemExit
