@@ -353,6 +353,7 @@ void shard_setup(cosine_ctx_t ctx, SplitParams& S) {
   const int64_t units = (int64_t)S.B * (S.k + 1);
   fill_scratch(ctx, S, stats_chunks(ctx, units, S.ngroups));
   S.fused = 0;
+  S.ucount = 1;  // shard_pack_kernel waits per unit (scheduled into the statistics' tail)
   S.shard = 1;
   S.G = ctx->cfg.nranks;
   S.rank = ctx->cfg.rank;
@@ -424,7 +425,7 @@ cudaError_t shard_phase_c(cudaStream_t s, const SplitParams& S, const KernelSet&
 cudaError_t shard_phase_d(cudaStream_t s, const SplitParams& S, const char** stage) {
   ShardLaunch L(s);
   *stage = "finish";
-  return L(shard_finish_kernel, (unsigned)((S.B + kThreads - 1) / kThreads), S.p2p != 0, S);
+  return L(shard_finish_kernel, (unsigned)((S.B + kWarps - 1) / kWarps), S.p2p != 0, S);
 }
 size_t shard_x_bytes(const SplitParams& S, int x) {  // bytes one rank contributes to exchange x
   if (x == 1) return (size_t)S.B * (S.k + 1) * S.rec_words * 4;

@@ -100,18 +100,18 @@ __device__ __forceinline__ void shard_pack_unit(const SplitParams& P, int64_t un
   // combine this rank's chunk records (chunk r in lane r), as warp_decide does
   const PartRec* parts = P.parts + unit * C;
   const bool own = lane < C;
-  const float tmax = own ? parts[lane].tmax : kNegBig;
-  const int bad = __reduce_or_sync(0xffffffffu, own ? parts[lane].bad : 0);
+  const float tmax = own ? __ldcg(&parts[lane].tmax) : kNegBig;
+  const int bad = __reduce_or_sync(0xffffffffu, own ? __ldcg(&parts[lane].bad) : 0);
   float M = kNegBig, bv = -INFINITY;
   double S = 0.0;
   int64_t bi = -1;
   if (P.greedy) {
     bv = own ? tmax : -INFINITY;
-    bi = own ? parts[lane].targ : -1;
+    bi = own ? (int64_t)__ldcg((const long long*)&parts[lane].targ) : -1;
     warp_argmax(bv, bi);
   } else {
     M = warp_max(tmax);
-    const double tsum = own ? parts[lane].tsum : 0.0;
+    const double tsum = own ? __ldcg(&parts[lane].tsum) : 0.0;
     S = warp_sum(tsum != 0.0 ? tsum * exp2((double)tmax * k2 - (double)M * k2) : 0.0);
   }
   double sig[kMaxN];
@@ -120,9 +120,9 @@ __device__ __forceinline__ void shard_pack_unit(const SplitParams& P, int64_t un
     sig[n] = 0.0;
     dmx[n] = kNegBig;
     if (!has_d) continue;
-    const double ds = own ? parts[lane].dsum[n] : 0.0;
+    const double ds = own ? __ldcg(&parts[lane].dsum[n]) : 0.0;
     if (kLogits) {
-      const float dmr = own ? parts[lane].dmax[n] : kNegBig;
+      const float dmr = own ? __ldcg(&parts[lane].dmax[n]) : kNegBig;
       dmx[n] = warp_max(dmr);
       sig[n] = warp_sum(ds != 0.0 ? ds * exp2((double)dmr * k2 - (double)dmx[n] * k2) : 0.0);
     } else {
@@ -156,11 +156,25 @@ template <typename TT, typename TQ, bool kLogits>
 __global__ void __launch_bounds__(kThreads) shard_pack_kernel(const SplitParams P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t unit = (int64_t)blockIdx.x * kWarps + warp;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // stats_kernel's partial records (PDL)
+  if (!P.ucount) asm volatile("griddepcontrol.wait;" ::: "memory");  // stats_kernel's records (PDL)
   const int b = (int)(unit / (P.k + 1)), i = (int)(unit % (P.k + 1));
   const bool valid = unit < (int64_t)P.B * (P.k + 1);
   const int g = valid ? (P.draft_len ? P.draft_len[b] : P.k) : 0;
-  if (valid && g >= 1 && g <= P.k && i <= g) shard_pack_unit<TT, TQ, kLogits>(P, unit, b, i, g);
+  if (valid && g >= 1 && g <= P.k && i <= g) {
+    if (P.ucount) {  // this unit's C chunk records (every stats CTA is resident or done by now)
+      if (lane == 0) {
+        uint32_t n;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(n) : "l"(P.ucnt + unit) : "memory");
+          if ((int)n >= P.C) break;
+          __nanosleep(100);
+        }
+        P.ucnt[unit] = 0;  // ready for the next call (nothing else reads it)
+      }
+      __syncwarp();
+    }
+    shard_pack_unit<TT, TQ, kLogits>(P, unit, b, i, g);
+  }
   if (P.p2p) {  // every rank's copy of this CTA's records, then one arrival per CTA on every rank
     __syncthreads();
     if (threadIdx.x == 0) p2p_arrive(P, 0);
@@ -397,48 +411,61 @@ __global__ void __launch_bounds__(kThreads) shard_sample_kernel(const SplitParam
 
 // ---------------- 5. the replicated outputs (one thread per request) ----------------
 __global__ void __launch_bounds__(kThreads) shard_finish_kernel(const SplitParams P) {
+  // one warp per request: lanes over its positions (a thread per request walked them serially)
   if (P.p2p) {  // every rank's token has arrived
     if (threadIdx.x == 0) p2p_wait(P, 2);
     __syncthreads();
   }
-  const int b = blockIdx.x * kThreads + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (b >= P.B) return;
   const int g = P.draft_len ? P.draft_len[b] : P.k;
   int32_t* out = P.out_tokens + (int64_t)b * (P.k + 1);
   if (g < 1 || g > P.k) {
-    P.accept_len[b] = -1;
-    for (int j = 0; j <= P.k; ++j) out[j] = -1;
-    P.status[b] = COSINE_REQ_BAD_DRAFT_LEN;
+    for (int j = lane; j <= P.k; j += 32) out[j] = -1;
+    if (lane == 0) {
+      P.accept_len[b] = -1;
+      P.status[b] = COSINE_REQ_BAD_DRAFT_LEN;
+    }
     return;
   }
   const PosDec* pds = P.pdec + (int64_t)b * (P.k + 1);
-  const ReqView v = request_view(P, pds, g);
+  const ReqView v = request_view_warp(P, pds, g);
   if (!v.sample) {
-    for (int j = 0; j <= P.k; ++j)
+    for (int j = lane; j <= P.k; j += 32)
       out[j] = v.err ? -1 : ((j < v.L) ? pds[j].xstar : (j == v.L ? (int32_t)pds[v.L].amax : -1));
-    P.accept_len[b] = v.err ? -1 : v.L;
-    P.status[b] = v.err ? v.err : ((v.tm < 1e-6f) ? COSINE_INFO_NEAR_TIE : 0);
-    if (!v.err && P.dbg.tie_margin) P.dbg.tie_margin[b] = v.tm;
+    if (lane == 0) {
+      P.accept_len[b] = v.err ? -1 : v.L;
+      P.status[b] = v.err ? v.err : ((v.tm < 1e-6f) ? COSINE_INFO_NEAR_TIE : 0);
+      if (!v.err && P.dbg.tie_margin) P.dbg.tie_margin[b] = v.tm;
+    }
     return;
   }
+  // the owner's token: the first rank (in rank order) with y >= 0; rank 0's deg / z otherwise
+  YRec mine;
+  mine.y = -1;
+  mine.margin = 0.f;
+  mine.deg = 0;
+  mine.z = 0.f;
+  if (lane < P.G) mine = P.yall[(int64_t)lane * P.B + b];
+  const unsigned has = __ballot_sync(0xffffffffu, lane < P.G && mine.y >= 0);
+  const int src = has ? __ffs(has) - 1 : 0;
   YRec yr;
-  yr.y = -1;
-  yr.margin = 0.f;
-  yr.deg = 0;
-  yr.z = 0.f;
-  for (int r = 0; r < P.G; ++r) {
-    const YRec o = P.yall[(int64_t)r * P.B + b];
-    if (r == 0) { yr.deg = o.deg; yr.z = o.z; }
-    if (o.y >= 0) { yr = o; break; }
+  yr.y = __shfl_sync(0xffffffffu, mine.y, src);
+  yr.margin = __shfl_sync(0xffffffffu, mine.margin, src);
+  yr.deg = __shfl_sync(0xffffffffu, mine.deg, src);
+  yr.z = __shfl_sync(0xffffffffu, mine.z, src);
+  if (!has) yr.y = -1, yr.margin = 0.f;
+  for (int j = lane; j <= P.k; j += 32) out[j] = (j < v.L) ? pds[j].xstar : (j == v.L ? yr.y : -1);
+  if (lane == 0) {
+    P.accept_len[b] = v.L;
+    const float tm = fmin_(v.tm, yr.margin);
+    P.status[b] = (yr.deg ? COSINE_INFO_DEGENERATE_RESIDUAL : 0) | (tm < 1e-6f ? COSINE_INFO_NEAR_TIE : 0) |
+                  (yr.y < 0 ? 0xff : 0);
+    const bool bonus = !yr.deg && v.L == v.g;
+    if (P.dbg.residual_mass) P.dbg.residual_mass[b] = bonus ? (float)((double)yr.z / pds[v.L].S) : yr.z;
+    if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
   }
-  for (int j = 0; j <= P.k; ++j) out[j] = (j < v.L) ? pds[j].xstar : (j == v.L ? yr.y : -1);
-  P.accept_len[b] = v.L;
-  const float tm = fmin_(v.tm, yr.margin);
-  P.status[b] = (yr.deg ? COSINE_INFO_DEGENERATE_RESIDUAL : 0) | (tm < 1e-6f ? COSINE_INFO_NEAR_TIE : 0) |
-                (yr.y < 0 ? 0xff : 0);
-  const bool bonus = !yr.deg && v.L == v.g;
-  if (P.dbg.residual_mass) P.dbg.residual_mass[b] = bonus ? (float)((double)yr.z / pds[v.L].S) : yr.z;
-  if (P.dbg.tie_margin) P.dbg.tie_margin[b] = tm;
 }
 
 #endif

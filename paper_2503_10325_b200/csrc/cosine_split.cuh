@@ -93,6 +93,7 @@ struct SplitParams {
   // dependents scheduled into the previous kernel's tail wave; B1 waits for its unit's C chunk
   // records, B2 for its request's g + 1 decisions, instead of for the whole previous grid
   int fused;
+  int ucount;         // stats_kernel counts each chunk on ucnt (fused split path; sharded records)
   int32_t* ucnt;      // [B][k+1] chunk CTAs of a unit done (kernel A), reset by kernel B1
   int32_t* dcnt;      // [B] units of a request decided (kernel B1), reset by the request's last B2 CTA
   // lazy verification (NEXT-1, cosine_verify_batch_lazy): lazy = r + 1 in round r, which
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX>()))
   COSINE_TRACE_AT(P, 0);
   const int64_t gu =
       stats_body<TT, TQ, kLogits, NMAX, kSlices>(P, blockIdx.x / P.C, (int)(blockIdx.x % P.C));
-  if (P.fused && gu >= 0) {  // count this chunk for the unit (kernel B1 waits per unit, not per grid)
+  if ((P.fused || P.ucount) && gu >= 0) {  // count this chunk for the unit (the next kernel waits per unit)
     __syncthreads();
     COSINE_TRACE_AT(P, 1);
     if (threadIdx.x == 0) red_release_add(&P.ucnt[gu], 1);  // the record before the count
@@ -1373,6 +1374,34 @@ __device__ __forceinline__ ReqView request_view(const SplitParams& P, const PosD
   for (int j = 0; j < g; ++j)
     if (!pds[j].accept) { v.L = j; break; }
   for (int j = 0; j <= v.L; ++j) v.tm = fmin_(v.tm, pds[j].m_fa);
+  v.sample = (!v.err && !P.greedy) ? 1 : 0;
+  return v;
+}
+
+// The same view computed by one warp from global memory (lanes over positions; every lane
+// returns it): the first error, the first rejection L, the smallest margin on positions <= L.
+__device__ __forceinline__ ReqView request_view_warp(const SplitParams& P, const PosDec* pds, int g) {
+  const int lane = threadIdx.x & 31;
+  ReqView v;
+  v.g = g;
+  v.err = 0;
+  v.L = g;
+  v.tm = INFINITY;
+  for (int j0 = 0; j0 <= g; j0 += 32) {
+    const int j = j0 + lane;
+    const bool in = j <= g;
+    const int st = in ? pds[j].status : 0;
+    const int acc = in ? pds[j].accept : 1;
+    const unsigned e = __ballot_sync(0xffffffffu, st != 0);
+    if (!v.err && e) v.err = __shfl_sync(0xffffffffu, st, __ffs(e) - 1);
+    const unsigned r = __ballot_sync(0xffffffffu, j < g && !acc);
+    if (v.L == g && r) v.L = j0 + __ffs(r) - 1;
+  }
+  float tm = INFINITY;
+  for (int j = lane; j <= v.L; j += 32) tm = fmin_(tm, pds[j].m_fa);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tm = fmin_(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+  v.tm = tm;
   v.sample = (!v.err && !P.greedy) ? 1 : 0;
   return v;
 }
