@@ -206,9 +206,12 @@ cosine_status_t cosine_fuse_drafts(cosine_ctx_t ctx, cosine_stream_t stream, int
  *   x*_{L-1}, y, then -1; status [B].  debug may be NULL.
  * Rows after gamma_b are never read.  All rows 0..gamma_b are read and validated.
  * One GPU: three launches on `stream` — the row statistics (every input byte read once), the
- * decisions (ARGMAX: a warp per position; SAMPLE: a CTA per position that draws x* ~ q from the
- * crossing chunk found in the statistics' chunk records, reading #26) and the final draws (the
- * rows at L re-read once) — the latter two as programmatic dependents waiting on device counters.
+ * decisions (a warp per position; SAMPLE over probability drafts draws x* ~ q from the chunk
+ * records and the 32-group slice sums the statistics keep, reading #26; over logit drafts a CTA
+ * per position scans the crossing chunk) and the final draws (the rows at L re-read once) — the
+ * latter two as programmatic dependents waiting on device counters.  When the batch's (position,
+ * chunk) grid fits one wave (small batches, ARGMAX), the three steps run as ONE cooperative
+ * launch instead (cosine_last_launch_count reports 1).
  */
 cosine_status_t cosine_verify_batch(cosine_ctx_t ctx, cosine_stream_t stream, int32_t B, int32_t k,
                                     int32_t N, const void* target_logits, int64_t ld_t,
