@@ -98,7 +98,8 @@ typedef struct {
   const void* nccl_unique_id; /* nranks > 1: COSINE_NCCL_UNIQUE_ID_BYTES from rank 0's        */
                            /* cosine_nccl_unique_id(), identical on every rank (the caller    */
                            /* broadcasts it); the context owns the NCCL communicator          */
-  int32_t cluster_size;    /* 0 = automatic; else 1, 2, 4 or 8 CTAs per (request, position)  */
+  int32_t cluster_size;    /* 0 = automatic; else 1, 2, 4, 8 or 16 CTAs per (request,        */
+                           /* position) of the statistics pass (fixed: no one-launch path)    */
   int32_t exchange;        /* sharded contexts: 0 = in-kernel peer writes when every rank can  */
                            /* map the others' memory, else NCCL; 1 = NCCL all-gathers only    */
 } cosine_config_t;
