@@ -238,9 +238,10 @@ __device__ __forceinline__ float warp_sums_scatter(const float (&v)[K]) {
 
 // Resident CTAs per SM of the streaming kernels: register-lean (40 registers) for bf16 with
 // N <= 4, so that 48 warps of 128-bit loads are in flight per SM.
-template <typename TT, typename TQ, int NMAX>
+template <typename TT, typename TQ, int NMAX, bool kLogits = false>
 constexpr int stats_occupancy() {
-  return (NMAX <= 4 && sizeof(TT) == 2 && sizeof(TQ) == 2) ? 6 : 4;
+  // logit drafter rows keep a running max per drafter and are ex2-bound: 48 registers, 5 CTAs
+  return (NMAX <= 4 && sizeof(TT) == 2 && sizeof(TQ) == 2) ? (kLogits ? 5 : 6) : 4;
 }
 
 // One CTA's share of a unit: chunk `rank` of the unit's target row and N drafter rows, streamed
@@ -523,7 +524,7 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
 }
 
 template <typename TT, typename TQ, bool kLogits, int NMAX, bool kSlices = false>
-__global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX>()))
+__global__ void __launch_bounds__(kThreads, (stats_occupancy<TT, TQ, NMAX, kLogits>()))
     stats_kernel(const SplitParams P) {
   // every CTA of this grid is resident or done once all passed this point: kernel B (launched
   // as a programmatic dependent) may then be scheduled into the tail wave (it waits per unit)
