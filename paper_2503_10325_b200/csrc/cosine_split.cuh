@@ -356,7 +356,31 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
     }
   };
 
-  if constexpr (kSlices) {
+  if (kRowU4 && Nd == 0) {
+    // a target row alone (the bonus position, a tree leaf): four groups per thread in flight,
+    // as many bytes as the (1 + N)-row units keep in flight (one group per row) — with one load
+    // per step such a CTA held its slot ~75% as long for ~20% of the bytes.  Same per-thread
+    // order of the groups as the loop below.
+    int64_t gi = gb + tid;
+    for (; gi + 3 * kThreads < gfe; gi += 4 * kThreads) {
+      Group<TT> t4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t4[u].load(trow, gi + u * kThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float f[8];
+        t4[u].unpack(f);
+        t_step(f, gi + u * kThreads);
+      }
+    }
+    for (; gi < gfe; gi += kThreads) {
+      Group<TT> tv;
+      tv.load(trow, gi);
+      float f[8];
+      tv.unpack(f);
+      t_step(f, gi);
+    }
+  } else if constexpr (kSlices) {
     // the same stream in warp-contiguous slices: warp w covers slices s = w, w + 8, ... of
     // kSliceGroups consecutive groups (two coalesced 32-group steps each), whose drafter sums it
     // writes (a transposed warp reduction: one shuffle tree for all N sums)
@@ -397,30 +421,6 @@ __device__ __forceinline__ int64_t stats_body(const SplitParams& P, int64_t unit
       dacc += tot;
       const int idx = lane / (32 / NMAX);
       if (lane % (32 / NMAX) == 0 && idx < Nd) sl[((s0 - gb) / kSliceGroups) * N + idx] = tot;
-    }
-  } else if (kRowU4 && Nd == 0) {
-    // a target row alone (the bonus position, a tree leaf): four groups per thread in flight,
-    // as many bytes as the (1 + N)-row units keep in flight (one group per row) — with one load
-    // per step such a CTA held its slot ~75% as long for ~20% of the bytes.  Same per-thread
-    // order of the groups as the loop below.
-    int64_t gi = gb + tid;
-    for (; gi + 3 * kThreads < gfe; gi += 4 * kThreads) {
-      Group<TT> t4[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) t4[u].load(trow, gi + u * kThreads);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float f[8];
-        t4[u].unpack(f);
-        t_step(f, gi + u * kThreads);
-      }
-    }
-    for (; gi < gfe; gi += kThreads) {
-      Group<TT> tv;
-      tv.load(trow, gi);
-      float f[8];
-      tv.unpack(f);
-      t_step(f, gi);
     }
   } else {
     for (int64_t gi = gb + tid; gi < gfe; gi += kThreads) {
